@@ -1,0 +1,382 @@
+/*
+ * lfe_oracle.c -- plain, slow, obviously-correct CPU oracle for the hot path of
+ * arXiv 1304.3992 ("GPU Accelerated Automated Feature Extraction from Satellite
+ * Images"): two LoG masks -> zero crossings -> standard-deviation gate -> OR
+ * merge -> optional hybrid median.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  The
+ * product path (paper_1304_3992_b200/) never links, loads or calls it, and this
+ * file shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Every stage is materialised as a whole image, in the paper's order
+ * (Sec. 4.1), with each stage padding its OWN input by
+ * replication ("padded with 2 rows/columns", "padded with 1 row/column"; fill
+ * value unstated -> DESIGN.md reading R5).  Arithmetic: double for Eq. 1,
+ * int64 for every integer stage.  OpenMP only parallelises the outer row loop
+ * of each stage; it changes no arithmetic.
+ *
+ * Readings of the paper are cited as R<n>.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define LFO_PI 3.14159265358979323846
+
+/* ------------------------------------------------------------------ */
+/* threads                                                             */
+/* ------------------------------------------------------------------ */
+void lfo_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+int lfo_get_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* ------------------------------------------------------------------ */
+/* O1 masks -- Eq. 1, PAPER.md:48-50 (Sec. 3.1); 5x5 masks PAPER.md:94  */
+/* ------------------------------------------------------------------ */
+
+/* Eq. 1 sampled at the integer offsets (x, y), |x|,|y| <= (n-1)/2 (R2).
+ * out is n*n, row-major over y then x.  Returns 0, or -1 on bad args. */
+int lfo_log_raw(double sigma, int n, double *out)
+{
+    if (!(sigma > 0.0) || n < 1 || (n % 2) == 0) return -1;
+    int R = n / 2;
+    for (int y = -R; y <= R; ++y)
+        for (int x = -R; x <= R; ++x) {
+            double r2 = (double)(x * x + y * y);
+            double s2 = sigma * sigma;
+            double v = -1.0 / (LFO_PI * s2 * s2) * (1.0 - r2 / (2.0 * s2)) * exp(-r2 / (2.0 * s2));
+            out[(y + R) * n + (x + R)] = v;
+        }
+    return 0;
+}
+
+/* DC correction (R2): subtract the mean coefficient so the mask sums to zero
+ * -- the paper calls LoG "equivalent to band-pass filter". */
+int lfo_log_dc(double sigma, int n, double *out)
+{
+    if (lfo_log_raw(sigma, n, out) != 0) return -1;
+    double sum = 0.0;
+    for (int i = 0; i < n * n; ++i) sum += out[i];
+    double mean = sum / (double)(n * n);
+    for (int i = 0; i < n * n; ++i) out[i] -= mean;
+    return 0;
+}
+
+/* Integer quantisation (R3): c = |L_dc(0,0)|, M = 2^b - 1.  For F = 16 down
+ * to 0: q = round-half-away(L_dc / c * 2^F) off-centre, q(0,0) = -sum(others);
+ * accept the first F with M * sum|q| < 2^24 (so every LoG response is exact in
+ * int32 and in fp32).  Returns 0 or -1. */
+int lfo_mask_int(double sigma, int n, int bit_depth, int32_t *q, int *F_out)
+{
+    if (n < 1 || (n % 2) == 0 || n > 15 || bit_depth < 1 || bit_depth > 16) return -1;
+    double L[15 * 15];
+    if (lfo_log_dc(sigma, n, L) != 0) return -1;
+    int R = n / 2;
+    int centre = R * n + R;
+    double c = fabs(L[centre]);
+    int64_t M = ((int64_t)1 << bit_depth) - 1;
+    for (int F = 16; F >= 0; --F) {
+        double scale = ldexp(1.0, F);
+        int64_t others = 0, abssum = 0;
+        for (int i = 0; i < n * n; ++i) {
+            if (i == centre) continue;
+            int64_t v = (c > 0.0) ? (int64_t)round(L[i] / c * scale) : 0;
+            q[i] = (int32_t)v;
+            others += v;
+            abssum += v < 0 ? -v : v;
+        }
+        q[centre] = (int32_t)(-others);
+        abssum += others < 0 ? -others : others;
+        if (M * abssum < ((int64_t)1 << 24)) {
+            *F_out = F;
+            return 0;
+        }
+    }
+    return -1;
+}
+
+/* ZC gap threshold in integer response units (R9): t = ceil(thr * 2^F * M). */
+int64_t lfo_zc_threshold_int(double thr, int F, int bit_depth)
+{
+    double M = (double)(((int64_t)1 << bit_depth) - 1);
+    return (int64_t)ceil(thr * ldexp(1.0, F) * M);
+}
+
+/* ------------------------------------------------------------------ */
+/* O2 LoG response: "The LoG mask was applied on each pixel */
+/* with its 5x5 neighborhood" on the input padded by replication.      */
+/* ------------------------------------------------------------------ */
+void lfo_log_response(const uint16_t *I, int W, int H, const int32_t *q, int n, int64_t *r)
+{
+    int R = n / 2;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            int64_t acc = 0;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx) {
+                    int yy = clampi(y + dy, 0, H - 1), xx = clampi(x + dx, 0, W - 1);
+                    acc += (int64_t)q[(dy + R) * n + (dx + R)] * (int64_t)I[(size_t)yy * W + xx];
+                }
+            r[(size_t)y * W + x] = acc;
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* O3 zero crossing, PAPER.md:60 (Sec. 3.2), 86, 94 -- rule R* (R6-R9).  */
+/* ------------------------------------------------------------------ */
+static inline int sgn64(int64_t v) { return (v > 0) - (v < 0); }
+
+void lfo_zero_crossing(const int64_t *r, int W, int H, int64_t t, uint8_t *Z)
+{
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            /* the four neighbours up, down, left, right of the LoG image padded
+             * with 1 row/column by replication */
+            int64_t nb[4];
+            nb[0] = r[(size_t)clampi(y - 1, 0, H - 1) * W + x];
+            nb[1] = r[(size_t)clampi(y + 1, 0, H - 1) * W + x];
+            nb[2] = r[(size_t)y * W + clampi(x - 1, 0, W - 1)];
+            nb[3] = r[(size_t)y * W + clampi(x + 1, 0, W - 1)];
+            int64_t rp = r[(size_t)y * W + x];
+            int z = 0;
+            if (rp != 0) {
+                /* opposite-sign neighbours O(p); p qualifies if it has the
+                 * smallest absolute value compared to all of them (R7, ties
+                 * included R8), and the strongest opposite pair passes the gap
+                 * threshold (R9). */
+                int any = 0, smallest = 1;
+                int64_t gap = 0;
+                int64_t ap = rp < 0 ? -rp : rp;
+                for (int k = 0; k < 4; ++k) {
+                    if (sgn64(nb[k]) == -sgn64(rp)) {
+                        int64_t an = nb[k] < 0 ? -nb[k] : nb[k];
+                        any = 1;
+                        if (!(ap <= an)) smallest = 0;
+                        if (ap + an > gap) gap = ap + an;
+                    }
+                }
+                z = any && smallest && gap >= t;
+            } else {
+                /* a pixel exactly at zero: "the positive maximum and the negative
+                 * minimum" of its neighbours, R6 */
+                int64_t mx = nb[0], mn = nb[0];
+                for (int k = 1; k < 4; ++k) {
+                    if (nb[k] > mx) mx = nb[k];
+                    if (nb[k] < mn) mn = nb[k];
+                }
+                z = mx > 0 && mn < 0 && (mx - mn) >= t;
+            }
+            Z[(size_t)y * W + x] = (uint8_t)z;
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* O4 standard-deviation gate, Eq. 2 (Sec. 3.3) and the */
+/* 5x5 / 3x3 procedure of PAPER.md:94 (R10-R13).                        */
+/* ------------------------------------------------------------------ */
+
+/* Eq. 2 literally: unbiased sample standard deviation of n values. */
+double lfo_sample_std(const double *a, int n)
+{
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) m += a[i];
+    m /= (double)n;
+    double ss = 0.0;
+    for (int i = 0; i < n; ++i) ss += (a[i] - m) * (a[i] - m);
+    return sqrt(ss / (double)(n - 1));
+}
+
+/* s > T decided exactly (R11): Lambda*S2 - S1^2 = Lambda*(Lambda-1)*s^2 is an
+ * exact integer; it is compared in double against Lambda*(Lambda-1)*T*T. */
+static inline int std_exceeds(int64_t S1, int64_t S2, int Lambda, double T)
+{
+    int64_t num = (int64_t)Lambda * S2 - S1 * S1;
+    double rhs = (double)(Lambda * (Lambda - 1)) * T * T;
+    return (double)num > rhs;
+}
+
+/* src is the image the deviation is computed on (the binary ZC image, R10
+ * default, or the intensity image); both are replicate-padded (PAPER.md:94
+ * "padded with 2 rows/columns").  keep = Z & s_w > T & (T3 < 0 | s_3 > T3). */
+void lfo_std_gate(const uint16_t *src, const uint8_t *Z, int W, int H, int w, double T, double T3,
+                  uint8_t *keep)
+{
+    int R = w / 2;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t p = (size_t)y * W + x;
+            if (!Z[p]) { keep[p] = 0; continue; }
+            int64_t S1 = 0, S2 = 0;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx) {
+                    int64_t a = src[(size_t)clampi(y + dy, 0, H - 1) * W + clampi(x + dx, 0, W - 1)];
+                    S1 += a;
+                    S2 += a * a;
+                }
+            int pass = std_exceeds(S1, S2, w * w, T);
+            if (pass && T3 >= 0.0) {
+                int64_t s1 = 0, s2 = 0;
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        int64_t a = src[(size_t)clampi(y + dy, 0, H - 1) * W + clampi(x + dx, 0, W - 1)];
+                        s1 += a;
+                        s2 += a * a;
+                    }
+                pass = std_exceeds(s1, s2, 9, T3);
+            }
+            keep[p] = (uint8_t)pass;
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* O5 merge, "combined together" (R14, R15)                 */
+/* ------------------------------------------------------------------ */
+void lfo_merge(const uint8_t *k0, const uint8_t *k1, const uint16_t *I, int W, int H, int out_mode,
+               uint16_t *E)
+{
+    size_t N = (size_t)W * H;
+    for (size_t p = 0; p < N; ++p) {
+        int m = k0[p] | k1[p];
+        E[p] = m ? (out_mode == 1 ? 255 : I[p]) : 0;
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* O6 hybrid median, PAPER.md:76 (Sec. 3.4), R16-R17                    */
+/* ------------------------------------------------------------------ */
+static int cmp_u16(const void *a, const void *b)
+{
+    int x = *(const uint16_t *)a, y = *(const uint16_t *)b;
+    return (x > y) - (x < y);
+}
+
+void lfo_hybrid_median(const uint16_t *E, int W, int H, int m, uint16_t *out)
+{
+    int R = m / 2;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            uint16_t P[64], X[64];
+            int np = 0, nx = 0;
+#define AT(yy, xx) E[(size_t)clampi((yy), 0, H - 1) * W + clampi((xx), 0, W - 1)]
+            P[np++] = AT(y, x);
+            X[nx++] = AT(y, x);
+            for (int d = 1; d <= R; ++d) {
+                /* "parallel ... to the edges": the + shaped subgroup */
+                P[np++] = AT(y, x - d);
+                P[np++] = AT(y, x + d);
+                P[np++] = AT(y - d, x);
+                P[np++] = AT(y + d, x);
+                /* "at 45 degrees": the x shaped subgroup */
+                X[nx++] = AT(y - d, x - d);
+                X[nx++] = AT(y - d, x + d);
+                X[nx++] = AT(y + d, x - d);
+                X[nx++] = AT(y + d, x + d);
+            }
+            qsort(P, np, sizeof(uint16_t), cmp_u16);
+            qsort(X, nx, sizeof(uint16_t), cmp_u16);
+            uint16_t tri[3] = {P[np / 2], X[nx / 2], AT(y, x)};
+#undef AT
+            qsort(tri, 3, sizeof(uint16_t), cmp_u16);
+            out[(size_t)y * W + x] = tri[1];
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* Whole pipeline (Fig. 1 / Fig. 2 flow)              */
+/* ------------------------------------------------------------------ */
+typedef struct lfo_params {
+    int32_t bit_depth;
+    int32_t sigma_is_variance;
+    double sigma[2];
+    int32_t log_size[2];
+    double zc_threshold[2];
+    int32_t std_source;   /* 0 = ZC image (R10), 1 = intensity */
+    int32_t std_window;
+    double std_threshold[2];
+    double std3_threshold[2];
+    int32_t hybrid_median;
+    int32_t median_window;
+    int32_t out_mode;     /* 0 = extract intensities, 1 = 0/255 mask */
+    int32_t pad_;
+} lfo_params;
+
+/* Optional intermediates (any may be NULL): r0/r1 int64[W*H], z0/z1, k0/k1
+ * uint8[W*H], E uint16[W*H].  out is uint16[W*H].  Returns 0, -1 bad params,
+ * -2 out of memory, -3 a pixel exceeds 2^b - 1. */
+int lfo_run(const lfo_params *p, const uint16_t *I, int W, int H, uint16_t *out, int64_t *r0o,
+            int64_t *r1o, uint8_t *z0o, uint8_t *z1o, uint8_t *k0o, uint8_t *k1o, uint16_t *Eo)
+{
+    if (W < 1 || H < 1) return -1;
+    size_t N = (size_t)W * H;
+    uint16_t maxv = (uint16_t)(((int32_t)1 << p->bit_depth) - 1);
+    for (size_t i = 0; i < N; ++i)
+        if (I[i] > maxv) return -3;
+    int64_t *r = (int64_t *)malloc(N * sizeof(int64_t));
+    uint8_t *Z = (uint8_t *)malloc(N), *K[2];
+    uint16_t *src = NULL, *E = (uint16_t *)malloc(N * sizeof(uint16_t));
+    K[0] = (uint8_t *)malloc(N);
+    K[1] = (uint8_t *)malloc(N);
+    if (p->std_source == 0) src = (uint16_t *)malloc(N * sizeof(uint16_t));
+    if (!r || !Z || !K[0] || !K[1] || !E || (p->std_source == 0 && !src)) {
+        free(r); free(Z); free(K[0]); free(K[1]); free(E); free(src);
+        return -2;
+    }
+    int rc = 0;
+    for (int j = 0; j < 2 && rc == 0; ++j) {
+        int n = p->log_size[j];
+        int32_t q[15 * 15];
+        int F;
+        double s = p->sigma_is_variance ? sqrt(p->sigma[j]) : p->sigma[j];
+        if (lfo_mask_int(s, n, p->bit_depth, q, &F) != 0) { rc = -1; break; }
+        lfo_log_response(I, W, H, q, n, r);
+        int64_t t = lfo_zc_threshold_int(p->zc_threshold[j], F, p->bit_depth);
+        lfo_zero_crossing(r, W, H, t, Z);
+        if (j == 0 && r0o) memcpy(r0o, r, N * sizeof(int64_t));
+        if (j == 1 && r1o) memcpy(r1o, r, N * sizeof(int64_t));
+        if (j == 0 && z0o) memcpy(z0o, Z, N);
+        if (j == 1 && z1o) memcpy(z1o, Z, N);
+        const uint16_t *s_img = I;
+        if (p->std_source == 0) {
+            for (size_t i = 0; i < N; ++i) src[i] = Z[i];
+            s_img = src;
+        }
+        lfo_std_gate(s_img, Z, W, H, p->std_window, p->std_threshold[j], p->std3_threshold[j], K[j]);
+    }
+    if (rc == 0) {
+        if (k0o) memcpy(k0o, K[0], N);
+        if (k1o) memcpy(k1o, K[1], N);
+        lfo_merge(K[0], K[1], I, W, H, p->out_mode, E);
+        if (Eo) memcpy(Eo, E, N * sizeof(uint16_t));
+        if (p->hybrid_median)
+            lfo_hybrid_median(E, W, H, p->median_window, out);
+        else
+            memcpy(out, E, N * sizeof(uint16_t));
+    }
+    free(r); free(Z); free(K[0]); free(K[1]); free(E); free(src);
+    return rc;
+}

@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the dual-LoG feature-extraction hot path (arXiv 1304.3992) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lfe|reference]
+
+A step = one pass of the whole hot path (LoG x2 -> zero crossing -> std gate ->
+OR merge -> hybrid median) over the c3 scene: 12000 x 12000 uint16 (10-bit),
+Cartosat-1-like synthetic PAN, resident in HBM.  At N > 1 (torchrun, one
+process per GPU) the scene is split into N row strips with an NCCL halo
+exchange of 7 boundary rows per neighbour (strong scaling: the scene is fixed).
+Rank 0 prints one JSON line.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixels/s per scene at 1/2/4/8 B200; achieved HBM GB/s fraction of peak"
+UNIT = "Mpx/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["lfe", "reference"], default="lfe")
+    ap.add_argument("--kernel", choices=["auto", "staged", "fused"], default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--size", type=int, default=12000, help="scene side (default: c3's 12000)")
+    ap.add_argument("--tile", type=str, default="", help="TWxTH override (tuning only)")
+    return ap.parse_args()
+
+
+def workload_params():
+    from paper_1304_3992_b200 import lfe
+    # SURVEY.md 8(c) defaults for benchmark scenes: ZC gap 0.02 (normalised),
+    # std source = ZC image, 5x5 window, T = 0.3, hybrid median on, extract.
+    return lfe.Params(bit_depth=10, sigma=(0.5, 20.0), log_size=(5, 5), zc_threshold=(0.02, 0.02),
+                      std_source=lfe.LFE_STD_ZC, std_window=5, std_threshold=(0.3, 0.3),
+                      std3_threshold=(-1.0, -1.0), hybrid_median=True, median_window=5,
+                      out_mode=lfe.LFE_OUT_EXTRACT)
+
+
+def config_dict(size, world, p):
+    return {
+        "workload": f"c3: {size}x{size} uint16 (10-bit) synthetic Cartosat-1-like PAN scene, "
+                    "dual LoG (sigma 0.5, 20; 5x5) + ZC (gap 0.02) + 5x5 std gate (T=0.3) + OR + 5x5 hybrid median, extract",
+        "width": size, "height": size, "bit_depth": 10, "bands": 1,
+        "parallelism": f"row strips x{world}, 7-row NCCL halo exchange" if world > 1 else "single GPU",
+        "l2": "inputs larger than L2 (288 MB in + 288 MB out per step > 126 MB L2); no flush",
+        "params": {"sigma": list(p.sigma), "log_size": list(p.log_size), "zc_threshold": list(p.zc_threshold),
+                   "std_source": "zc", "std_window": p.std_window, "std_threshold": list(p.std_threshold),
+                   "hybrid_median": bool(p.hybrid_median), "median_window": p.median_window, "out_mode": "extract"},
+    }
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self._proc is None:
+            return None
+        time.sleep(0.25)
+        self._proc.terminate()
+        try:
+            self._proc.wait(2)
+        except Exception:
+            self._proc.kill()
+        self._t.join(1)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 8:
+                for n, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "lfe" else "gloo")
+    return world, rank, local
+
+
+def cpu_baseline(img, p, rows=2048):
+    """The oracle as it stands, on the host cores, on a bounded sample of the
+    same workload: `rows` full-width rows (+7 halo rows each side)."""
+    import oracle
+    H = img.shape[0]
+    a = H // 2 - rows // 2
+    lo, hi = max(0, a - 7), min(H, a + rows + 7)
+    band = img[lo:hi].copy()
+    op = oracle.Params(bit_depth=p.bit_depth, sigma=p.sigma, log_size=p.log_size, zc_threshold=p.zc_threshold,
+                       std_source=p.std_source, std_window=p.std_window, std_threshold=p.std_threshold,
+                       std3_threshold=p.std3_threshold, hybrid_median=p.hybrid_median,
+                       median_window=p.median_window, out_mode=p.out_mode)
+    t0 = time.perf_counter()
+    oracle.run(band, op)
+    dt = time.perf_counter() - t0
+    px = rows * img.shape[1]  # output rows counted (halo rows are overhead)
+    return {"value": round(px / dt / 1e6, 3), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"{rows} x {img.shape[1]} rows of the c3 scene (+7 halo rows each side), one run, "
+                      f"{dt:.2f} s, plain C oracle -O2 OpenMP over rows"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle, as it stands, on the same config."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_1304_3992_b200 import scenes
+    p = workload_params()
+    img = scenes.scene_c3(size=args.size)
+    rows = 512
+    H, W = img.shape
+    op = oracle.Params(bit_depth=p.bit_depth, sigma=p.sigma, log_size=p.log_size, zc_threshold=p.zc_threshold,
+                       std_source=p.std_source, std_window=p.std_window, std_threshold=p.std_threshold,
+                       std3_threshold=p.std3_threshold, hybrid_median=p.hybrid_median,
+                       median_window=p.median_window, out_mode=p.out_mode)
+    times = []
+    for i in range(args.warmup + args.steps):
+        a = (H // 2 - rows // 2 + 977 * i) % (H - rows)
+        band = np.ascontiguousarray(img[max(0, a - 7):min(H, a + rows + 7)])
+        t0 = time.perf_counter()
+        oracle.run(band, op)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = rows * W * len(times) / tot / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": config_dict(args.size, world, p),
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+                             "sample": f"each step: {rows} x {W} rows of c3 (+7 halo rows), plain C oracle -O2 OpenMP"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_1304_3992_b200 import lfe, scenes
+    from paper_1304_3992_b200.shard import StripShard
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p = workload_params()
+    size = args.size
+    img = scenes.scene_c3(size=size)                      # host, numpy uint16
+    H, W = img.shape
+    ctx = lfe.Context(p)
+    ctx.set_option(lfe.LFE_OPT_KERNEL, {"auto": 0, "staged": 1, "fused": 2}[args.kernel])
+    if args.tile:
+        tw, th = (int(v) for v in args.tile.split("x"))
+        ctx.set_option(lfe.LFE_OPT_TILE_W, tw)
+        ctx.set_option(lfe.LFE_OPT_TILE_H, th)
+    halo = ctx.halo
+    shard = StripShard(H, W, rank, world, halo)
+    buf = shard.alloc(torch.uint16, dev)
+    shard.load_owned(img)
+    out = torch.empty((shard.rows, W), dtype=torch.uint16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    bpitch, opitch = buf.stride(0) * 2, out.stride(0) * 2
+    kernel_events = []
+
+    def launch(band, record):
+        s, n, ha, hb, flags, _ = band
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        lfe.lfe_extract_rows(ctx.handle, buf.data_ptr() + (shard.ha + s) * bpitch, bpitch, W, n, ha, hb, flags,
+                             out.data_ptr() + s * opitch, opitch, sptr)
+        if record:
+            e1.record(stream)
+            kernel_events.append((e0, e1, n))
+
+    bands = shard.bands()
+
+    def step(record=False):
+        works = shard.exchange() if world > 1 else []
+        for b in bands:
+            if b[5]:
+                continue
+            launch(b, record)
+        for w in works:
+            w.wait()
+        for b in bands:
+            if b[5]:
+                launch(b, record)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    ctx.check()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launches
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    launches = ctx.launches - launches0
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    ctx.check()
+
+    # dominant kernel: the full-strip launch (interior band); average duration
+    main_n = max(n for _, _, n in kernel_events)
+    kms = [a.elapsed_time(b) for a, b, n in kernel_events if n == main_n]
+    k_ms = sum(kms) / len(kms)
+    px_launch = main_n * W
+    bytes_launch = px_launch * (2 + 2)  # input read once + output written once (u16 -> u16)
+    achieved = bytes_launch / (k_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+
+    # end-to-end through the public API with host buffers (pinned), rank-local strip
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.from_numpy(np.ascontiguousarray(img[shard.a:shard.b])).pin_memory()
+        h_out = torch.empty((shard.rows, W), dtype=torch.uint16).pin_memory()
+        K = max(1, min(args.steps, 10))
+        strip_rows = 1024
+        ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, strip_rows)
+        ctx.extract_host_ptr(h_in.data_ptr(), W * 2, W, shard.rows, h_out.data_ptr(), W * 2)  # warm-up
+        if world > 1:
+            dist.barrier()
+        tw0 = time.perf_counter()
+        for _ in range(K):
+            ctx.extract_host_ptr(h_in.data_ptr(), W * 2, W, shard.rows, h_out.data_ptr(), W * 2)
+        e2e_s = time.perf_counter() - tw0
+        if world > 1:
+            tt = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        nst = (shard.rows + strip_rows - 1) // strip_rows
+        h2d_rows = sum(min(shard.rows, (i + 1) * strip_rows + halo) - max(0, i * strip_rows - halo) for i in range(nst))
+        e2e = {"value": round(H * W * K / e2e_s / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d_rows * W * 2 * world), "d2h_bytes_per_step": int(H * W * 2),
+               "how": "lfe_extract_host on pinned host buffers: strip-pipelined H2D -> kernel -> D2H on 3 streams, "
+                      f"{strip_rows}-row strips, wall clock of {K} synchronous calls (max over ranks)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(img, p)
+
+    if rank == 0:
+        value = H * W * args.steps / (ms * 1e-3) / 1e6
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": config_dict(size, world, p),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "lfe fused/staged stencil kernel (dominant; one launch per step at N=1)",
+                         "kernel_ms": round(k_ms, 4), "algorithmic_bytes_per_launch": bytes_launch,
+                         "bytes_per_px": 4, "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        tr = ncu_traffic()
+        if tr:
+            line["roofline"]["traffic"] = tr.get("bytes_per_launch")
+            line["roofline"]["traffic_source"] = tr.get("source")
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/*
+ * lfe.h -- C ABI of liblfe, the B200-native (sm_100a) hot path of arXiv
+ * 1304.3992, "GPU Accelerated Automated Feature Extraction from Satellite
+ * Images": two Laplacian-of-Gaussian masks -> zero crossings -> standard-
+ * deviation gate -> OR merge -> optional hybrid median.
+ *
+ * Paper passages (PAPER.md line, section):
+ *   Eq. 1 LoG mask ............... :50  (Sec. 3.1)
+ *   zero-crossing rule ........... :60  (Sec. 3.2), :86, :94
+ *   Eq. 2 sample std ............. :68  (Sec. 3.3), :88, :94
+ *   hybrid median ................ :76  (Sec. 3.4)
+ *   urban pipeline / padding ..... :94  (Sec. 4.1, Fig. 1)
+ *   water pipeline (median) ...... :102 (Sec. 4.2, Fig. 2)
+ * Readings of silent or ambiguous points are R1..R20 in DESIGN.md.
+ *
+ * Conventions for every call:
+ *   - No C++ exception crosses this ABI; every call returns an lfe_status.
+ *   - Images are row-major, top-left origin, pitched: row y starts at
+ *     base + y * pitch_bytes.  Storage type is uint8 when bit_depth <= 8,
+ *     else uint16 (little endian).  Output storage: the input type for
+ *     LFE_OUT_EXTRACT, uint8 for LFE_OUT_MASK.
+ *   - The caller owns every image buffer and must keep it alive until the
+ *     work enqueued on `cuda_stream` completes.  liblfe never frees or
+ *     retains caller pointers.  A ctx owns only its masks, a device error
+ *     flag and (for lfe_extract_host) its staging buffers.
+ *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - A ctx is used by one host thread at a time; distinct ctxs are
+ *     independent.  A ctx is bound to the CUDA device current at create.
+ *   - There is no CPU fallback: without an sm_100 device every compute entry
+ *     point returns LFE_ENODEV.
+ */
+#ifndef LFE_H
+#define LFE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFE_ABI_VERSION 1
+
+typedef enum lfe_status {
+    LFE_OK = 0,
+    LFE_EINVAL = 1,        /* bad argument (synchronous; nothing enqueued)          */
+    LFE_EUNSUPPORTED = 2,  /* valid by the paper but not compiled (window > 7 ...)   */
+    LFE_ENOMEM = 3,        /* host or device allocation failed                        */
+    LFE_ENODEV = 4,        /* no sm_100 CUDA device current                           */
+    LFE_ECUDA = 5,         /* a CUDA runtime/driver call failed                       */
+    LFE_ERANGE = 6         /* an input pixel exceeded 2^bit_depth - 1 (asynchronous)  */
+} lfe_status;
+
+/* Which image the Eq. 2 deviation is computed on (reading R10). */
+enum { LFE_STD_ZC = 0, LFE_STD_INTENSITY = 1 };
+/* What the merged image holds (reading R15). */
+enum { LFE_OUT_EXTRACT = 0, LFE_OUT_MASK = 1 };
+/* lfe_extract_rows: which strip sides are true image edges (clamped). */
+enum { LFE_TOP_IS_EDGE = 1u, LFE_BOTTOM_IS_EDGE = 2u };
+/* lfe_set_option keys (test/tuning only; results never depend on them). */
+enum { LFE_OPT_KERNEL = 1, LFE_OPT_TILE_W = 2, LFE_OPT_TILE_H = 3, LFE_OPT_HOST_STRIP_ROWS = 4 };
+/* LFE_OPT_KERNEL values. */
+enum { LFE_KERNEL_AUTO = 0, LFE_KERNEL_STAGED = 1, LFE_KERNEL_FUSED = 2 };
+
+/* The problem as the paper states it.  Index 0/1 = the two
+ * LoG branches (neutral labels, reading R18).  112 bytes, natural alignment. */
+typedef struct lfe_params {
+    uint32_t abi_size;          /* = sizeof(lfe_params)                                  */
+    int32_t bit_depth;          /* 1..16                                                 */
+    double sigma[2];            /* Eq. 1 sigma (> 0, finite)                              */
+    int32_t sigma_is_variance;  /* 0: sigma used directly (R1); 1: sigma = sqrt(value)    */
+    int32_t log_size[2];        /* odd mask side: 3, 5 or 7 (paper: 5)       */
+    int32_t reserved0;          /* must be 0                                             */
+    double zc_threshold[2];     /* >= 0; gap threshold normalised by 2^F * (2^b - 1) (R9) */
+    int32_t std_source;         /* LFE_STD_ZC (default, R10) or LFE_STD_INTENSITY         */
+    int32_t std_window;         /* odd 3, 5 or 7 (paper: 5)                               */
+    double std_threshold[2];    /* T >= 0: keep iff s > T (Eq. 2, strict, R11)            */
+    double std3_threshold[2];   /* < 0 disables the 3x3 re-check (R12); else s3 > T3 too  */
+    int32_t hybrid_median;      /* 0 / 1                              */
+    int32_t median_window;      /* odd 3, 5 or 7 (paper: 5x5)                             */
+    int32_t out_mode;           /* LFE_OUT_EXTRACT (default) or LFE_OUT_MASK              */
+    int32_t reserved1;          /* must be 0                                             */
+} lfe_params;
+
+typedef struct lfe_ctx lfe_ctx;
+
+/* Defaults of DESIGN.md: sigma (0.5, 20) sigma-direct, 5x5 masks, ZC threshold
+ * 0, std source ZC, 5x5 window, T = 0.3, re-check off, hybrid median on (5x5),
+ * extract mode, bit_depth 8. */
+void lfe_params_default(lfe_params *p);
+
+/* Validates p and synthesises both integer masks (Eq. 1 -> DC correction ->
+ * quantisation, R2/R3).  Binds the current CUDA device.  On success *out is a
+ * new ctx.  Errors: EINVAL (p NULL, abi_size wrong, any field out of range --
+ * the message is in lfe_last_message()), EUNSUPPORTED, ENODEV (no sm_100
+ * device), ENOMEM. */
+lfe_status lfe_create(const lfe_params *p, lfe_ctx **out);
+
+/* Whole-image extraction on the device (the Fig. 1 / Fig. 2 pipeline).
+ * d_in/d_out: device pointers to W x H pitched images; pitches must be >= the
+ * row bytes and multiples of the element size; in and out must not overlap.
+ * 16-byte aligned bases and pitches select the fast fused kernel; anything
+ * else runs the general staged kernel (same result).  Enqueued on cuda_stream; returns immediately.  Every
+ * stage pads its own input by edge replication at the image border (R5).
+ * Errors (synchronous): EINVAL, ENODEV, ECUDA (launch failure).  An input
+ * pixel > 2^b - 1 sets the ctx's sticky ERANGE flag (see
+ * lfe_last_async_error); the output is then unspecified. */
+lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
+                       int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
+
+/* One row strip of a larger image (multi-GPU sharding, streaming).  d_in_row0
+ * points at the first OWNED row; `halo_above` rows above it and `halo_below`
+ * rows below the last owned row are readable.  If a side's edge flag is set,
+ * its outermost readable row (row -halo_above, resp. rows-1+halo_below) is the
+ * true image edge and every stage clamps there (any halo >= 0); if the flag is
+ * clear the halo must be >= lfe_halo(c) and exactly lfe_halo(c) rows are read.
+ * Either way the result equals the whole-image result bit for bit.  Writes
+ * `rows` output rows starting at d_out_row0.  Errors as lfe_extract. */
+lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_bytes,
+                            int32_t width, int32_t rows, int32_t halo_above, int32_t halo_below,
+                            uint32_t edge_flags, void *d_out_row0, int64_t out_pitch_bytes,
+                            void *cuda_stream);
+
+/* End-to-end call on HOST buffers (the paper's H2D -> kernel -> D2H flow,
+ * PAPER.md:150, Table 6): copies the image in row strips to device staging
+ * buffers owned by the ctx, runs lfe_extract_rows per strip and copies the
+ * result back, overlapping the three on separate streams.  Synchronous:
+ * returns when h_out is complete.  Pinned (page-locked) host buffers give
+ * full PCIe bandwidth; pageable ones work but are slower.  Errors: EINVAL,
+ * ENOMEM, ECUDA, ERANGE (checked at the end of the call). */
+lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch_bytes, int32_t width,
+                            int32_t height, void *h_out, int64_t out_pitch_bytes);
+
+/* Rows of real input needed above/below a strip for a bit-exact result:
+ * LoG radius + 1 (ZC) + std radius + median radius (0 if off). */
+int32_t lfe_halo(const lfe_ctx *c);
+
+/* The integer mask of branch 0/1 (R3): coeffs[n*n] row-major (caller buffer
+ * of >= 49 int32), *n the side, *shift_F the quantisation shift and
+ * *zc_t the gap threshold in integer response units.  Any out pointer may be
+ * NULL.  Errors: EINVAL. */
+lfe_status lfe_get_mask(const lfe_ctx *c, int32_t branch, int32_t *coeffs, int32_t *n,
+                        int32_t *shift_F, int64_t *zc_t);
+
+/* Synchronises cuda_stream, then returns and clears the sticky asynchronous
+ * error: ERANGE if an input pixel exceeded 2^b - 1 since the last call,
+ * ECUDA if the stream reports a CUDA error, else OK. */
+lfe_status lfe_last_async_error(lfe_ctx *c, void *cuda_stream);
+
+/* Tuning/test knobs (LFE_OPT_*).  Results never depend on them (tile-shape
+ * invariance is tested).  Errors: EINVAL for an unknown key or bad value. */
+lfe_status lfe_set_option(lfe_ctx *c, int32_t key, int64_t value);
+
+/* Number of kernel launches the ctx has enqueued so far (instrumentation). */
+int64_t lfe_launch_count(const lfe_ctx *c);
+
+/* Frees the ctx (NULL is a no-op).  Does not synchronise streams. */
+void lfe_destroy(lfe_ctx *c);
+
+/* Static description of a status code. */
+const char *lfe_strerror(lfe_status s);
+
+/* Human-readable detail of the last error raised on this host thread. */
+const char *lfe_last_message(void);
+
+/* LFE_ABI_VERSION of the loaded library. */
+int32_t lfe_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFE_H */

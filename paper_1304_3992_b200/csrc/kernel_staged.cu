@@ -1,0 +1,288 @@
+// kernel_staged.cu -- the general ("staged") fused kernel of liblfe.
+//
+// One CTA produces one TW x TH output tile.  It stages the input tile plus the
+// combined halo (LoG radius + 1 + std radius + median radius, north_star) in
+// shared memory and then evaluates the paper's stages one after the other on
+// shrinking shared-memory regions, never touching HBM in between:
+//
+//   I  (tile + h)      -> LoG x 2          PAPER.md:94, Eq. 1 (:50)
+//   r  (tile + h - RL) -> zero crossing x2 PAPER.md:60 (Sec. 3.2), rule R*
+//   Z  (tile + Rs + Rm)-> std gate x 2     PAPER.md:64-72 (Eq. 2), :94
+//                      -> OR merge         PAPER.md:94 "combined together"
+//   E  (tile + Rm)     -> hybrid median    PAPER.md:76 (Sec. 3.4)
+//   out (tile)         -> HBM
+//
+// Border semantics (reading R5): each stage pads ITS OWN input by replication.
+// Every shared-memory region entry (i, j) holds the stage value at the CLAMPED
+// virtual coordinate, and each stage reads its input at clamp(c + d); a halo
+// entry outside the image therefore equals the stage value at the image edge,
+// exactly as if that stage's input had been padded.
+//
+// This kernel handles every supported parameter set (mask 3/5/7, std window
+// 3/5/7, median 3/5/7, both std sources, any bit depth).  kernel_fused.cu is
+// the fast path for the paper's 5x5 configuration.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lfe_internal.h"
+
+namespace lfe {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+struct Region {
+    int oy, ox;  // virtual coordinate of entry (0, 0)
+    int h, w;    // rows, cols
+    __device__ __forceinline__ int idx(int vy, int vx) const { return (vy - oy) * w + (vx - ox); }
+};
+
+__device__ __forceinline__ void cswap(uint32_t &a, uint32_t &b)
+{
+    uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// median of n (odd, <= 13) values by an insertion sort (general path only)
+__device__ __forceinline__ uint32_t median_n(uint32_t *v, int n)
+{
+    for (int i = 1; i < n; ++i) {
+        uint32_t x = v[i];
+        int j = i - 1;
+        while (j >= 0 && v[j] > x) {
+            v[j + 1] = v[j];
+            --j;
+        }
+        v[j + 1] = x;
+    }
+    return v[n / 2];
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(kThreads)
+    staged_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, int TW, int TH,
+                  int *err_flag)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int W = g.width, Hv = g.Hv;
+    const int x0 = blockIdx.x * TW;
+    const int y0 = g.o0 + blockIdx.y * TH;
+    const int h = kp.halo;
+    const int hr = h - kp.RL;      // LoG-response halo
+    const int hz = hr - 1;         // ZC halo (= Rs + Rm)
+    const int he = kp.Rm;          // merged-image halo
+
+    const Region RI{y0 - h, x0 - h, TH + 2 * h, TW + 2 * h};
+    const Region RR{y0 - hr, x0 - hr, TH + 2 * hr, TW + 2 * hr};
+    const Region RZ{y0 - hz, x0 - hz, TH + 2 * hz, TW + 2 * hz};
+    const Region RE{y0 - he, x0 - he, TH + 2 * he, TW + 2 * he};
+
+    uint16_t *sI = reinterpret_cast<uint16_t *>(smem);
+    size_t off = ((size_t)RI.h * RI.w * sizeof(uint16_t) + 15) & ~(size_t)15;
+    int32_t *sR = reinterpret_cast<int32_t *>(smem + off);
+    off += (size_t)2 * RR.h * RR.w * sizeof(int32_t);
+    uint8_t *sZ = smem + off;
+    off += ((size_t)2 * RZ.h * RZ.w + 15) & ~(size_t)15;
+    uint16_t *sE = reinterpret_cast<uint16_t *>(smem + off);
+
+    // ---- stage 0: input tile + halo, edge-replicated ("padded with 2 rows/columns")
+    int bad = 0;
+    for (int i = threadIdx.x; i < RI.h * RI.w; i += kThreads) {
+        int vy = clampi(RI.oy + i / RI.w, 0, Hv - 1);
+        int vx = clampi(RI.ox + i % RI.w, 0, W - 1);
+        const Tin *row = reinterpret_cast<const Tin *>(reinterpret_cast<const char *>(g.in) + (int64_t)vy * g.in_pitch);
+        uint32_t v = row[vx];
+        bad |= v > (uint32_t)kp.maxv;
+        sI[i] = (uint16_t)v;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err_flag, 1);
+
+    // ---- stage 1: the two LoG responses (Eq. 1 masks, integer, R3)
+    for (int i = threadIdx.x; i < RR.h * RR.w; i += kThreads) {
+        int cy = clampi(RR.oy + i / RR.w, 0, Hv - 1);
+        int cx = clampi(RR.ox + i % RR.w, 0, W - 1);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int n = kp.n[j], R = n / 2;
+            int32_t acc = 0;
+            for (int dy = -R; dy <= R; ++dy) {
+                int yy = clampi(cy + dy, 0, Hv - 1);
+                for (int dx = -R; dx <= R; ++dx) {
+                    int xx = clampi(cx + dx, 0, W - 1);
+                    acc += kp.q[j][(dy + R) * n + (dx + R)] * (int32_t)sI[RI.idx(yy, xx)];
+                }
+            }
+            sR[j * RR.h * RR.w + i] = acc;
+        }
+    }
+    __syncthreads();
+
+    // ---- stage 2: zero crossings, rule R* (readings R6-R9)
+    for (int i = threadIdx.x; i < RZ.h * RZ.w; i += kThreads) {
+        int cy = clampi(RZ.oy + i / RZ.w, 0, Hv - 1);
+        int cx = clampi(RZ.ox + i % RZ.w, 0, W - 1);
+        int nbi[4] = {RR.idx(clampi(cy - 1, 0, Hv - 1), cx), RR.idx(clampi(cy + 1, 0, Hv - 1), cx),
+                      RR.idx(cy, clampi(cx - 1, 0, W - 1)), RR.idx(cy, clampi(cx + 1, 0, W - 1))};
+        int pi = RR.idx(cy, cx);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int32_t *r = sR + j * RR.h * RR.w;
+            int32_t rp = r[pi];
+            int z;
+            if (rp != 0) {
+                int32_t ap = rp < 0 ? -rp : rp;
+                bool any = false, smallest = true;
+                int32_t gap = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    int32_t rn = r[nbi[k]];
+                    bool opp = rp > 0 ? rn < 0 : rn > 0;
+                    if (opp) {
+                        int32_t an = rn < 0 ? -rn : rn;
+                        any = true;
+                        smallest &= ap <= an;
+                        gap = max(gap, ap + an);
+                    }
+                }
+                z = any && smallest && gap >= kp.zc_t[j];
+            } else {
+                int32_t mx = r[nbi[0]], mn = mx;
+#pragma unroll
+                for (int k = 1; k < 4; ++k) {
+                    mx = max(mx, r[nbi[k]]);
+                    mn = min(mn, r[nbi[k]]);
+                }
+                z = mx > 0 && mn < 0 && (mx - mn) >= kp.zc_t[j];
+            }
+            sZ[j * RZ.h * RZ.w + i] = (uint8_t)z;
+        }
+    }
+    __syncthreads();
+
+    // ---- stage 3: std gate per branch (Eq. 2, R10-R13), OR merge (R14), extract (R15)
+    for (int i = threadIdx.x; i < RE.h * RE.w; i += kThreads) {
+        int cy = clampi(RE.oy + i / RE.w, 0, Hv - 1);
+        int cx = clampi(RE.ox + i % RE.w, 0, W - 1);
+        int zi = RZ.idx(cy, cx);
+        bool merged = false;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const uint8_t *Z = sZ + j * RZ.h * RZ.w;
+            if (!Z[zi]) continue;
+            const int Rs = kp.Rs;
+            bool pass;
+            if (kp.std_source == LFE_STD_ZC) {
+                int k = 0, k3 = 0;
+                for (int dy = -Rs; dy <= Rs; ++dy) {
+                    int yy = clampi(cy + dy, 0, Hv - 1);
+                    for (int dx = -Rs; dx <= Rs; ++dx) {
+                        int xx = clampi(cx + dx, 0, W - 1);
+                        int zv = Z[RZ.idx(yy, xx)];
+                        k += zv;
+                        if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) k3 += zv;
+                    }
+                }
+                pass = (kp.pass_lut[j] >> k) & 1ull;
+                if (pass && kp.recheck[j]) pass = (kp.pass3_lut[j] >> k3) & 1u;
+            } else {
+                int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
+                for (int dy = -Rs; dy <= Rs; ++dy) {
+                    int yy = clampi(cy + dy, 0, Hv - 1);
+                    for (int dx = -Rs; dx <= Rs; ++dx) {
+                        int xx = clampi(cx + dx, 0, W - 1);
+                        int64_t a = sI[RI.idx(yy, xx)];
+                        s1 += a;
+                        s2 += a * a;
+                        if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
+                            t1 += a;
+                            t2 += a * a;
+                        }
+                    }
+                }
+                const int L = kp.w * kp.w;
+                pass = (double)((int64_t)L * s2 - s1 * s1) > kp.rhs[j];
+                if (pass && kp.recheck[j]) pass = (double)(9 * t2 - t1 * t1) > kp.rhs3[j];
+            }
+            merged |= pass;
+        }
+        uint16_t e = 0;
+        if (merged) e = kp.out_mode == LFE_OUT_MASK ? 255 : sI[RI.idx(cy, cx)];
+        sE[i] = e;
+    }
+    __syncthreads();
+
+    // ---- stage 4: hybrid median (R16, R17) and store
+    for (int i = threadIdx.x; i < TH * TW; i += kThreads) {
+        int vy = y0 + i / TW, vx = x0 + i % TW;
+        if (vy >= g.o1 || vx >= W) continue;
+        uint32_t o;
+        if (kp.hm) {
+            const int R = kp.Rm;
+            uint32_t P[13], X[13];
+            int np = 0;
+            P[np] = sE[RE.idx(vy, vx)];
+            X[np] = P[np];
+            ++np;
+            for (int d = 1; d <= R; ++d) {
+                int ym = clampi(vy - d, 0, Hv - 1), yp = clampi(vy + d, 0, Hv - 1);
+                int xm = clampi(vx - d, 0, W - 1), xp = clampi(vx + d, 0, W - 1);
+                P[np] = sE[RE.idx(vy, xm)];
+                X[np++] = sE[RE.idx(ym, xm)];
+                P[np] = sE[RE.idx(vy, xp)];
+                X[np++] = sE[RE.idx(ym, xp)];
+                P[np] = sE[RE.idx(ym, vx)];
+                X[np++] = sE[RE.idx(yp, xm)];
+                P[np] = sE[RE.idx(yp, vx)];
+                X[np++] = sE[RE.idx(yp, xp)];
+            }
+            uint32_t c = sE[RE.idx(vy, vx)];
+            uint32_t a = median_n(P, np), b = median_n(X, np);
+            cswap(a, b);
+            cswap(b, c);
+            cswap(a, b);
+            o = b;  // median of three
+        } else {
+            o = sE[RE.idx(vy, vx)];
+        }
+        char *orow = reinterpret_cast<char *>(g.out) + (int64_t)(vy - g.o0) * g.out_pitch;
+        if (kp.out_mode == LFE_OUT_MASK)
+            reinterpret_cast<uint8_t *>(orow)[vx] = (uint8_t)o;
+        else
+            reinterpret_cast<Tin *>(orow)[vx] = (Tin)o;
+    }
+}
+
+size_t staged_smem(const KParams &kp, int TW, int TH)
+{
+    int h = kp.halo, hr = h - kp.RL, hz = hr - 1, he = kp.Rm;
+    size_t s = (((size_t)(TH + 2 * h) * (TW + 2 * h) * 2) + 15) & ~(size_t)15;
+    s += (size_t)2 * (TH + 2 * hr) * (TW + 2 * hr) * 4;
+    s += ((size_t)2 * (TH + 2 * hz) * (TW + 2 * hz) + 15) & ~(size_t)15;
+    s += (size_t)(TH + 2 * he) * (TW + 2 * he) * 2;
+    return s;
+}
+
+}  // namespace
+
+cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
+                          int *err_flag, cudaStream_t s)
+{
+    int TW = tile_w > 0 ? tile_w : 64;
+    int TH = tile_h > 0 ? tile_h : 32;
+    size_t smem = staged_smem(kp, TW, TH);
+    dim3 grid((g.width + TW - 1) / TW, (g.o1 - g.o0 + TH - 1) / TH);
+    if (grid.y == 0 || grid.x == 0) return cudaSuccess;
+    if (in16) {
+        cudaFuncSetAttribute(staged_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        staged_kernel<uint16_t><<<grid, kThreads, smem, s>>>(kp, g, TW, TH, err_flag);
+    } else {
+        cudaFuncSetAttribute(staged_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        staged_kernel<uint8_t><<<grid, kThreads, smem, s>>>(kp, g, TW, TH, err_flag);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace lfe

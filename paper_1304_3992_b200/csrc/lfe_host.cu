@@ -1,0 +1,502 @@
+// lfe_host.cu -- liblfe host core and C ABI (include/lfe.h).
+//
+// Parameter validation, integer mask synthesis (Eq. 1 -> DC correction ->
+// quantisation, readings R1-R3), the derived integer
+// thresholds (R9, R11, R12), launch planning for the two kernels, the strip
+// entry point used by multi-GPU sharding and the host-buffer end-to-end call.
+// Product code: shares nothing with oracle/.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "lfe.h"
+#include "lfe_internal.h"
+#include "lfe_test.h"
+
+using namespace lfe;
+
+namespace {
+
+thread_local char g_msg[512] = "";
+
+lfe_status fail(lfe_status s, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_msg, sizeof g_msg, fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+constexpr int kHostBuffers = 2;
+
+}  // namespace
+
+struct lfe_ctx {
+    lfe_params p;
+    KParams kp;
+    int F[2];
+    int device;
+    int *d_err = nullptr;
+    LaunchCfg cfg{LFE_KERNEL_AUTO, 0, 0};
+    int64_t launches = 0;
+    // lfe_extract_host staging
+    int host_strip_rows = 1024;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+    cudaEvent_t ev_h2d[kHostBuffers] = {}, ev_comp[kHostBuffers] = {}, ev_d2h[kHostBuffers] = {};
+    void *d_in[kHostBuffers] = {}, *d_out[kHostBuffers] = {};
+    size_t in_cap = 0, out_cap = 0;
+};
+
+namespace {
+
+// ---- Eq. 1, sampled at integer offsets (R2) ----------------
+double eq1(double s, int x, int y)
+{
+    const double pi = 3.14159265358979323846;
+    double rr = (double)(x * x + y * y);
+    double s2 = s * s;
+    return -1.0 / (pi * s2 * s2) * (1.0 - rr / (2.0 * s2)) * std::exp(-rr / (2.0 * s2));
+}
+
+// Integer mask per reading R3.  q is n*n row-major; returns false if no F fits.
+bool make_mask(double sigma, int n, int bit_depth, int32_t *q, int *F_out)
+{
+    const int R = n / 2, nn = n * n, centre = R * n + R;
+    double L[kMaxMaskCoeffs];
+    double total = 0.0;
+    for (int i = 0; i < nn; ++i) {
+        L[i] = eq1(sigma, i % n - R, i / n - R);
+        total += L[i];
+    }
+    const double mean = total / (double)nn;  // DC correction: zero-sum mask (band-pass)
+    for (int i = 0; i < nn; ++i) L[i] -= mean;
+    const double c = std::fabs(L[centre]);
+    const int64_t maxv = (int64_t(1) << bit_depth) - 1;
+    for (int F = 16; F >= 0; --F) {
+        const double scale = std::ldexp(1.0, F);
+        int64_t sum_others = 0, l1 = 0;
+        for (int i = 0; i < nn; ++i) {
+            if (i == centre) continue;
+            int64_t v = c > 0.0 ? (int64_t)std::round(L[i] / c * scale) : 0;  // half away from zero
+            q[i] = (int32_t)v;
+            sum_others += v;
+            l1 += std::llabs(v);
+        }
+        q[centre] = (int32_t)-sum_others;
+        l1 += std::llabs(sum_others);
+        if (maxv * l1 < (int64_t(1) << 24)) {  // every response exact in int32 and fp32
+            *F_out = F;
+            return true;
+        }
+    }
+    return false;
+}
+
+bool odd_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & 1); }
+
+lfe_status validate(const lfe_params *p)
+{
+    if (!p) return fail(LFE_EINVAL, "params is NULL");
+    if (p->abi_size != sizeof(lfe_params))
+        return fail(LFE_EINVAL, "abi_size %u != sizeof(lfe_params) %zu", p->abi_size, sizeof(lfe_params));
+    if (p->reserved0 || p->reserved1) return fail(LFE_EINVAL, "reserved fields must be 0");
+    if (p->bit_depth < 1 || p->bit_depth > 16) return fail(LFE_EINVAL, "bit_depth %d not in 1..16", p->bit_depth);
+    if (p->sigma_is_variance != 0 && p->sigma_is_variance != 1)
+        return fail(LFE_EINVAL, "sigma_is_variance must be 0 or 1");
+    for (int j = 0; j < 2; ++j) {
+        if (!std::isfinite(p->sigma[j]) || !(p->sigma[j] > 0.0))
+            return fail(LFE_EINVAL, "sigma[%d] must be finite and > 0", j);
+        if (p->log_size[j] < 1 || !(p->log_size[j] & 1)) return fail(LFE_EINVAL, "log_size[%d] must be odd", j);
+        if (!odd_in(p->log_size[j], 3, kMaxMask))
+            return fail(LFE_EUNSUPPORTED, "log_size[%d] = %d not in {3,5,7}", j, p->log_size[j]);
+        if (!std::isfinite(p->zc_threshold[j]) || p->zc_threshold[j] < 0.0)
+            return fail(LFE_EINVAL, "zc_threshold[%d] must be finite and >= 0", j);
+        if (!std::isfinite(p->std_threshold[j]) || p->std_threshold[j] < 0.0)
+            return fail(LFE_EINVAL, "std_threshold[%d] must be finite and >= 0", j);
+        if (std::isnan(p->std3_threshold[j]) || std::isinf(p->std3_threshold[j]))
+            return fail(LFE_EINVAL, "std3_threshold[%d] must be finite (< 0 disables)", j);
+    }
+    if (p->std_source != LFE_STD_ZC && p->std_source != LFE_STD_INTENSITY)
+        return fail(LFE_EINVAL, "std_source must be LFE_STD_ZC or LFE_STD_INTENSITY");
+    if (p->std_window < 1 || !(p->std_window & 1)) return fail(LFE_EINVAL, "std_window must be odd");
+    if (!odd_in(p->std_window, 3, kMaxStdWindow))
+        return fail(LFE_EUNSUPPORTED, "std_window %d not in {3,5,7}", p->std_window);
+    if (p->hybrid_median != 0 && p->hybrid_median != 1) return fail(LFE_EINVAL, "hybrid_median must be 0 or 1");
+    if (p->median_window < 1 || !(p->median_window & 1)) return fail(LFE_EINVAL, "median_window must be odd");
+    if (!odd_in(p->median_window, 3, kMaxMedianWindow))
+        return fail(LFE_EUNSUPPORTED, "median_window %d not in {3,5,7}", p->median_window);
+    if (p->out_mode != LFE_OUT_EXTRACT && p->out_mode != LFE_OUT_MASK)
+        return fail(LFE_EINVAL, "out_mode must be LFE_OUT_EXTRACT or LFE_OUT_MASK");
+    return LFE_OK;
+}
+
+lfe_status check_device(int *dev)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(LFE_ENODEV, "no CUDA device");
+    }
+    if (cudaGetDevice(dev) != cudaSuccess) return fail(LFE_ENODEV, "cudaGetDevice failed");
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, *dev);
+    if (major != 10) return fail(LFE_ENODEV, "device %d is sm_%d*, liblfe is built for sm_100a only", *dev, major);
+    return LFE_OK;
+}
+
+size_t elem_in(const lfe_ctx *c) { return c->p.bit_depth <= 8 ? 1 : 2; }
+size_t elem_out(const lfe_ctx *c) { return c->p.out_mode == LFE_OUT_MASK ? 1 : elem_in(c); }
+
+bool overlap(const void *a, size_t na, const void *b, size_t nb)
+{
+    auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + nb && y < x + na;
+}
+
+lfe_status run(lfe_ctx *c, const Geometry &g, cudaStream_t s)
+{
+    const bool in16 = c->p.bit_depth > 8;
+    int k = c->cfg.kernel;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(g.in) | reinterpret_cast<uintptr_t>(g.out) |
+                           (uintptr_t)g.in_pitch | (uintptr_t)g.out_pitch) & 15u) == 0;
+    const bool fused_ok = aligned && fused_supports(c->kp, c->p.bit_depth);
+    if (k == LFE_KERNEL_AUTO) k = fused_ok ? LFE_KERNEL_FUSED : LFE_KERNEL_STAGED;
+    if (k == LFE_KERNEL_FUSED && !fused_ok)
+        return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
+    cudaError_t e = k == LFE_KERNEL_FUSED
+                        ? launch_fused(c->kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s)
+                        : launch_staged(c->kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+    ++c->launches;
+    return LFE_OK;
+}
+
+lfe_status check_image_args(const lfe_ctx *c, const void *in, int64_t in_pitch, int32_t W, int64_t rows_total,
+                            const void *out, int64_t out_pitch, int64_t out_rows)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (!in || !out) return fail(LFE_EINVAL, "image pointer is NULL");
+    if (W < 1 || rows_total < 1 || out_rows < 1) return fail(LFE_EINVAL, "width/height must be >= 1");
+    const size_t ei = elem_in(c), eo = elem_out(c);
+    if ((int64_t)W * (int64_t)ei > ((int64_t)1 << 31)) return fail(LFE_EINVAL, "width too large");
+    if (in_pitch < (int64_t)W * (int64_t)ei) return fail(LFE_EINVAL, "in_pitch %lld < row bytes", (long long)in_pitch);
+    if (out_pitch < (int64_t)W * (int64_t)eo) return fail(LFE_EINVAL, "out_pitch %lld < row bytes", (long long)out_pitch);
+    if (in_pitch % (int64_t)ei || out_pitch % (int64_t)eo) return fail(LFE_EINVAL, "pitch not a multiple of the element size");
+    if (reinterpret_cast<uintptr_t>(in) % ei || reinterpret_cast<uintptr_t>(out) % eo)
+        return fail(LFE_EINVAL, "misaligned image pointer");
+    (void)rows_total;
+    return LFE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t lfe_abi_version(void) { return LFE_ABI_VERSION; }
+
+const char *lfe_last_message(void) { return g_msg; }
+
+const char *lfe_strerror(lfe_status s)
+{
+    switch (s) {
+    case LFE_OK: return "ok";
+    case LFE_EINVAL: return "invalid argument";
+    case LFE_EUNSUPPORTED: return "unsupported parameter";
+    case LFE_ENOMEM: return "out of memory";
+    case LFE_ENODEV: return "no sm_100 CUDA device";
+    case LFE_ECUDA: return "CUDA error";
+    case LFE_ERANGE: return "input pixel exceeds 2^bit_depth - 1";
+    }
+    return "unknown status";
+}
+
+void lfe_params_default(lfe_params *p)
+{
+    if (!p) return;
+    std::memset(p, 0, sizeof *p);
+    p->abi_size = sizeof(lfe_params);
+    p->bit_depth = 8;
+    p->sigma[0] = 0.5;   // "variance 0.5 and 20", sigma-direct (R1)
+    p->sigma[1] = 20.0;
+    p->sigma_is_variance = 0;
+    p->log_size[0] = p->log_size[1] = 5;  // "The LoG filter dimension ... was 5x5"
+    p->zc_threshold[0] = p->zc_threshold[1] = 0.0;
+    p->std_source = LFE_STD_ZC;
+    p->std_window = 5;                    // "5x5 neighborhood"
+    p->std_threshold[0] = p->std_threshold[1] = 0.3;
+    p->std3_threshold[0] = p->std3_threshold[1] = -1.0;
+    p->hybrid_median = 1;
+    p->median_window = 5;                 // "two subgroups of a 5x5 neighborhood"
+    p->out_mode = LFE_OUT_EXTRACT;
+}
+
+lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
+{
+    if (!out) return fail(LFE_EINVAL, "out is NULL");
+    *out = nullptr;
+    lfe_status st = validate(p);
+    if (st != LFE_OK) return st;
+    int dev = 0;
+    st = check_device(&dev);
+    if (st != LFE_OK) return st;
+
+    lfe_ctx *c = new (std::nothrow) lfe_ctx();
+    if (!c) return fail(LFE_ENOMEM, "host allocation");
+    c->p = *p;
+    c->device = dev;
+    KParams &kp = c->kp;
+    std::memset(&kp, 0, sizeof kp);
+    const int64_t maxv = (int64_t(1) << p->bit_depth) - 1;
+    kp.maxv = (int32_t)maxv;
+    kp.RL = 0;
+    for (int j = 0; j < 2; ++j) {
+        const double s = p->sigma_is_variance ? std::sqrt(p->sigma[j]) : p->sigma[j];
+        const int n = p->log_size[j];
+        if (!make_mask(s, n, p->bit_depth, kp.q[j], &c->F[j])) {
+            delete c;
+            return fail(LFE_EINVAL, "mask %d cannot be quantised", j);
+        }
+        kp.n[j] = n;
+        kp.RL = n / 2 > kp.RL ? n / 2 : kp.RL;
+        // gap threshold in integer units, t = ceil(thr * 2^F * M) (R9); a gap never exceeds 2^25
+        const double t = std::ceil(p->zc_threshold[j] * std::ldexp(1.0, c->F[j]) * (double)maxv);
+        kp.zc_t[j] = t > (double)(1 << 26) ? (1 << 26) : (int32_t)t;
+        // std gate (R11): s > T  <=>  L*S2 - S1^2 > L*(L-1)*T*T, compared in double
+        const int L = p->std_window * p->std_window;
+        const double T = p->std_threshold[j];
+        kp.rhs[j] = (double)(L * (L - 1)) * T * T;
+        kp.pass_lut[j] = 0;
+        for (int k = 0; k <= L; ++k)
+            if ((double)((int64_t)L * k - (int64_t)k * k) > kp.rhs[j]) kp.pass_lut[j] |= 1ull << k;
+        const double T3 = p->std3_threshold[j];
+        kp.recheck[j] = T3 >= 0.0;
+        kp.rhs3[j] = (double)(9 * 8) * T3 * T3;
+        kp.pass3_lut[j] = 0;
+        for (int k = 0; k <= 9; ++k)
+            if ((double)(9 * k - k * k) > kp.rhs3[j]) kp.pass3_lut[j] |= 1u << k;
+        if (n == 5) {
+            const int32_t *q = kp.q[j];
+            // orbits (0,0) (1,0) (2,0) (1,1) (2,1) (2,2) at row-major index (2+y)*5+(2+x)
+            kp.orb[j][0] = q[12];
+            kp.orb[j][1] = q[13];
+            kp.orb[j][2] = q[14];
+            kp.orb[j][3] = q[18];
+            kp.orb[j][4] = q[19];
+            kp.orb[j][5] = q[24];
+        }
+    }
+    kp.std_source = p->std_source;
+    kp.w = p->std_window;
+    kp.Rs = p->std_window / 2;
+    kp.hm = p->hybrid_median;
+    kp.m = p->median_window;
+    kp.Rm = p->hybrid_median ? p->median_window / 2 : 0;
+    kp.out_mode = p->out_mode;
+    kp.halo = kp.RL + 1 + kp.Rs + kp.Rm;
+
+    if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return fail(LFE_ENOMEM, "device error flag");
+    }
+    *out = c;
+    return LFE_OK;
+}
+
+int32_t lfe_halo(const lfe_ctx *c) { return c ? c->kp.halo : -1; }
+
+int64_t lfe_launch_count(const lfe_ctx *c) { return c ? c->launches : -1; }
+
+lfe_status lfe_get_mask(const lfe_ctx *c, int32_t branch, int32_t *coeffs, int32_t *n, int32_t *shift_F,
+                        int64_t *zc_t)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (branch != 0 && branch != 1) return fail(LFE_EINVAL, "branch must be 0 or 1");
+    const int nn = c->kp.n[branch];
+    if (coeffs) std::memcpy(coeffs, c->kp.q[branch], sizeof(int32_t) * nn * nn);
+    if (n) *n = nn;
+    if (shift_F) *shift_F = c->F[branch];
+    if (zc_t) *zc_t = c->kp.zc_t[branch];
+    return LFE_OK;
+}
+
+lfe_status lfe_set_option(lfe_ctx *c, int32_t key, int64_t value)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    switch (key) {
+    case LFE_OPT_KERNEL:
+        if (value < LFE_KERNEL_AUTO || value > LFE_KERNEL_FUSED) return fail(LFE_EINVAL, "bad kernel id");
+        c->cfg.kernel = (int)value;
+        return LFE_OK;
+    case LFE_OPT_TILE_W:
+        if (value < 0 || value > 1024) return fail(LFE_EINVAL, "bad tile width");
+        c->cfg.tile_w = (int)value;
+        return LFE_OK;
+    case LFE_OPT_TILE_H:
+        if (value < 0 || value > 1024) return fail(LFE_EINVAL, "bad tile height");
+        c->cfg.tile_h = (int)value;
+        return LFE_OK;
+    case LFE_OPT_HOST_STRIP_ROWS:
+        if (value < 1 || value > (1 << 20)) return fail(LFE_EINVAL, "bad strip rows");
+        c->host_strip_rows = (int)value;
+        return LFE_OK;
+    }
+    return fail(LFE_EINVAL, "unknown option %d", key);
+}
+
+lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
+                       int64_t out_pitch, void *stream)
+{
+    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
+    if (st != LFE_OK) return st;
+    if (overlap(d_in, (size_t)(H - 1) * in_pitch + W * elem_in(c), d_out, (size_t)(H - 1) * out_pitch + W * elem_out(c)))
+        return fail(LFE_EINVAL, "input and output overlap");
+    Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H};
+    return run(c, g, (cudaStream_t)stream);
+}
+
+lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
+                            int32_t halo_above, int32_t halo_below, uint32_t edge_flags, void *d_out_row0,
+                            int64_t out_pitch, void *stream)
+{
+    lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_out_row0, out_pitch, rows);
+    if (st != LFE_OK) return st;
+    if (edge_flags & ~3u) return fail(LFE_EINVAL, "unknown edge flag");
+    const int h = c->kp.halo;
+    const bool top = edge_flags & LFE_TOP_IS_EDGE, bot = edge_flags & LFE_BOTTOM_IS_EDGE;
+    if (halo_above < 0 || halo_below < 0) return fail(LFE_EINVAL, "negative halo");
+    if (!top && halo_above < h) return fail(LFE_EINVAL, "halo_above %d < required %d", halo_above, h);
+    if (!bot && halo_below < h) return fail(LFE_EINVAL, "halo_below %d < required %d", halo_below, h);
+    // an edge side clamps at its outermost readable row; an inner side reads exactly h rows
+    const int ha = top ? halo_above : h, hb = bot ? halo_below : h;
+    const char *vin = reinterpret_cast<const char *>(d_in_row0) - (int64_t)ha * in_pitch;
+    if (overlap(vin, (size_t)(rows + ha + hb - 1) * in_pitch + W * elem_in(c), d_out_row0,
+                (size_t)(rows - 1) * out_pitch + W * elem_out(c)))
+        return fail(LFE_EINVAL, "input and output overlap");
+    Geometry g{vin, in_pitch, d_out_row0, out_pitch, W, rows + ha + hb, ha, ha + rows};
+    return run(c, g, (cudaStream_t)stream);
+}
+
+lfe_status lfe_last_async_error(lfe_ctx *c, void *stream)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "stream: %s", cudaGetErrorString(e));
+    int flag = 0;
+    if (cudaMemcpy(&flag, c->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess)
+        return fail(LFE_ECUDA, "error flag: %s", cudaGetErrorString(cudaGetLastError()));
+    if (flag) return fail(LFE_ERANGE, "an input pixel exceeded 2^%d - 1", c->p.bit_depth);
+    return LFE_OK;
+}
+
+static lfe_status host_prepare(lfe_ctx *c, size_t in_bytes, size_t out_bytes)
+{
+    if (!c->st[0]) {
+        for (auto &s : c->st)
+            if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+                return fail(LFE_ECUDA, "stream create");
+        for (int b = 0; b < kHostBuffers; ++b)
+            if (cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming) != cudaSuccess)
+                return fail(LFE_ECUDA, "event create");
+    }
+    if (in_bytes > c->in_cap || out_bytes > c->out_cap) {
+        cudaDeviceSynchronize();
+        for (int b = 0; b < kHostBuffers; ++b) {
+            cudaFree(c->d_in[b]);
+            cudaFree(c->d_out[b]);
+            c->d_in[b] = c->d_out[b] = nullptr;
+        }
+        c->in_cap = c->out_cap = 0;
+        for (int b = 0; b < kHostBuffers; ++b)
+            if (cudaMalloc(&c->d_in[b], in_bytes) != cudaSuccess || cudaMalloc(&c->d_out[b], out_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(LFE_ENOMEM, "staging buffers (%zu + %zu bytes)", in_bytes, out_bytes);
+            }
+        c->in_cap = in_bytes;
+        c->out_cap = out_bytes;
+    }
+    return LFE_OK;
+}
+
+lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int32_t W, int32_t H, void *h_out,
+                            int64_t out_pitch)
+{
+    lfe_status st = check_image_args(c, h_in, in_pitch, W, H, h_out, out_pitch, H);
+    if (st != LFE_OK) return st;
+    const int h = c->kp.halo;
+    const int S = c->host_strip_rows < H ? c->host_strip_rows : H;
+    const size_t ei = elem_in(c), eo = elem_out(c);
+    const size_t dpi = ((size_t)W * ei + 127) & ~(size_t)127;  // device pitches, 128-B aligned rows
+    const size_t dpo = ((size_t)W * eo + 127) & ~(size_t)127;
+    st = host_prepare(c, dpi * (size_t)(S + 2 * h), dpo * (size_t)S);
+    if (st != LFE_OK) return st;
+    cudaStream_t sh = c->st[0], sc = c->st[1], sd = c->st[2];
+    const int nstrips = (H + S - 1) / S;
+    for (int i = 0; i < nstrips; ++i) {
+        const int b = i % kHostBuffers;
+        const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
+        const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
+        if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);  // input buffer free
+        cudaError_t e = cudaMemcpy2DAsync(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
+                                          in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
+        if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
+        cudaEventRecord(c->ev_h2d[b], sh);
+        cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
+        if (i >= kHostBuffers) cudaStreamWaitEvent(sc, c->ev_d2h[b], 0);   // output buffer free
+        const uint32_t flags = (lo == 0 ? LFE_TOP_IS_EDGE : 0u) | (hi == H ? LFE_BOTTOM_IS_EDGE : 0u);
+        const char *row0 = reinterpret_cast<const char *>(c->d_in[b]) + (size_t)(a0 - lo) * dpi;
+        st = lfe_extract_rows(c, row0, (int64_t)dpi, W, a1 - a0, a0 - lo, hi - a1, flags, c->d_out[b], (int64_t)dpo, sc);
+        if (st != LFE_OK) return st;
+        cudaEventRecord(c->ev_comp[b], sc);
+        cudaStreamWaitEvent(sd, c->ev_comp[b], 0);
+        e = cudaMemcpy2DAsync(reinterpret_cast<char *>(h_out) + (int64_t)a0 * out_pitch, out_pitch, c->d_out[b], dpo,
+                              (size_t)W * eo, a1 - a0, cudaMemcpyDeviceToHost, sd);
+        if (e != cudaSuccess) return fail(LFE_ECUDA, "D2H: %s", cudaGetErrorString(e));
+        cudaEventRecord(c->ev_d2h[b], sd);
+    }
+    return lfe_last_async_error(c, sd);
+}
+
+lfe_status lfe_test_mask(double sigma, int32_t n, int32_t bit_depth, int32_t *q, int32_t *shift_F)
+{
+    if (!q || !shift_F) return fail(LFE_EINVAL, "NULL output");
+    if (!std::isfinite(sigma) || !(sigma > 0.0)) return fail(LFE_EINVAL, "sigma must be > 0");
+    if (!odd_in(n, 1, kMaxMask)) return fail(LFE_EINVAL, "n must be odd 1..7");
+    if (bit_depth < 1 || bit_depth > 16) return fail(LFE_EINVAL, "bit depth");
+    int F = 0;
+    if (!make_mask(sigma, n, bit_depth, q, &F)) return fail(LFE_EINVAL, "no quantisation");
+    *shift_F = F;
+    return LFE_OK;
+}
+
+lfe_status lfe_test_validate(const lfe_params *p) { return validate(p); }
+
+void lfe_destroy(lfe_ctx *c)
+{
+    if (!c) return;
+    if (c->st[0]) {
+        for (auto s : c->st) cudaStreamSynchronize(s);
+        for (auto s : c->st) cudaStreamDestroy(s);
+        for (int b = 0; b < kHostBuffers; ++b) {
+            cudaEventDestroy(c->ev_h2d[b]);
+            cudaEventDestroy(c->ev_comp[b]);
+            cudaEventDestroy(c->ev_d2h[b]);
+        }
+    }
+    for (int b = 0; b < kHostBuffers; ++b) {
+        cudaFree(c->d_in[b]);
+        cudaFree(c->d_out[b]);
+    }
+    cudaFree(c->d_err);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// lfe_internal.h -- definitions shared by liblfe's host core and its kernels.
+// (Product path only; nothing here is shared with oracle/.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lfe.h"
+
+namespace lfe {
+
+constexpr int kMaxMask = 7;                 // largest compiled LoG side
+constexpr int kMaxMaskCoeffs = kMaxMask * kMaxMask;
+constexpr int kMaxStdWindow = 7;
+constexpr int kMaxMedianWindow = 7;
+
+// Everything a kernel needs, passed by value as a __grid_constant__ parameter.
+struct KParams {
+    int32_t q[2][kMaxMaskCoeffs];  // integer masks, row-major n x n (R3)
+    int32_t n[2];                  // mask sides
+    int32_t RL;                    // max mask radius
+    int32_t zc_t[2];               // ZC gap threshold, integer response units (R9)
+    int32_t std_source;            // LFE_STD_ZC / LFE_STD_INTENSITY
+    int32_t w;                     // std window side
+    int32_t Rs;                    // std window radius
+    uint64_t pass_lut[2];          // ZC source: bit k <=> w*w*k - k*k > w*w*(w*w-1)*T^2 (R11)
+    uint32_t pass3_lut[2];         // ZC source 3x3 re-check: bit k <=> 9k - k^2 > 72*T3^2
+    int32_t recheck[2];            // T3 >= 0
+    double rhs[2];                 // INTENSITY source: w*w*(w*w-1)*T*T (compared in double)
+    double rhs3[2];                // INTENSITY source: 72*T3*T3
+    int32_t hm;                    // hybrid median on/off
+    int32_t m;                     // median window side
+    int32_t Rm;                    // median radius (0 if off)
+    int32_t out_mode;              // LFE_OUT_EXTRACT / LFE_OUT_MASK
+    int32_t maxv;                  // 2^b - 1
+    int32_t halo;                  // RL + 1 + Rs + Rm
+    // orbit coefficients of 5x5 masks for the fused kernel: (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
+    int32_t orb[2][6];
+};
+
+// A virtual image: rows [0, Hv) of `width` pixels, clamped (edge-replicated)
+// at row 0, row Hv-1, column 0 and column width-1.  Output rows [o0, o1).
+struct Geometry {
+    const void *in;      // virtual row 0
+    int64_t in_pitch;    // bytes
+    void *out;           // output row o0
+    int64_t out_pitch;   // bytes
+    int32_t width;
+    int32_t Hv;
+    int32_t o0, o1;
+};
+
+struct LaunchCfg {
+    int kernel;   // LFE_KERNEL_*
+    int tile_w;   // 0 = default
+    int tile_h;
+};
+
+// kernel launchers (return cudaGetLastError())
+cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
+                          int *err_flag, cudaStream_t s);
+cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
+                         int *err_flag, cudaStream_t s);
+bool fused_supports(const KParams &kp, int bit_depth);
+
+}  // namespace lfe

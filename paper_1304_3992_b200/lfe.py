@@ -1,0 +1,355 @@
+"""Thin Python binding of liblfe (include/lfe.h) -- argument marshalling only.
+
+Every step of the hot path runs inside liblfe's CUDA kernels; this module only
+turns torch tensors / numpy arrays into pointers, pitches and streams.  There
+is no CPU fallback: if liblfe.so is missing or no sm_100 device is present the
+calls raise.
+
+Function names mirror the C ABI (``lfe_create``, ``lfe_extract``, ...); the
+``Context`` class is a convenience wrapper over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblfe.so")
+
+LFE_OK, LFE_EINVAL, LFE_EUNSUPPORTED, LFE_ENOMEM, LFE_ENODEV, LFE_ECUDA, LFE_ERANGE = range(7)
+LFE_STD_ZC, LFE_STD_INTENSITY = 0, 1
+LFE_OUT_EXTRACT, LFE_OUT_MASK = 0, 1
+LFE_TOP_IS_EDGE, LFE_BOTTOM_IS_EDGE = 1, 2
+LFE_OPT_KERNEL, LFE_OPT_TILE_W, LFE_OPT_TILE_H, LFE_OPT_HOST_STRIP_ROWS = 1, 2, 3, 4
+LFE_KERNEL_AUTO, LFE_KERNEL_STAGED, LFE_KERNEL_FUSED = 0, 1, 2
+
+_STATUS = {0: "LFE_OK", 1: "LFE_EINVAL", 2: "LFE_EUNSUPPORTED", 3: "LFE_ENOMEM",
+           4: "LFE_ENODEV", 5: "LFE_ECUDA", 6: "LFE_ERANGE"}
+
+
+class LfeError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        super().__init__(f"{where}: {_STATUS.get(status, status)}: {detail}")
+
+
+class lfe_params(ctypes.Structure):
+    _fields_ = [
+        ("abi_size", ctypes.c_uint32),
+        ("bit_depth", ctypes.c_int32),
+        ("sigma", ctypes.c_double * 2),
+        ("sigma_is_variance", ctypes.c_int32),
+        ("log_size", ctypes.c_int32 * 2),
+        ("reserved0", ctypes.c_int32),
+        ("zc_threshold", ctypes.c_double * 2),
+        ("std_source", ctypes.c_int32),
+        ("std_window", ctypes.c_int32),
+        ("std_threshold", ctypes.c_double * 2),
+        ("std3_threshold", ctypes.c_double * 2),
+        ("hybrid_median", ctypes.c_int32),
+        ("median_window", ctypes.c_int32),
+        ("out_mode", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
+    ]
+
+
+assert ctypes.sizeof(lfe_params) == 112
+
+_lib = None
+
+# every symbol include/lfe.h declares (the CPU test checks the .so exports them)
+EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows", "lfe_extract_host",
+           "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
+           "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version"]
+TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate"]  # include/lfe_test.h
+
+
+def load():
+    """Load liblfe.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"liblfe.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    st = ctypes.c_int
+    L.lfe_params_default.argtypes = [ctypes.POINTER(lfe_params)]
+    L.lfe_params_default.restype = None
+    L.lfe_create.argtypes = [ctypes.POINTER(lfe_params), ctypes.POINTER(P)]
+    L.lfe_create.restype = st
+    L.lfe_extract.argtypes = [P, P, I64, I32, I32, P, I64, P]
+    L.lfe_extract.restype = st
+    L.lfe_extract_rows.argtypes = [P, P, I64, I32, I32, I32, I32, U32, P, I64, P]
+    L.lfe_extract_rows.restype = st
+    L.lfe_extract_host.argtypes = [P, P, I64, I32, I32, P, I64]
+    L.lfe_extract_host.restype = st
+    L.lfe_halo.argtypes = [P]
+    L.lfe_halo.restype = I32
+    L.lfe_get_mask.argtypes = [P, I32, P, P, P, P]
+    L.lfe_get_mask.restype = st
+    L.lfe_last_async_error.argtypes = [P, P]
+    L.lfe_last_async_error.restype = st
+    L.lfe_set_option.argtypes = [P, I32, I64]
+    L.lfe_set_option.restype = st
+    L.lfe_launch_count.argtypes = [P]
+    L.lfe_launch_count.restype = I64
+    L.lfe_destroy.argtypes = [P]
+    L.lfe_destroy.restype = None
+    L.lfe_strerror.argtypes = [st]
+    L.lfe_strerror.restype = ctypes.c_char_p
+    L.lfe_last_message.argtypes = []
+    L.lfe_last_message.restype = ctypes.c_char_p
+    L.lfe_abi_version.argtypes = []
+    L.lfe_abi_version.restype = I32
+    L.lfe_test_mask.argtypes = [ctypes.c_double, I32, I32, P, P]
+    L.lfe_test_mask.restype = st
+    L.lfe_test_validate.argtypes = [ctypes.POINTER(lfe_params)]
+    L.lfe_test_validate.restype = st
+    _lib = L
+    return L
+
+
+def _check(status: int, where: str):
+    if status != LFE_OK:
+        raise LfeError(status, where, load().lfe_last_message().decode())
+
+
+# ------------------------------------------------------------ C names ----
+def lfe_params_default() -> lfe_params:
+    p = lfe_params()
+    load().lfe_params_default(ctypes.byref(p))
+    return p
+
+
+def lfe_create(p: lfe_params) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(load().lfe_create(ctypes.byref(p), ctypes.byref(h)), "lfe_create")
+    return h
+
+
+def lfe_extract(ctx, d_in: int, in_pitch: int, width: int, height: int, d_out: int, out_pitch: int,
+                stream: int = 0):
+    _check(load().lfe_extract(ctx, d_in, in_pitch, width, height, d_out, out_pitch, stream), "lfe_extract")
+
+
+def lfe_extract_rows(ctx, d_in_row0: int, in_pitch: int, width: int, rows: int, halo_above: int,
+                     halo_below: int, edge_flags: int, d_out_row0: int, out_pitch: int, stream: int = 0):
+    _check(load().lfe_extract_rows(ctx, d_in_row0, in_pitch, width, rows, halo_above, halo_below,
+                                   edge_flags, d_out_row0, out_pitch, stream), "lfe_extract_rows")
+
+
+def lfe_extract_host(ctx, h_in: int, in_pitch: int, width: int, height: int, h_out: int, out_pitch: int):
+    _check(load().lfe_extract_host(ctx, h_in, in_pitch, width, height, h_out, out_pitch), "lfe_extract_host")
+
+
+def lfe_halo(ctx) -> int:
+    return int(load().lfe_halo(ctx))
+
+
+def lfe_get_mask(ctx, branch: int):
+    coeffs = (ctypes.c_int32 * 49)()
+    n, F, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    _check(load().lfe_get_mask(ctx, branch, coeffs, ctypes.byref(n), ctypes.byref(F), ctypes.byref(t)),
+           "lfe_get_mask")
+    q = np.array(coeffs[: n.value * n.value], np.int32).reshape(n.value, n.value)
+    return q, F.value, t.value
+
+
+def lfe_last_async_error(ctx, stream: int = 0) -> int:
+    return int(load().lfe_last_async_error(ctx, stream))
+
+
+def lfe_set_option(ctx, key: int, value: int):
+    _check(load().lfe_set_option(ctx, key, value), "lfe_set_option")
+
+
+def lfe_launch_count(ctx) -> int:
+    return int(load().lfe_launch_count(ctx))
+
+
+def lfe_destroy(ctx):
+    load().lfe_destroy(ctx)
+
+
+def lfe_strerror(status: int) -> str:
+    return load().lfe_strerror(status).decode()
+
+
+def lfe_abi_version() -> int:
+    return int(load().lfe_abi_version())
+
+
+def lfe_test_mask(sigma: float, n: int, bit_depth: int):
+    """Host-side mask synthesis of the library (include/lfe_test.h)."""
+    q = np.zeros(n * n, np.int32)
+    F = ctypes.c_int32()
+    _check(load().lfe_test_mask(float(sigma), n, bit_depth, q.ctypes.data, ctypes.byref(F)), "lfe_test_mask")
+    return q.reshape(n, n), F.value
+
+
+def lfe_test_validate(p: lfe_params) -> int:
+    return int(load().lfe_test_validate(ctypes.byref(p)))
+
+
+# ------------------------------------------------------ convenience ----
+@dataclass
+class Params:
+    """Python view of lfe_params (defaults = lfe_params_default)."""
+    bit_depth: int = 8
+    sigma: tuple = (0.5, 20.0)
+    sigma_is_variance: bool = False
+    log_size: tuple = (5, 5)
+    zc_threshold: tuple = (0.0, 0.0)
+    std_source: int = LFE_STD_ZC
+    std_window: int = 5
+    std_threshold: tuple = (0.3, 0.3)
+    std3_threshold: tuple = (-1.0, -1.0)
+    hybrid_median: bool = True
+    median_window: int = 5
+    out_mode: int = LFE_OUT_EXTRACT
+
+    def to_c(self) -> lfe_params:
+        p = lfe_params()
+        p.abi_size = ctypes.sizeof(lfe_params)
+        p.bit_depth = self.bit_depth
+        p.sigma[0], p.sigma[1] = self.sigma
+        p.sigma_is_variance = int(bool(self.sigma_is_variance))
+        p.log_size[0], p.log_size[1] = self.log_size
+        p.zc_threshold[0], p.zc_threshold[1] = self.zc_threshold
+        p.std_source = self.std_source
+        p.std_window = self.std_window
+        p.std_threshold[0], p.std_threshold[1] = self.std_threshold
+        p.std3_threshold[0], p.std3_threshold[1] = self.std3_threshold
+        p.hybrid_median = int(bool(self.hybrid_median))
+        p.median_window = self.median_window
+        p.out_mode = self.out_mode
+        return p
+
+
+def _in_dtype(bit_depth):
+    return np.uint8 if bit_depth <= 8 else np.uint16
+
+
+class Context:
+    """One lfe_ctx: masks synthesised once, then any number of extractions."""
+
+    def __init__(self, params: Params | None = None, **kw):
+        self.params = params if params is not None else Params(**kw)
+        self.handle = lfe_create(self.params.to_c())
+
+    # -- metadata
+    @property
+    def halo(self) -> int:
+        return lfe_halo(self.handle)
+
+    def mask(self, branch: int):
+        return lfe_get_mask(self.handle, branch)
+
+    def set_option(self, key: int, value: int):
+        lfe_set_option(self.handle, key, value)
+
+    @property
+    def launches(self) -> int:
+        return lfe_launch_count(self.handle)
+
+    def in_dtype(self):
+        return _in_dtype(self.params.bit_depth)
+
+    def out_dtype(self):
+        return np.uint8 if self.params.out_mode == LFE_OUT_MASK else self.in_dtype()
+
+    # -- device (torch) entry points
+    @staticmethod
+    def _torch_img(t, name):
+        import torch
+        if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+            raise TypeError(f"{name} must be a CUDA torch tensor")
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError(f"{name} must be 2-D with unit column stride")
+        return t.data_ptr(), t.stride(0) * t.element_size()
+
+    @staticmethod
+    def _stream(stream):
+        import torch
+        if stream is None:
+            return torch.cuda.current_stream().cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def _check_dtype(self, t_in, t_out):
+        import torch
+        tin = torch.uint8 if self.params.bit_depth <= 8 else torch.uint16
+        tout = torch.uint8 if self.params.out_mode == LFE_OUT_MASK else tin
+        if t_in.dtype != tin or t_out.dtype != tout:
+            raise TypeError(f"dtypes must be {tin} -> {tout}")
+
+    def extract(self, t_in, t_out=None, stream=None):
+        """Whole-image extraction of a 2-D CUDA tensor; returns the output tensor."""
+        import torch
+        if t_out is None:
+            tout = torch.uint8 if self.params.out_mode == LFE_OUT_MASK else t_in.dtype
+            t_out = torch.empty(t_in.shape, dtype=tout, device=t_in.device)
+        self._check_dtype(t_in, t_out)
+        if t_in.shape != t_out.shape:
+            raise ValueError("shape mismatch")
+        pi, pin = self._torch_img(t_in, "input")
+        po, pout = self._torch_img(t_out, "output")
+        H, W = t_in.shape
+        lfe_extract(self.handle, pi, pin, W, H, po, pout, self._stream(stream))
+        return t_out
+
+    def extract_rows(self, t_in_full, row0: int, rows: int, halo_above: int, halo_below: int,
+                     edge_flags: int, t_out, out_row0: int = 0, stream=None):
+        """Strip entry point: t_in_full holds rows [row0-halo_above, row0+rows+halo_below)."""
+        pi, pin = self._torch_img(t_in_full, "input")
+        po, pout = self._torch_img(t_out, "output")
+        self._check_dtype(t_in_full, t_out)
+        W = t_in_full.shape[1]
+        lfe_extract_rows(self.handle, pi + row0 * pin, pin, W, rows, halo_above, halo_below, edge_flags,
+                         po + out_row0 * pout, pout, self._stream(stream))
+        return t_out
+
+    def last_async_error(self, stream=None) -> int:
+        return lfe_last_async_error(self.handle, self._stream(stream))
+
+    def check(self, stream=None):
+        _check(self.last_async_error(stream), "lfe_last_async_error")
+
+    # -- host entry point
+    def extract_host(self, a_in: np.ndarray, a_out: np.ndarray | None = None) -> np.ndarray:
+        """End to end on host memory (H2D -> kernel -> D2H inside liblfe)."""
+        if a_in.ndim != 2 or a_in.strides[1] != a_in.itemsize:
+            raise ValueError("input must be 2-D with unit column stride")
+        if a_in.dtype != self.in_dtype():
+            raise TypeError(f"input dtype must be {np.dtype(self.in_dtype())}")
+        if a_out is None:
+            a_out = np.empty(a_in.shape, self.out_dtype())
+        if a_out.dtype != self.out_dtype() or a_out.shape != a_in.shape:
+            raise TypeError("bad output array")
+        H, W = a_in.shape
+        lfe_extract_host(self.handle, a_in.ctypes.data, a_in.strides[0], W, H, a_out.ctypes.data,
+                         a_out.strides[0])
+        return a_out
+
+    def extract_host_ptr(self, p_in: int, in_pitch: int, W: int, H: int, p_out: int, out_pitch: int):
+        lfe_extract_host(self.handle, p_in, in_pitch, W, H, p_out, out_pitch)
+
+    def close(self):
+        if self.handle:
+            lfe_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

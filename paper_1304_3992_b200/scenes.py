@@ -88,15 +88,13 @@ def _urban(H, W, seed, scale, n_rect, noise_sigma, maxval, dtype, rows_per_block
     ph = rng.uniform(0, 2 * np.pi, 4)
     img = np.empty((H, W), np.float32)
     xs = np.arange(W, dtype=np.float64)
+    # cos(kx x + ky y + ph) = cos(kx x) cos(ky y + ph) - sin(kx x) sin(ky y + ph): a rank-8 product
+    B = np.concatenate([np.cos(np.outer(kx, xs)), np.sin(np.outer(kx, xs))]).astype(np.float32)
     for y0 in range(0, H, rows_per_block):
         y1 = min(H, y0 + rows_per_block)
         ys = np.arange(y0, y1, dtype=np.float64)
-        acc = np.full((y1 - y0, W), 100.0 * scale, np.float64)
-        for k in range(4):
-            a = np.cos(kx[k] * xs)[None, :] * np.cos(ky[k] * ys + ph[k])[:, None]
-            b = np.sin(kx[k] * xs)[None, :] * np.sin(ky[k] * ys + ph[k])[:, None]
-            acc += 10.0 * scale * (a - b)
-        img[y0:y1] = acc
+        A = np.concatenate([np.cos(np.outer(ys, ky) + ph), -np.sin(np.outer(ys, ky) + ph)], axis=1)
+        img[y0:y1] = np.float32(100.0 * scale) + np.float32(10.0 * scale) * (A.astype(np.float32) @ B)
     # rectangles: sides U{6..48}, value U{130..230} (x scale)
     rw = rng.integers(6, 49, n_rect)
     rh = rng.integers(6, 49, n_rect)
@@ -120,7 +118,7 @@ def _urban(H, W, seed, scale, n_rect, noise_sigma, maxval, dtype, rows_per_block
     for y0 in range(0, H, rows_per_block):
         y1 = min(H, y0 + rows_per_block)
         nrng = np.random.default_rng([seed, 1, y0])
-        blk = img[y0:y1] + nrng.normal(0.0, noise_sigma, (y1 - y0, W)).astype(np.float32)
+        blk = img[y0:y1] + np.float32(noise_sigma) * nrng.standard_normal((y1 - y0, W), dtype=np.float32)
         out[y0:y1] = np.clip(np.rint(blk), 0, maxval).astype(dtype)
     # salt-and-pepper 0.2%
     n_sp = int(round(0.002 * H * W))

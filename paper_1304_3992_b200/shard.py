@@ -1,0 +1,118 @@
+"""Row-strip sharding of one scene across the GPUs of a node (north_star:
+"Large scenes are partitioned into row strips across the GPUs ... with an NCCL
+halo exchange of boundary rows over NVLink").
+
+Host logic only: strip planning and the neighbour halo exchange, written
+against ``torch.distributed`` so the same code runs over NCCL on GPUs and over
+gloo on CPU (tests).  The compute on each strip is ``lfe_extract_rows``.
+
+Each rank keeps ONE contiguous buffer ``[halo_above | owned rows | halo_below]``
+so a strip is a single pitched image for liblfe.  The exchange is the only
+data-path collective: rank k sends its first ``halo`` owned rows to k-1 and its
+last ``halo`` owned rows to k+1.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def plan_strips(H: int, world: int, halo: int):
+    """Contiguous, balanced row ranges [a, b) covering [0, H).  Every strip must
+    hold at least ``halo`` rows so one neighbour exchange suffices."""
+    if world < 1 or H < 1:
+        raise ValueError("bad H/world")
+    base, extra = divmod(H, world)
+    out, a = [], 0
+    for k in range(world):
+        b = a + base + (1 if k < extra else 0)
+        out.append((a, b))
+        a = b
+    if world > 1 and min(b - a for a, b in out) < halo:
+        raise ValueError(f"strip of {min(b - a for a, b in out)} rows < halo {halo}: use fewer ranks")
+    return out
+
+
+@dataclass
+class StripShard:
+    H: int
+    W: int
+    rank: int
+    world: int
+    halo: int
+
+    def __post_init__(self):
+        self.plan = plan_strips(self.H, self.world, self.halo)
+        self.a, self.b = self.plan[self.rank]
+        self.rows = self.b - self.a
+        self.ha = self.halo if self.rank > 0 else 0
+        self.hb = self.halo if self.rank < self.world - 1 else 0
+
+    @property
+    def buf_rows(self) -> int:
+        return self.ha + self.rows + self.hb
+
+    def alloc(self, dtype, device):
+        import torch
+        self.buf = torch.zeros((self.buf_rows, self.W), dtype=dtype, device=device)
+        return self.buf
+
+    def load_owned(self, full_image_rows):
+        """Copy this rank's owned rows (from a full-image tensor/array)."""
+        import torch
+        src = full_image_rows[self.a:self.b]
+        if not isinstance(src, torch.Tensor):
+            src = torch.from_numpy(src)
+        self.buf[self.ha:self.ha + self.rows].copy_(src)
+
+    def exchange(self, group=None):
+        """Post the halo exchange (isend/irecv with both neighbours); returns the
+        works to wait on.  Owned rows are not modified."""
+        import torch.distributed as dist
+        h, ops = self.halo, []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, self.buf[self.ha:self.ha + h], self.rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, self.buf[0:self.ha], self.rank - 1, group))
+        if self.rank < self.world - 1:
+            e = self.ha + self.rows
+            ops.append(dist.P2POp(dist.isend, self.buf[e - h:e], self.rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, self.buf[e:e + self.hb], self.rank + 1, group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def edge_flags(self) -> int:
+        from .lfe import LFE_BOTTOM_IS_EDGE, LFE_TOP_IS_EDGE
+        return (LFE_TOP_IS_EDGE if self.rank == 0 else 0) | (LFE_BOTTOM_IS_EDGE if self.rank == self.world - 1 else 0)
+
+    def band(self, s: int, n: int):
+        """Arguments of lfe_extract_rows for owned rows [s, s+n) of this strip:
+        (s, n, halo_above, halo_below, flags, needs_exchange)."""
+        from .lfe import LFE_BOTTOM_IS_EDGE, LFE_TOP_IS_EDGE
+        h, R = self.halo, self.rows
+        flags, need = 0, False
+        if self.rank == 0:                    # buffer row 0 is the image top
+            ha = s
+            flags |= LFE_TOP_IS_EDGE
+        else:
+            ha = h
+            need |= s < h                     # reads received rows above
+        if self.rank == self.world - 1:       # last buffer row is the image bottom
+            hb = R - s - n
+            flags |= LFE_BOTTOM_IS_EDGE
+        else:
+            hb = h
+            need |= s + n > R - h             # reads received rows below
+        return (s, n, ha, hb, flags, need)
+
+    def bands(self):
+        """The interior band (local rows only: computable while the exchange is
+        in flight) followed by the boundary bands that wait for it."""
+        h, R = self.halo, self.rows
+        lo = 0 if self.rank == 0 else h
+        hi = R if self.rank == self.world - 1 else R - h
+        if hi - lo <= 0:
+            return [self.band(0, R)]
+        out = [self.band(lo, hi - lo)]
+        if lo > 0:
+            out.append(self.band(0, lo))
+        if hi < R:
+            out.append(self.band(hi, R - hi))
+        return out

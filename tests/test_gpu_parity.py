@@ -1,0 +1,234 @@
+"""GPU parity: liblfe (through its C ABI) vs the CPU oracle, bit for bit.
+
+The contract (north_star): integer inputs with integer
+masks and integer std sums -> the output must equal the oracle exactly.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1304_3992_b200 import lfe, scenes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    lfe.load()
+
+
+def _oparams(p: lfe.Params) -> O.Params:
+    return O.Params(bit_depth=p.bit_depth, sigma=tuple(p.sigma), sigma_is_variance=p.sigma_is_variance,
+                    log_size=tuple(p.log_size), zc_threshold=tuple(p.zc_threshold),
+                    std_source=p.std_source, std_window=p.std_window,
+                    std_threshold=tuple(p.std_threshold), std3_threshold=tuple(p.std3_threshold),
+                    hybrid_median=p.hybrid_median, median_window=p.median_window, out_mode=p.out_mode)
+
+
+def run_gpu(img: np.ndarray, p: lfe.Params, kernel=lfe.LFE_KERNEL_AUTO, tile=None):
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_KERNEL, kernel)
+        if tile:
+            ctx.set_option(lfe.LFE_OPT_TILE_W, tile[0])
+            ctx.set_option(lfe.LFE_OPT_TILE_H, tile[1])
+        d = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        out = ctx.extract(d)
+        ctx.check()
+        return out.cpu().numpy()
+
+
+def assert_same(got, want, what=""):
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        y, x = bad[0]
+        raise AssertionError(f"{what}: {len(bad)} pixels differ; first at ({y},{x}): "
+                             f"got {got[y, x]} want {want[y, x]}")
+
+
+KERNELS = [lfe.LFE_KERNEL_STAGED, lfe.LFE_KERNEL_AUTO]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("clean", [True, False])
+@pytest.mark.parametrize("hm", [True, False])
+@pytest.mark.parametrize("mode", [lfe.LFE_OUT_EXTRACT, lfe.LFE_OUT_MASK])
+def test_c1(kernel, clean, hm, mode):
+    img = scenes.scene_c1(clean=clean)
+    thr = 0.0 if clean else 0.02
+    p = lfe.Params(bit_depth=8, zc_threshold=(thr, thr), hybrid_median=hm, out_mode=mode)
+    assert_same(run_gpu(img, p, kernel), O.run(img, _oparams(p)), "c1")
+
+
+def _param_cases():
+    yield lfe.Params(bit_depth=8)
+    yield lfe.Params(bit_depth=10, zc_threshold=(0.01, 0.03))
+    yield lfe.Params(bit_depth=12, sigma=(0.5, 20.0), sigma_is_variance=True)
+    yield lfe.Params(bit_depth=16, out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=1)
+    yield lfe.Params(bit_depth=8, log_size=(3, 7), std_window=3, median_window=3)
+    yield lfe.Params(bit_depth=10, log_size=(7, 7), std_window=7, median_window=7)
+    yield lfe.Params(bit_depth=8, std3_threshold=(0.4, 0.2), std_threshold=(0.25, 0.35))
+    yield lfe.Params(bit_depth=10, std_source=lfe.LFE_STD_INTENSITY, std_threshold=(20.0, 60.0),
+                     std3_threshold=(10.0, -1.0))
+    yield lfe.Params(bit_depth=16, std_source=lfe.LFE_STD_INTENSITY, std_threshold=(3000.0, 100.0),
+                     std_window=7)
+    yield lfe.Params(bit_depth=8, hybrid_median=False, std_threshold=(0.0, 0.0))
+    yield lfe.Params(bit_depth=12, sigma=(1.0, 2.0), zc_threshold=(0.005, 0.0), out_mode=lfe.LFE_OUT_MASK)
+
+
+SHAPES = [(1, 1), (1, 17), (23, 1), (2, 2), (5, 7), (37, 53), (64, 64), (65, 129), (130, 257), (300, 200)]
+
+
+@pytest.mark.parametrize("ci", range(12))
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_random_images_param_sweep(ci, kernel):
+    p = list(_param_cases())[ci]
+    rng = np.random.default_rng(100 + ci)
+    for (H, W), kind in itertools.product(SHAPES, ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, p.bit_depth, kind)
+        assert_same(run_gpu(img, p, kernel), O.run(img, _oparams(p)), f"{H}x{W} {kind} {p}")
+
+
+@pytest.mark.parametrize("tile", [(32, 8), (64, 32), (128, 16), (40, 24), (256, 4)])
+def test_tile_shape_invariance_staged(tile):
+    """Result never depends on the tile shape (Table 4 analogue)."""
+    img = scenes.scene_c1(size=300)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.01))
+    want = O.run(img, _oparams(p))
+    assert_same(run_gpu(img, p, lfe.LFE_KERNEL_STAGED, tile), want, f"tile {tile}")
+
+
+def test_c2_full():
+    img = scenes.scene_c2()
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.02, 0.02))
+    assert_same(run_gpu(img, p), O.run(img, _oparams(p)), "c2")
+
+
+def _sampled_rows(img, p, got, bands):
+    """Compare rows [a, b) of a full-size GPU result with the oracle run on the
+    band plus a halo of real rows (clamped only at the true image edge)."""
+    H = img.shape[0]
+    halo = 3 + 1 + 3 + 3 + 1  # >= any configuration's halo
+    for a, b in bands:
+        lo, hi = max(0, a - halo), min(H, b + halo)
+        ref = O.run(np.ascontiguousarray(img[lo:hi]), _oparams(p))
+        assert_same(got[a:b], ref[a - lo:a - lo + (b - a)], f"rows {a}:{b}")
+
+
+def test_c3_full_size_sampled():
+    """c3 at its full 12000x12000 u16 size in bench.py's configuration; the
+    oracle checks sampled row bands including the first and last rows."""
+    img = scenes.scene_c3()
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    got = run_gpu(img, p)
+    _sampled_rows(img, p, got, [(0, 40), (5997, 6031), (11960, 12000)])
+
+
+def test_c4_band_full_size_sampled():
+    img = scenes.scene_c4(size=8192)
+    p = lfe.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
+    for b in (0, 3):
+        got = run_gpu(img[b], p)
+        _sampled_rows(img[b], p, got, [(0, 24), (4100, 4124), (8170, 8192)])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_strips_equal_whole_image(kernel):
+    """lfe_extract_rows with halos from neighbours (what multi-GPU sharding
+    does) is bit-identical to the whole-image result, for any strip split."""
+    img = scenes.scene_c1(size=200)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.01))
+    H, W = img.shape
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_KERNEL, kernel)
+        h = ctx.halo
+        assert h == 7
+        d = torch.from_numpy(img).cuda()
+        whole = ctx.extract(d).cpu().numpy()
+        for cuts in ([0, 100, 200], [0, 7, 14, 150, 200], [0, 1, 2, 199, 200], [0, 33, 66, 99, 132, 165, 200]):
+            out = torch.zeros_like(d)
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                ha, hb = min(h, a), min(h, H - b)
+                flags = (lfe.LFE_TOP_IS_EDGE if a - ha == 0 else 0) | \
+                    (lfe.LFE_BOTTOM_IS_EDGE if b + hb == H else 0)
+                # a separate buffer holding only the strip + halo rows
+                strip = d[a - ha:b + hb].clone()
+                ctx.extract_rows(strip, ha, b - a, ha, hb, flags, out, out_row0=a)
+            ctx.check()
+            assert_same(out.cpu().numpy(), whole, f"cuts {cuts}")
+
+
+def test_strip_halo_validation():
+    with lfe.Context(lfe.Params()) as ctx:
+        d = torch.zeros((40, 32), dtype=torch.uint8, device="cuda")
+        o = torch.zeros_like(d)
+        with pytest.raises(lfe.LfeError):
+            ctx.extract_rows(d, 5, 10, 5, 7, 0, o)   # halo_above 5 < 7
+        with pytest.raises(lfe.LfeError):
+            ctx.extract_rows(d, 7, 10, 7, 6, lfe.LFE_TOP_IS_EDGE, o)  # halo_below 6 < 7
+
+
+def test_extract_host_matches_device():
+    img = scenes.scene_c3(size=1000, height=2500)
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    want = run_gpu(img, p)
+    with lfe.Context(p) as ctx:
+        for strip in (64, 1000, 4096):
+            ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, strip)
+            pin_in = torch.from_numpy(img).pin_memory()
+            pin_out = torch.empty(img.shape, dtype=torch.uint16).pin_memory()
+            ctx.extract_host_ptr(pin_in.data_ptr(), pin_in.stride(0) * 2, img.shape[1], img.shape[0],
+                                 pin_out.data_ptr(), pin_out.stride(0) * 2)
+            assert_same(pin_out.numpy(), want, f"host strip {strip}")
+        got = ctx.extract_host(img)  # pageable numpy buffers
+        assert_same(got, want, "host pageable")
+
+
+def test_pitched_and_offset_views():
+    img = scenes.scene_c1(size=160)
+    p = lfe.Params(bit_depth=8)
+    want = O.run(img, _oparams(p))
+    big = torch.zeros((170, 200), dtype=torch.uint8, device="cuda")
+    big[3:163, 5:165] = torch.from_numpy(img).cuda()
+    outbig = torch.zeros((165, 190), dtype=torch.uint8, device="cuda")
+    with lfe.Context(p) as ctx:
+        ctx.extract(big[3:163, 5:165], outbig[2:162, 1:161])
+        ctx.check()
+    assert_same(outbig[2:162, 1:161].cpu().numpy(), want, "pitched views")
+    assert not outbig[0:2].any() and not outbig[:, 0].any()
+
+
+def test_out_of_range_pixel_sets_erange():
+    img = np.full((50, 60), 100, np.uint16)
+    img[20, 30] = 1024
+    with lfe.Context(lfe.Params(bit_depth=10)) as ctx:
+        ctx.extract(torch.from_numpy(img).cuda())
+        assert ctx.last_async_error() == lfe.LFE_ERANGE
+        assert ctx.last_async_error() == lfe.LFE_OK  # cleared
+        ok = np.full((50, 60), 1023, np.uint16)
+        ctx.extract(torch.from_numpy(ok).cuda())
+        assert ctx.last_async_error() == lfe.LFE_OK
+
+
+def test_masks_from_device_ctx_equal_oracle():
+    with lfe.Context(lfe.Params(bit_depth=10)) as ctx:
+        for j, s in enumerate((0.5, 20.0)):
+            q, F, t = ctx.mask(j)
+            qo, Fo = O.mask_int(s, 5, 10)
+            assert F == Fo
+            np.testing.assert_array_equal(q, qo)
+
+
+def test_dihedral_covariance_on_device():
+    rng = np.random.default_rng(5)
+    img = scenes.random_image(rng, 77, 131, 8)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.0))
+    base = run_gpu(img, p)
+    for T in (lambda a: a.T, lambda a: a[::-1], lambda a: np.rot90(a)):
+        assert_same(run_gpu(np.ascontiguousarray(T(img)), p), T(base), "dihedral")

@@ -31,16 +31,34 @@ def _oparams(p: lfe.Params) -> O.Params:
                     hybrid_median=p.hybrid_median, median_window=p.median_window, out_mode=p.out_mode)
 
 
+def _pitched(shape, dtype):
+    """A 2-D CUDA view whose row pitch is a multiple of 16 bytes (fused-kernel
+    eligible) inside a larger zeroed allocation."""
+    H, W = shape
+    esz = torch.tensor([], dtype=dtype).element_size()
+    Wp = ((W * esz + 15) // 16) * 16 // esz + 16 // esz
+    return torch.zeros((H, Wp), dtype=dtype, device="cuda")[:, :W]
+
+
 def run_gpu(img: np.ndarray, p: lfe.Params, kernel=lfe.LFE_KERNEL_AUTO, tile=None):
     with lfe.Context(p) as ctx:
         ctx.set_option(lfe.LFE_OPT_KERNEL, kernel)
         if tile:
             ctx.set_option(lfe.LFE_OPT_TILE_W, tile[0])
             ctx.set_option(lfe.LFE_OPT_TILE_H, tile[1])
-        d = torch.from_numpy(np.ascontiguousarray(img)).cuda()
-        out = ctx.extract(d)
+        tin = torch.uint8 if p.bit_depth <= 8 else torch.uint16
+        tout = torch.uint8 if p.out_mode == lfe.LFE_OUT_MASK else tin
+        d = _pitched(img.shape, tin)
+        d.copy_(torch.from_numpy(np.ascontiguousarray(img)))
+        out = _pitched(img.shape, tout)
+        ctx.extract(d, out)
         ctx.check()
         return out.cpu().numpy()
+
+
+def fused_ok(p: lfe.Params) -> bool:
+    return (tuple(p.log_size) == (5, 5) and p.std_source == lfe.LFE_STD_ZC and p.std_window == 5
+            and max(p.std3_threshold) < 0 and (not p.hybrid_median or p.median_window == 5))
 
 
 def assert_same(got, want, what=""):
@@ -232,3 +250,39 @@ def test_dihedral_covariance_on_device():
     base = run_gpu(img, p)
     for T in (lambda a: a.T, lambda a: a[::-1], lambda a: np.rot90(a)):
         assert_same(run_gpu(np.ascontiguousarray(T(img)), p), T(base), "dihedral")
+
+
+# ------------------------------------------------ fused-kernel specifics ----
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4, 10])
+def test_fused_random_images(ci):
+    """The fused kernel forced on every shape (pitched buffers), bit-exact."""
+    p = list(_param_cases())[ci]
+    assert fused_ok(p)
+    rng = np.random.default_rng(200 + ci)
+    for (H, W), kind in itertools.product(SHAPES + [(33, 450), (9, 900), (129, 463)], ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, p.bit_depth, kind)
+        assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), f"{H}x{W} {kind}")
+
+
+@pytest.mark.parametrize("seg", [1, 3, 8, 17, 64, 128, 1000])
+def test_fused_segment_rows_invariance(seg):
+    """Rows per work item (LFE_OPT_TILE_H) never changes a bit."""
+    img = scenes.scene_c1(size=300)
+    for hm in (True, False):
+        p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.01), hybrid_median=hm)
+        want = O.run(img, _oparams(p))
+        assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED, (0, seg)), want, f"seg {seg} hm {hm}")
+
+
+@pytest.mark.parametrize("mode", [lfe.LFE_OUT_EXTRACT, lfe.LFE_OUT_MASK])
+@pytest.mark.parametrize("hm", [True, False])
+def test_fused_c2(mode, hm):
+    img = scenes.scene_c2()
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.02, 0.02), out_mode=mode, hybrid_median=hm)
+    assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), "c2 fused")
+
+
+def test_fused_equals_staged_on_c3_strip():
+    img = scenes.scene_c3(size=3000, height=700)
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), run_gpu(img, p, lfe.LFE_KERNEL_STAGED), "c3 strip")

@@ -20,7 +20,7 @@
 // Arithmetic.  Integer masks (R3) keep every partial LoG sum below 2^24, so the
 // LoG runs exactly in fp32 FFMA (FMA pipe).  The zero-crossing edge tests
 // (signs of r_p + r_n, |r_p - r_n| - t) are fp32 adds whose SIGN is exact;
-// their sign bits are packed into bit planes (byte per pixel, bit 0/4 per
+// their sign bits are packed into bit planes (byte per pixel, bit 3/7 per
 // branch) and the rule R* is evaluated bit-sliced, 8 pixel-branches per
 // LOP3.  The std gate counts zero crossings in bytes (exact integers) and
 // compares against the interval {k : 25k - k^2 > 600 T^2} (R11).  The hybrid
@@ -45,7 +45,6 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kWarpOut = 112;            // output columns per warp
 constexpr int kHaloX = 8;                // computed columns left of the output
 constexpr int kCtaOut = kWarps * kWarpOut;  // 448
-constexpr int kCtaCols = kCtaOut + 2 * kHaloX;  // 464 loaded columns
 constexpr int kR = 8;                    // rows per TMA stage
 constexpr int kS = 4;                    // ring stages
 
@@ -59,7 +58,7 @@ struct FusedArgs {
     int W, H;               // virtual image
     int o0, o1;             // output rows
     int col_groups, seg_rows, items;
-    int boxw;               // TMA box width in elements
+    int boxw;               // TMA box width in tensor-map elements (u16)
     void *out;
     long long out_pitch;
 };
@@ -251,9 +250,16 @@ __global__ void __launch_bounds__(kThreads, 3)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + kS;
     unsigned char *ring = smem + 128;
-    const int box_bytes = a.boxw * kR * kElem;
-    const int stage_bytes = 2 * box_bytes;
-    const int row_bytes = a.boxw * kElem;
+    // u16 images: two 232-pixel boxes per row starting at column xo-8.  u8
+    // images are loaded through a u16 view of the same bytes: one 240-element
+    // (480-pixel) box per row starting at column xo-16, because a TMA box must
+    // start on a 16-byte boundary (measured: scripts/tma_probe.cu).
+    constexpr int kNBox = IN16 ? 2 : 1;
+    constexpr int kBoxCols = IN16 ? 232 : 480;   // pixels per box
+    constexpr int kColOrg = IN16 ? 0 : 8;        // staged column of CTA-local column 0
+    constexpr int box_bytes = kBoxCols * kR * kElem;
+    constexpr int stage_bytes = kNBox * box_bytes;
+    constexpr int row_bytes = kBoxCols * kElem;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = a.W, H = a.H;
@@ -291,8 +297,12 @@ __global__ void __launch_bounds__(kThreads, 3)
             if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
             mbar_expect_tx(&full[slot], stage_bytes);
             unsigned char *dst = ring + slot * stage_bytes;
-            tma_load_2d(dst, &tmap, xo - kHaloX, plo + p_k * kR, &full[slot]);
-            tma_load_2d(dst + box_bytes, &tmap, xo - kHaloX + a.boxw, plo + p_k * kR, &full[slot]);
+            if constexpr (IN16) {
+                tma_load_2d(dst, &tmap, xo - kHaloX, plo + p_k * kR, &full[slot]);
+                tma_load_2d(dst + box_bytes, &tmap, xo - kHaloX + kBoxCols, plo + p_k * kR, &full[slot]);
+            } else {
+                tma_load_2d(dst, &tmap, (xo - 2 * kHaloX) / 2, plo + p_k * kR, &full[slot]);
+            }
             ++p_g;
             if (++p_k == nst) {
                 p_k = 0;
@@ -305,9 +315,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     // per-lane shared-memory offsets within a staged row (two TMA boxes side by side)
     const int cl = warp * kWarpOut + 4 * lane;  // CTA-local column of pixel 0
     auto col_off = [&](int c) {
-        c = max(0, min(c, 2 * a.boxw - 4));
-        const int b = c >= a.boxw;
-        return b * box_bytes + (c - b * a.boxw) * kElem;
+        c = max(0, min(c + kColOrg, kNBox * kBoxCols - 4));
+        const int b = c >= kBoxCols;
+        return b * box_bytes + (c - b * kBoxCols) * kElem;
     };
     const int off_own = col_off(cl), off_l = col_off(cl - 2), off_r = col_off(cl + 4);
 
@@ -338,6 +348,16 @@ __global__ void __launch_bounds__(kThreads, 3)
         fx.pxR = dr & 3;
         fx.any = fx.laneL >= 0 || fx.laneR >= 0;
         const bool warp_live = xw + kHaloX < W;  // has output columns inside the image
+        // bits of this lane's input words that belong to pixels inside the image (ERANGE check)
+        uint32_t in_lo = 0, in_hi = 0;
+        if constexpr (IN16) {
+            in_lo = (x0 < W ? 0xFFFFu : 0u) | (x0 + 1 < W ? 0xFFFF0000u : 0u);
+            in_hi = (x0 + 2 < W ? 0xFFFFu : 0u) | (x0 + 3 < W ? 0xFFFF0000u : 0u);
+        } else {
+            in_lo = (x0 < W ? 0xFFu : 0u) | (x0 + 1 < W ? 0xFF00u : 0u) | (x0 + 2 < W ? 0xFF0000u : 0u) |
+                    (x0 + 3 < W ? 0xFF000000u : 0u);
+        }
+        if (x0 < 0) in_lo = in_hi = 0;
 
         // ---- per-item stage state ----
         float acc[2][4][4];
@@ -370,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             float I[8];  // columns x0-2 .. x0+5
             if constexpr (IN16) {
                 const uint2 own = *reinterpret_cast<const uint2 *>(rowp + off_own);
-                range_acc |= own.x | own.y;
+                range_acc |= (own.x & in_lo) | (own.y & in_hi);
                 I[2] = lo16f(own.x);
                 I[3] = hi16f(own.x);
                 I[4] = lo16f(own.y);
@@ -385,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 }
             } else {
                 const uint32_t own = *reinterpret_cast<const uint32_t *>(rowp + off_own);
-                range_acc |= own;
+                range_acc |= own & in_lo;
                 I[2] = byte_f(own, 0x5440);
                 I[3] = byte_f(own, 0x5441);
                 I[4] = byte_f(own, 0x5442);
@@ -786,8 +806,7 @@ template <bool IN16, bool HM, bool MASKOUT, bool GAP>
 cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
 {
     auto kfn = fused_kernel<IN16, HM, MASKOUT, GAP>;
-    const int boxw = fa.boxw;
-    const size_t smem = 128 + (size_t)kS * 2 * boxw * kR * (IN16 ? 2 : 1);
+    const size_t smem = 128 + (size_t)kS * (IN16 ? 2 * 232 * 2 : 480) * kR;
     static int grid_cap = 0;
     if (!grid_cap) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -852,11 +871,13 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     if (fa.items <= 0) return cudaSuccess;
 
     CUtensorMap map;
-    const cuuint64_t dims[2] = {(cuuint64_t)g.width, (cuuint64_t)g.Hv};
+    // u8 rows are fetched as u16 pairs (the row pitch is a multiple of 16 bytes,
+    // so the pair holding an odd last pixel stays inside the row)
+    const cuuint64_t dims[2] = {(cuuint64_t)(in16 ? g.width : (g.width + 1) / 2), (cuuint64_t)g.Hv};
     const cuuint64_t strides[1] = {(cuuint64_t)g.in_pitch};
     const cuuint32_t box[2] = {(cuuint32_t)fa.boxw, (cuuint32_t)kR};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&map, in16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
                              const_cast<void *>(g.in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

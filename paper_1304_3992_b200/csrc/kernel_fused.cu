@@ -3,37 +3,40 @@
 // none): one persistent kernel, every stage fused, no HBM
 // traffic between stages.
 //
-// Work decomposition.  A CTA owns a 448-column x `segRows`-row output tile and
-// stages the tile plus its combined halo (8 columns, 7 rows = LoG 2 + ZC 1 +
-// std 2 + median 2; north_star) into a shared-memory ring with TMA
-// (cp.async.bulk.tensor, mbarrier completion).  Each of its 4 warps walks a
-// 128-column strip (112 output columns + 8 + 8 halo) down the rows; lane l
-// owns 4 adjacent columns.  Every stage keeps a sliding window of its last
-// rows in registers, so each input row is read from shared memory once:
+// Work decomposition.  A work item is a 448-column x `seg_rows`-row output
+// tile; CTAs take items from a global queue (atomic counter).  The CTA stages
+// the tile plus its combined halo (8 columns, 7 rows = LoG 2 + ZC 1 + std 2 +
+// median 2; north_star) into a shared-memory ring with TMA
+// (cp.async.bulk.tensor + mbarrier complete_tx), 8 rows per stage.  Each of
+// its 4 warps walks a 128-column strip (112 output columns + 8 + 8 halo) down
+// the rows; lane l owns 4 adjacent columns.  Per input row rho:
 //
-//   row rho  -> I, h1, h2 (fp32)      -> LoG x2, streaming  -> r(rho-2)
-//   r        -> ZC flags, rule R*     -> Z(rho-3)    (R6-R9)
-//   Z window -> 5x5 counts, Eq. 2     -> keep, OR    (R10-R14)
-//            -> E(rho-5) = I or 0     (R15)
-//   E window -> hybrid median         -> out(rho-7)  (R16)
+//   row rho  -> I, h1, h2 (fp32)      -> LoG x2, streaming  -> r(rho-2)   registers
+//   r        -> ZC flags, rule R*     -> Z(rho-3)           (R6-R9) -> Z ring (smem)
+//   Z ring   -> 5x5 counts, Eq. 2     -> keep, OR           (R10-R14)
+//            -> E(rho-5) = I or 0     (R15)                                      -> E ring (smem)
+//   E ring   -> hybrid median         -> out(rho-7)         (R16)   -> HBM
 //
 // Arithmetic.  Integer masks (R3) keep every partial LoG sum below 2^24, so the
 // LoG runs exactly in fp32 FFMA (FMA pipe).  The zero-crossing edge tests
 // (signs of r_p + r_n, |r_p - r_n| - t) are fp32 adds whose SIGN is exact;
-// their sign bits are packed into bit planes (byte per pixel, bit 3/7 per
-// branch) and the rule R* is evaluated bit-sliced, 8 pixel-branches per
-// LOP3.  The std gate counts zero crossings in bytes (exact integers) and
-// compares against the interval {k : 25k - k^2 > 600 T^2} (R11).  The hybrid
-// median is a sorting network on packed u16x2 (VIMNMX3.U16x2).
+// their sign bits are packed into flag words (byte per pixel, bit 3/7 per
+// branch) and rule R* is evaluated bit-sliced, 8 pixel-branches per LOP3.  The
+// std gate counts zero crossings in bytes (exact integers) and tests the
+// interval {k : 25k - k^2 > 600 T^2} (R11).  The hybrid median is a sorting
+// network on packed u16x2 (VIMNMX3.U16x2).
 //
-// Borders (R5): each stage pads its own input by replication.  Rows: when a
-// stage produces image row 0 its older window slots are filled with it; past
-// the last row the newest row is repeated.  Columns: in warps that touch the
-// image edge, each stage's values at outside columns are overwritten with the
-// edge column's value (warp shuffles) before the next stage reads them.
+// Borders (R5): each stage pads its own input by replication.  The Z and E
+// rings are read with row indices clamped to the image, which IS replicate
+// padding of those stages; the r stage repeats its first/last row explicitly;
+// at the left/right image edge each stage's values at outside columns are
+// overwritten with the edge column's value before the next stage reads them.
+// Only warps whose item touches an image edge take that (templated) path.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "lfe_internal.h"
 
@@ -42,11 +45,17 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kWarpOut = 112;            // output columns per warp
-constexpr int kHaloX = 8;                // computed columns left of the output
+constexpr int kWarpOut = 112;               // output columns per warp
+constexpr int kHaloX = 8;                   // computed columns left of the output
 constexpr int kCtaOut = kWarps * kWarpOut;  // 448
-constexpr int kR = 8;                    // rows per TMA stage
-constexpr int kS = 4;                    // ring stages
+constexpr int kR = 8;                       // rows per TMA stage (= rows per chunk)
+constexpr int kS = 4;                       // ring stages
+constexpr int kQ = 8;                       // item queue entries
+constexpr int kERow = 264;                  // bytes per E ring row: 128 px + 2 px pad each side
+constexpr int kEBytes = 8 * kERow;          // 8-row E ring per warp
+constexpr int kZBytes = 8 * 32 * 4;         // 8-row Z ring per warp
+constexpr int kRBytes = 2 * 32 * 32;        // 2-row r ring per warp (zero-pixel slow path)
+constexpr int kHdr = 128;                   // barriers + item queue
 
 struct FusedArgs {
     float c[2][6];          // orbit coefficients (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
@@ -58,9 +67,9 @@ struct FusedArgs {
     int W, H;               // virtual image
     int o0, o1;             // output rows
     int col_groups, seg_rows, items;
-    int boxw;               // TMA box width in tensor-map elements (u16)
     void *out;
     long long out_pitch;
+    int *work;              // work-queue counter (zeroed before the launch)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -126,7 +135,7 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b)
     return d;
 }
 
-// median of three packed pairs: min3 / max3 then the remaining element by XOR
+// median of three packed pairs: min3 / max3, then the remaining element by XOR
 __device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c)
 {
     uint32_t lo = vmin2(vmin2(a, b), c), hi = vmax2(vmax2(a, b), c);
@@ -147,8 +156,8 @@ __device__ __forceinline__ uint32_t med9(uint32_t v0, uint32_t v1, uint32_t v2, 
 // pixel pair shifted by one: (a.hi, b.lo)
 __device__ __forceinline__ uint32_t sh1(uint32_t a, uint32_t b) { return prmt(a, b, 0x5432); }
 
-// Pack the sign bits of v[branch][px] into the flag layout: byte px, bit 3 + 4*branch
-// (a funnel shift by 4 leaves each sign at the top of its nibble).
+// Sign bits of v[branch][px] -> flag layout: byte px, bit 3 + 4*branch (a
+// funnel shift by 4 leaves each sign at the top of its nibble).
 __device__ __forceinline__ uint32_t pack_signs(const float (&v)[2][4])
 {
     uint32_t w = __float_as_uint(v[1][3]) >> 28;
@@ -162,15 +171,15 @@ __device__ __forceinline__ uint32_t pack_signs(const float (&v)[2][4])
     return w & 0x88888888u;
 }
 
-// u16 -> exact fp32 (2^23 + v, minus 2^23)
+// u16 / u8 -> exact fp32 (2^23 + v, minus 2^23)
 __device__ __forceinline__ float lo16f(uint32_t w) { return __uint_as_float(prmt(w, 0x4B00u, 0x5410)) - 8388608.0f; }
 __device__ __forceinline__ float hi16f(uint32_t w) { return __uint_as_float(prmt(w, 0x4B00u, 0x5432)) - 8388608.0f; }
 __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uint_as_float(prmt(w, 0x4B00u, sel)) - 8388608.0f; }
 
+// ---- left/right image-edge fix-ups (border warps only) ----------------------
 struct Fix {
-    bool any;         // this warp touches a left or right image edge
-    int laneL, laneR, pxR;
-    uint32_t oobL, oobR;  // 4-bit masks of this lane's pixels outside [0, W)
+    int laneL, laneR, pxR;  // lane holding column 0 / column W-1 (-1: not in this warp)
+    uint32_t oobL, oobR;    // 4-bit masks of this lane's pixels outside [0, W)
 };
 
 __device__ __forceinline__ float pick4(const float (&v)[4], int k)
@@ -185,13 +194,13 @@ __device__ __forceinline__ float pick4(const float (&v)[4], int k)
 __device__ __forceinline__ void fix_floats(const Fix &f, float (&v)[4])
 {
     if (f.laneL >= 0) {
-        float e = __shfl_sync(0xffffffffu, v[0], f.laneL);
+        const float e = __shfl_sync(0xffffffffu, v[0], f.laneL);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             if (f.oobL >> i & 1) v[i] = e;
     }
     if (f.laneR >= 0) {
-        float e = __shfl_sync(0xffffffffu, pick4(v, f.pxR), f.laneR);
+        const float e = __shfl_sync(0xffffffffu, pick4(v, f.pxR), f.laneR);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             if (f.oobR >> i & 1) v[i] = e;
@@ -203,65 +212,138 @@ __device__ __forceinline__ uint32_t bytemask(uint32_t m4)
     return (m4 & 1 ? 0xFFu : 0u) | (m4 & 2 ? 0xFF00u : 0u) | (m4 & 4 ? 0xFF0000u : 0u) | (m4 & 8 ? 0xFF000000u : 0u);
 }
 
-// flag word: byte per pixel
 __device__ __forceinline__ uint32_t fix_bytes(const Fix &f, uint32_t w)
 {
     if (f.laneL >= 0) {
-        uint32_t e = (__shfl_sync(0xffffffffu, w, f.laneL) & 0xFFu) * 0x01010101u;
-        uint32_t m = bytemask(f.oobL);
+        const uint32_t e = (__shfl_sync(0xffffffffu, w, f.laneL) & 0xFFu) * 0x01010101u;
+        const uint32_t m = bytemask(f.oobL);
         w = (w & ~m) | (e & m);
     }
     if (f.laneR >= 0) {
-        uint32_t e = ((__shfl_sync(0xffffffffu, w, f.laneR) >> (8 * f.pxR)) & 0xFFu) * 0x01010101u;
-        uint32_t m = bytemask(f.oobR);
+        const uint32_t e = ((__shfl_sync(0xffffffffu, w, f.laneR) >> (8 * f.pxR)) & 0xFFu) * 0x01010101u;
+        const uint32_t m = bytemask(f.oobR);
         w = (w & ~m) | (e & m);
     }
     return w;
 }
 
-// two u16 pairs (pixels 0,1 | 2,3)
 __device__ __forceinline__ void fix_pairs(const Fix &f, uint32_t &p0, uint32_t &p1)
 {
     if (f.laneL >= 0) {
-        uint32_t e = (__shfl_sync(0xffffffffu, p0, f.laneL) & 0xFFFFu) * 0x00010001u;
-        uint32_t m0 = (f.oobL & 1 ? 0xFFFFu : 0u) | (f.oobL & 2 ? 0xFFFF0000u : 0u);
-        uint32_t m1 = (f.oobL & 4 ? 0xFFFFu : 0u) | (f.oobL & 8 ? 0xFFFF0000u : 0u);
+        const uint32_t e = (__shfl_sync(0xffffffffu, p0, f.laneL) & 0xFFFFu) * 0x00010001u;
+        const uint32_t m0 = (f.oobL & 1 ? 0xFFFFu : 0u) | (f.oobL & 2 ? 0xFFFF0000u : 0u);
+        const uint32_t m1 = (f.oobL & 4 ? 0xFFFFu : 0u) | (f.oobL & 8 ? 0xFFFF0000u : 0u);
         p0 = (p0 & ~m0) | (e & m0);
         p1 = (p1 & ~m1) | (e & m1);
     }
     if (f.laneR >= 0) {
-        uint32_t src = f.pxR < 2 ? p0 : p1;
-        uint32_t v = __shfl_sync(0xffffffffu, src, f.laneR);
-        uint32_t e = ((v >> (16 * (f.pxR & 1))) & 0xFFFFu) * 0x00010001u;
-        uint32_t m0 = (f.oobR & 1 ? 0xFFFFu : 0u) | (f.oobR & 2 ? 0xFFFF0000u : 0u);
-        uint32_t m1 = (f.oobR & 4 ? 0xFFFFu : 0u) | (f.oobR & 8 ? 0xFFFF0000u : 0u);
+        const uint32_t src = f.pxR < 2 ? p0 : p1;
+        const uint32_t v = __shfl_sync(0xffffffffu, src, f.laneR);
+        const uint32_t e = ((v >> (16 * (f.pxR & 1))) & 0xFFFFu) * 0x00010001u;
+        const uint32_t m0 = (f.oobR & 1 ? 0xFFFFu : 0u) | (f.oobR & 2 ? 0xFFFF0000u : 0u);
+        const uint32_t m1 = (f.oobR & 4 ? 0xFFFFu : 0u) | (f.oobR & 8 ? 0xFFFF0000u : 0u);
         p0 = (p0 & ~m0) | (e & m0);
         p1 = (p1 & ~m1) | (e & m1);
     }
 }
+
+// ---- work items ---------------------------------------------------------------
+struct Item {
+    int ys, ye, plo, phi, xo, nst;
+};
+
+template <int kLag>
+__device__ __forceinline__ Item item_geo(const FusedArgs &a, int id)
+{
+    Item it;
+    const int rs = id / a.col_groups, cg = id - rs * a.col_groups;
+    it.ys = a.o0 + rs * a.seg_rows;
+    it.ye = min(it.ys + a.seg_rows, a.o1);
+    it.plo = max(0, it.ys - kLag);
+    it.phi = min(a.H, it.ye + kLag);
+    it.xo = cg * kCtaOut;
+    it.nst = (it.phi - it.plo + kR - 1) / kR;
+    return it;
+}
+
+// ---- TMA producer (thread 0 only) ----------------------------------------------
+template <bool IN16, int kLag, int kStageBytes, int kBoxBytes, int kBoxCols>
+struct Producer {
+    const FusedArgs *a;
+    const CUtensorMap *map;
+    uint64_t *full, *empty;
+    int *queue;
+    unsigned char *ring;
+    Item it;
+    int id = -1, k = 0;
+    uint32_t g = 0, idx = 0;
+    bool done = false;
+
+    // issue stages while fewer than kS are outstanding beyond `released`
+    __device__ __forceinline__ void run(uint32_t released)
+    {
+        while (!done && g < released + kS) {
+            if (id < 0) {
+                const int nid = atomicAdd(a->work, 1);
+                const int slot = g % kS;
+                const uint32_t use = g / kS;
+                if (nid >= a->items) {  // no more work: post the sentinel on its own ring slot
+                    queue[idx % kQ] = -1;
+                    if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
+                    mbar_arrive(&full[slot]);
+                    done = true;
+                    return;
+                }
+                id = nid;
+                it = item_geo<kLag>(*a, id);
+                k = 0;
+                queue[idx % kQ] = id;
+                ++idx;
+            }
+            const int slot = g % kS;
+            const uint32_t use = g / kS;
+            if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
+            mbar_expect_tx(&full[slot], kStageBytes);
+            unsigned char *dst = ring + slot * kStageBytes;
+            const int y = it.plo + k * kR;
+            if constexpr (IN16) {
+                tma_load_2d(dst, map, it.xo - kHaloX, y, &full[slot]);
+                tma_load_2d(dst + kBoxBytes, map, it.xo - kHaloX + kBoxCols, y, &full[slot]);
+            } else {
+                tma_load_2d(dst, map, (it.xo - 2 * kHaloX) / 2, y, &full[slot]);
+            }
+            ++g;
+            if (++k == it.nst) id = -1;
+        }
+    }
+};
 
 template <bool IN16, bool HM, bool MASKOUT, bool GAP>
 __global__ void __launch_bounds__(kThreads, 3)
     fused_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ FusedArgs a, int *err_flag)
 {
     constexpr int kElem = IN16 ? 2 : 1;
-    constexpr int kLag = HM ? 7 : 5;  // output row = input row - kLag; also the row halo
+    constexpr int kLag = HM ? 7 : 5;  // output row = input row - kLag (= row halo)
+    // u16 images: two 232-pixel boxes per row starting at column xo-8.  u8 images
+    // are loaded through a u16 view of the same bytes: one 240-element (480-pixel)
+    // box per row starting at column xo-16 -- a TMA box must start on a 16-byte
+    // boundary (measured: scripts/tma_probe.cu).
+    constexpr int kNBox = IN16 ? 2 : 1;
+    constexpr int kBoxCols = IN16 ? 232 : 480;
+    constexpr int kColOrg = IN16 ? 0 : 8;
+    constexpr int kBoxBytes = kBoxCols * kR * kElem;
+    constexpr int kStageBytes = kNBox * kBoxBytes;
+    constexpr int kRowBytes = kBoxCols * kElem;
+
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + kS;
-    unsigned char *ring = smem + 128;
-    // u16 images: two 232-pixel boxes per row starting at column xo-8.  u8
-    // images are loaded through a u16 view of the same bytes: one 240-element
-    // (480-pixel) box per row starting at column xo-16, because a TMA box must
-    // start on a 16-byte boundary (measured: scripts/tma_probe.cu).
-    constexpr int kNBox = IN16 ? 2 : 1;
-    constexpr int kBoxCols = IN16 ? 232 : 480;   // pixels per box
-    constexpr int kColOrg = IN16 ? 0 : 8;        // staged column of CTA-local column 0
-    constexpr int box_bytes = kBoxCols * kR * kElem;
-    constexpr int stage_bytes = kNBox * box_bytes;
-    constexpr int row_bytes = kBoxCols * kElem;
-
+    int *queue = reinterpret_cast<int *>(empty + kS);
+    unsigned char *ring = smem + kHdr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *eRing = ring + kS * kStageBytes + warp * (kEBytes + kZBytes + kRBytes);
+    uint32_t *zRing = reinterpret_cast<uint32_t *>(eRing + kEBytes);
+    float4 *rRing = reinterpret_cast<float4 *>(eRing + kEBytes + kZBytes);  // [2 rows][32 lanes][2 float4]
     const int W = a.W, H = a.H;
 
     if (threadIdx.x == 0) {
@@ -274,69 +356,428 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     __syncthreads();
 
-    // ---- producer state (thread 0): walks the same item/stage sequence ----
-    int p_item = blockIdx.x, p_k = 0;
-    uint32_t p_g = 0;            // stages issued
-    uint32_t rel0 = 0;           // stages released by warp 0 (producer throttle)
-    auto item_rows = [&](int item, int &ys, int &ye, int &plo, int &phi, int &xo) {
-        const int rs = item / a.col_groups, cg = item - rs * a.col_groups;
-        ys = a.o0 + rs * a.seg_rows;
-        ye = min(ys + a.seg_rows, a.o1);
-        plo = max(0, ys - kLag);
-        phi = min(H, ye + kLag);
-        xo = cg * kCtaOut;
-    };
-    auto produce = [&]() {
-        // issue stages while warp 0 has released enough slots
-        while (p_item < a.items && p_g < rel0 + kS) {
-            int ys, ye, plo, phi, xo;
-            item_rows(p_item, ys, ye, plo, phi, xo);
-            const int nst = (phi - plo + kR - 1) / kR;
-            const int slot = p_g % kS;
-            const uint32_t use = p_g / kS;
-            if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
-            mbar_expect_tx(&full[slot], stage_bytes);
-            unsigned char *dst = ring + slot * stage_bytes;
-            if constexpr (IN16) {
-                tma_load_2d(dst, &tmap, xo - kHaloX, plo + p_k * kR, &full[slot]);
-                tma_load_2d(dst + box_bytes, &tmap, xo - kHaloX + kBoxCols, plo + p_k * kR, &full[slot]);
-            } else {
-                tma_load_2d(dst, &tmap, (xo - 2 * kHaloX) / 2, plo + p_k * kR, &full[slot]);
-            }
-            ++p_g;
-            if (++p_k == nst) {
-                p_k = 0;
-                p_item += gridDim.x;
-            }
-        }
-    };
-    if (threadIdx.x == 0) produce();
+    Producer<IN16, kLag, kStageBytes, kBoxBytes, kBoxCols> prod;
+    prod.a = &a;
+    prod.map = &tmap;
+    prod.full = full;
+    prod.empty = empty;
+    prod.queue = queue;
+    prod.ring = ring;
+    uint32_t rel_w = 0;  // stages this warp has released (thread 0: throttles the producer)
+    if (threadIdx.x == 0) prod.run(0);
 
-    // per-lane shared-memory offsets within a staged row (two TMA boxes side by side)
-    const int cl = warp * kWarpOut + 4 * lane;  // CTA-local column of pixel 0
     auto col_off = [&](int c) {
         c = max(0, min(c + kColOrg, kNBox * kBoxCols - 4));
         const int b = c >= kBoxCols;
-        return b * box_bytes + (c - b * kBoxCols) * kElem;
+        return b * kBoxBytes + (c - b * kBoxCols) * kElem;
     };
+    const int cl = warp * kWarpOut + 4 * lane;  // CTA-local column of this lane's pixel 0
     const int off_own = col_off(cl), off_l = col_off(cl - 2), off_r = col_off(cl + 4);
 
-    const float c00[2] = {a.c[0][0], a.c[1][0]}, c10[2] = {a.c[0][1], a.c[1][1]}, c20[2] = {a.c[0][2], a.c[1][2]};
-    const float c11[2] = {a.c[0][3], a.c[1][3]}, c21[2] = {a.c[0][4], a.c[1][4]}, c22[2] = {a.c[0][5], a.c[1][5]};
+    float c00[2], c10[2], c20[2], c11[2], c21[2], c22[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        c00[j] = a.c[j][0];
+        c10[j] = a.c[j][1];
+        c20[j] = a.c[j][2];
+        c11[j] = a.c[j][3];
+        c21[j] = a.c[j][4];
+        c22[j] = a.c[j][5];
+    }
 
-    uint32_t g_base = 0;  // consumer: global stage index of the current item's stage 0
-    uint32_t range_acc = 0;
+    uint32_t g_base = 0, c_idx = 0, range_acc = 0;
 
-    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
-        int ys, ye, plo, phi, xo;
-        item_rows(item, ys, ye, plo, phi, xo);
-        const int nst = (phi - plo + kR - 1) / kR;
-        const int xw = xo - kHaloX + warp * kWarpOut;  // image column of this warp's column 0
-        const int x0 = xw + 4 * lane;                  // this lane's pixel 0
+    // ---- per-item state, shared by the step lambda --------------------------
+    Item it;
+    int waited = 0, released = 0, x0 = 0;
+    Fix fx;
+    uint32_t in_lo = 0, in_hi = 0;
+    float acc[2][4][4];
+    uint32_t PA, NA, PB, NB, Um, Up, Ung, V;
 
-        Fix fx;
-        fx.oobL = 0;
-        fx.oobR = 0;
+    auto row_ptr = [&](int p) -> const unsigned char * {
+        const int d = p - it.plo;
+        return ring + ((g_base + (d >> 3)) % kS) * kStageBytes + (d & 7) * kRowBytes;
+    };
+    auto prow = [&](int rho) { return min(max(rho, it.plo), it.phi - 1); };
+
+    auto store = [&](int row, uint32_t o0, uint32_t o1) {
+        if (lane < 2 || lane >= 30) return;
+        char *orow = reinterpret_cast<char *>(a.out) + (long long)(row - a.o0) * a.out_pitch;
+        if (IN16 && !MASKOUT) {
+            if (x0 + 3 < W) {
+                *reinterpret_cast<uint2 *>(orow + 2LL * x0) = make_uint2(o0, o1);
+            } else {
+                uint16_t *p = reinterpret_cast<uint16_t *>(orow);
+                if (x0 < W) p[x0] = (uint16_t)o0;
+                if (x0 + 1 < W) p[x0 + 1] = (uint16_t)(o0 >> 16);
+                if (x0 + 2 < W) p[x0 + 2] = (uint16_t)o1;
+            }
+        } else {
+            const uint32_t b = prmt(o0, o1, 0x6420);
+            if (x0 + 3 < W) {
+                *reinterpret_cast<uint32_t *>(orow + x0) = b;
+            } else {
+                uint8_t *p = reinterpret_cast<uint8_t *>(orow);
+                if (x0 < W) p[x0] = (uint8_t)b;
+                if (x0 + 1 < W) p[x0 + 1] = (uint8_t)(b >> 8);
+                if (x0 + 2 < W) p[x0 + 2] = (uint8_t)(b >> 16);
+            }
+        }
+    };
+
+    // ---- one row step: input row rho, centre r row rB = r(rho-3), new r row rC = r(rho-2)
+    auto step = [&](auto fix_tag, int rho, float(&rB)[2][4], float(&rC)[2][4]) {
+        constexpr bool FIX = decltype(fix_tag)::value;
+        // ---------------- input row ----------------
+        const unsigned char *rowp = row_ptr(prow(rho));
+        float I[8];  // columns x0-2 .. x0+5
+        if constexpr (IN16) {
+            const uint2 own = *reinterpret_cast<const uint2 *>(rowp + off_own);
+            range_acc |= (own.x & in_lo) | (own.y & in_hi);
+            I[2] = lo16f(own.x);
+            I[3] = hi16f(own.x);
+            I[4] = lo16f(own.y);
+            I[5] = hi16f(own.y);
+            if constexpr (!FIX) {
+                const uint32_t wl = *reinterpret_cast<const uint32_t *>(rowp + off_l);
+                const uint32_t wr = *reinterpret_cast<const uint32_t *>(rowp + off_r);
+                I[0] = lo16f(wl);
+                I[1] = hi16f(wl);
+                I[6] = lo16f(wr);
+                I[7] = hi16f(wr);
+            }
+        } else {
+            const uint32_t own = *reinterpret_cast<const uint32_t *>(rowp + off_own);
+            range_acc |= own & in_lo;
+            I[2] = byte_f(own, 0x5440);
+            I[3] = byte_f(own, 0x5441);
+            I[4] = byte_f(own, 0x5442);
+            I[5] = byte_f(own, 0x5443);
+            if constexpr (!FIX) {
+                const uint32_t wl = *reinterpret_cast<const uint16_t *>(rowp + off_l);
+                const uint32_t wr = *reinterpret_cast<const uint16_t *>(rowp + off_r);
+                I[0] = byte_f(wl, 0x5440);
+                I[1] = byte_f(wl, 0x5441);
+                I[6] = byte_f(wr, 0x5440);
+                I[7] = byte_f(wr, 0x5441);
+            }
+        }
+        if constexpr (FIX) {
+            float own4[4] = {I[2], I[3], I[4], I[5]};
+            fix_floats(fx, own4);
+            I[2] = own4[0];
+            I[3] = own4[1];
+            I[4] = own4[2];
+            I[5] = own4[3];
+            I[0] = __shfl_up_sync(0xffffffffu, I[4], 1);
+            I[1] = __shfl_up_sync(0xffffffffu, I[5], 1);
+            I[6] = __shfl_down_sync(0xffffffffu, I[2], 1);
+            I[7] = __shfl_down_sync(0xffffffffu, I[3], 1);
+        }
+
+        // ---------------- LoG x 2, streaming over rows ----------------
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float x = I[i + 2], h1 = I[i + 1] + I[i + 3], h2 = I[i] + I[i + 4];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                // row rho gets A, rows rho+-1 get B, rows rho+-2 get C (chains start at +0: never -0)
+                const float A = fmaf(c00[j], x, fmaf(c10[j], h1, fmaf(c20[j], h2, acc[j][2][i])));
+                const float B = fmaf(c21[j], h2, fmaf(c11[j], h1, fmaf(c10[j], x, 0.0f)));
+                const float C = fmaf(c22[j], h2, fmaf(c21[j], h1, fmaf(c20[j], x, 0.0f)));
+                rC[j][i] = acc[j][0][i] + C;
+                acc[j][0][i] = acc[j][1][i] + B;
+                acc[j][1][i] = A;
+                acc[j][2][i] = acc[j][3][i] + B;
+                acc[j][3][i] = C;
+            }
+        }
+        const int row_r = rho - 2;
+        if constexpr (FIX) {
+            if (row_r > H - 1) {  // past the bottom: r(H..) = r(H-1)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) rC[j][i] = rB[j][i];
+            } else {
+                fix_floats(fx, rC[0]);
+                fix_floats(fx, rC[1]);
+            }
+        }
+
+        // ---------------- zero crossings of row rho-3 (rule R*) ----------------
+        float rn[2][4];  // right neighbours in row B
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            rn[j][0] = rB[j][1];
+            rn[j][1] = rB[j][2];
+            rn[j][2] = rB[j][3];
+            rn[j][3] = __shfl_down_sync(0xffffffffu, rB[j][0], 1);
+        }
+        float t[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[j][i] = 0.0f - rC[j][i];
+        const uint32_t PC = pack_signs(t), NC = pack_signs(rC);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[j][i] = rB[j][i] + rC[j][i];
+        const uint32_t Dm = pack_signs(t);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[j][i] = -rB[j][i] - rC[j][i];
+        const uint32_t Dp = pack_signs(t);
+        uint32_t Dng = 0, Rng = 0;
+        if constexpr (GAP) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) t[j][i] = fabsf(rB[j][i] - rC[j][i]) - a.tg[j];
+            Dng = pack_signs(t);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[j][i] = rB[j][i] + rn[j][i];
+        const uint32_t Rm = pack_signs(t);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[j][i] = -rB[j][i] - rn[j][i];
+        const uint32_t Rp = pack_signs(t);
+        if constexpr (GAP) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) t[j][i] = fabsf(rB[j][i] - rn[j][i]) - a.tg[j];
+            Rng = pack_signs(t);
+        }
+        // neighbours' flag bytes across lanes
+        const uint32_t PL = prmt(PB, __shfl_up_sync(0xffffffffu, PB, 1), 0x2107);
+        const uint32_t NL = prmt(NB, __shfl_up_sync(0xffffffffu, NB, 1), 0x2107);
+        const uint32_t PR = prmt(PB, __shfl_down_sync(0xffffffffu, PB, 1), 0x4321);
+        const uint32_t NR = prmt(NB, __shfl_down_sync(0xffffffffu, NB, 1), 0x4321);
+        const uint32_t Lm = prmt(Rm, __shfl_up_sync(0xffffffffu, Rm, 1), 0x2107);
+        const uint32_t Lp = prmt(Rp, __shfl_up_sync(0xffffffffu, Rp, 1), 0x2107);
+        // violations: an opposite-sign neighbour of smaller magnitude (R7; ties allowed, R8)
+        const uint32_t X = (NA & Up) | (NC & Dp) | (NR & Rp) | (NL & Lp);
+        const uint32_t Y = (PA & Um) | (PC & Dm) | (PR & Rm) | (PL & Lm);
+        uint32_t XG, YG;
+        if constexpr (GAP) {
+            const uint32_t Lng = prmt(Rng, __shfl_up_sync(0xffffffffu, Rng, 1), 0x2107);
+            XG = (NA & ~Ung) | (NC & ~Dng) | (NR & ~Rng) | (NL & ~Lng);
+            YG = (PA & ~Ung) | (PC & ~Dng) | (PR & ~Rng) | (PL & ~Lng);
+        } else {
+            XG = NA | NC | NR | NL;
+            YG = PA | PC | PR | PL;
+        }
+        uint32_t Z = (PB & ~X & XG) | (NB & ~Y & YG);
+        // a pixel exactly at zero: a positive and a negative neighbour (R6)
+        const uint32_t z0 = ~PB & ~NB & (PA | PC | PR | PL) & (NA | NC | NR | NL) & 0x88888888u;
+        if constexpr (!GAP) {
+            Z |= z0;
+        } else {
+            if (__any_sync(0xffffffffu, z0 != 0)) {  // rare: also needs max - min >= t
+                const float4 *up = rRing + (((rho - 4) & 1) * 32 + lane) * 2;  // r(rho-4), stored last step
+                const float4 u0 = up[0], u1 = up[1];
+                const float rU[2][4] = {{u0.x, u0.y, u0.z, u0.w}, {u1.x, u1.y, u1.z, u1.w}};
+                const float l0 = __shfl_up_sync(0xffffffffu, rB[0][3], 1);
+                const float l1 = __shfl_up_sync(0xffffffffu, rB[1][3], 1);
+                if (z0) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            if (!(z0 >> (8 * i + 3 + 4 * j) & 1)) continue;
+                            const float left = i == 0 ? (j == 0 ? l0 : l1) : rB[j][i > 0 ? i - 1 : 0];
+                            const float mx = fmaxf(fmaxf(rU[j][i], rC[j][i]), fmaxf(left, rn[j][i]));
+                            const float mn = fminf(fminf(rU[j][i], rC[j][i]), fminf(left, rn[j][i]));
+                            if (mx - mn >= a.tg[j]) Z |= 1u << (8 * i + 3 + 4 * j);
+                        }
+                }
+            }
+            // keep r(rho-3) for the next step's slow path (and r(-1) := r(0) at the top)
+            float4 *me = rRing + (((rho - 3) & 1) * 32 + lane) * 2;
+            me[0] = make_float4(rB[0][0], rB[0][1], rB[0][2], rB[0][3]);
+            me[1] = make_float4(rB[1][0], rB[1][1], rB[1][2], rB[1][3]);
+            if constexpr (FIX) {
+                if (row_r == 0) {
+                    float4 *m2 = rRing + (((rho - 3) & 1) * 32 + lane) * 2;  // slot read as r(-1) next step
+                    m2[0] = make_float4(rC[0][0], rC[0][1], rC[0][2], rC[0][3]);
+                    m2[1] = make_float4(rC[1][0], rC[1][1], rC[1][2], rC[1][3]);
+                }
+            }
+        }
+        Z >>= 3;  // Z at bit 0 (branch 0) / bit 4 (branch 1) of each pixel byte: counts add per byte
+        if constexpr (FIX) Z = fix_bytes(fx, Z);
+        const int row_z = rho - 3;
+        // shift the ZC state
+        PA = PB;
+        NA = NB;
+        PB = PC;
+        NB = NC;
+        Um = Dm;
+        Up = Dp;
+        Ung = Dng;
+        if constexpr (FIX) {
+            if (row_r == 0) {  // top edge reached by r: r(-1) := r(0)
+                PA = PB;
+                NA = NB;
+                Um = NB;
+                Up = PB;
+                Ung = a.ung_top;
+            }
+        }
+
+        // ---------------- Z ring + std gate + merge for row rho-5 ----------------
+        const int row_e = rho - 5;
+        uint32_t Zc;
+        if constexpr (!FIX) {
+            const uint32_t z_old = zRing[((row_z - 5) & 7) * 32 + lane];
+            zRing[(row_z & 7) * 32 + lane] = Z;
+            V = V + Z - z_old;  // running 5-row count (bytes, no carries: <= 5 per nibble)
+            Zc = zRing[((row_z - 2) & 7) * 32 + lane];
+        } else {
+            if (row_z >= 0 && row_z <= H - 1) zRing[(row_z & 7) * 32 + lane] = Z;
+            V = 0;
+#pragma unroll
+            for (int k = -2; k <= 2; ++k) V += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
+            Zc = zRing[(min(max(row_e, 0), H - 1) & 7) * 32 + lane];
+        }
+        const uint32_t V0 = V & 0x0F0F0F0Fu, V1 = (V >> 4) & 0x0F0F0F0Fu;
+        const uint32_t Lw = __shfl_up_sync(0xffffffffu, prmt(V0, V1, 0x7632), 1);
+        const uint32_t Rw = __shfl_down_sync(0xffffffffu, prmt(V0, V1, 0x5410), 1);
+        const uint32_t K0 = V0 + prmt(V0, Lw, 0x2105) + prmt(V0, Lw, 0x1054) + prmt(V0, Rw, 0x4321) + prmt(V0, Rw, 0x5432);
+        const uint32_t K1 = V1 + prmt(V1, Lw, 0x2107) + prmt(V1, Lw, 0x1076) + prmt(V1, Rw, 0x6321) + prmt(V1, Rw, 0x7632);
+        const uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
+        const uint32_t pass1 = (K1 + a.add_lo[1]) & ~(K1 + a.add_hi[1]) & 0x80808080u;
+        const uint32_t M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
+        uint32_t e0, e1;                                              // E pairs of row rho-5
+        {
+            uint32_t i0, i1;
+            if constexpr (MASKOUT) {
+                i0 = i1 = 0x00FF00FFu;
+            } else {
+                const unsigned char *rp = row_ptr(prow(row_e));
+                if constexpr (IN16) {
+                    const uint2 own = *reinterpret_cast<const uint2 *>(rp + off_own);
+                    i0 = own.x;
+                    i1 = own.y;
+                } else {
+                    const uint32_t own = *reinterpret_cast<const uint32_t *>(rp + off_own);
+                    i0 = prmt(own, 0, 0x4140);
+                    i1 = prmt(own, 0, 0x4342);
+                }
+            }
+            e0 = i0 & prmt(M7, 0, 0x9988);
+            e1 = i1 & prmt(M7, 0, 0xBBAA);
+            if constexpr (FIX) fix_pairs(fx, e0, e1);
+        }
+
+        if constexpr (HM) {
+            uint32_t *erow = reinterpret_cast<uint32_t *>(eRing + (row_e & 7) * kERow + 4 + 8 * lane);
+            if (!FIX || (row_e >= 0 && row_e <= H - 1)) {
+                erow[0] = e0;
+                erow[1] = e1;
+            }
+            __syncwarp();
+            // ---------------- hybrid median for row rho-7 ----------------
+            const int row_o = rho - 7;
+            if (row_o >= it.ys && row_o < it.ye) {
+                uint32_t E[5][4];  // rows row_o-2 .. row_o+2: (x-2,x-1) (x,x+1) (x+2,x+3) (x+4,x+5)
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    int r = row_o - 2 + k;
+                    if constexpr (FIX) r = min(max(r, 0), H - 1);
+                    const unsigned char *b = eRing + (r & 7) * kERow + 8 * lane;
+                    const uint2 lo = *reinterpret_cast<const uint2 *>(b);
+                    const uint2 hi = *reinterpret_cast<const uint2 *>(b + 8);
+                    E[k][0] = lo.x;
+                    E[k][1] = lo.y;
+                    E[k][2] = hi.x;
+                    E[k][3] = hi.y;
+                }
+                const uint32_t s2a = sh1(E[2][0], E[2][1]), s2b = sh1(E[2][1], E[2][2]), s2c = sh1(E[2][2], E[2][3]);
+                const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
+                const uint32_t s3a = sh1(E[3][0], E[3][1]), s3b = sh1(E[3][1], E[3][2]), s3c = sh1(E[3][2], E[3][3]);
+                const uint32_t c0 = E[2][1];
+                const uint32_t mp0 = med9(E[2][0], s2a, c0, s2b, E[2][2], E[0][1], E[1][1], E[3][1], E[4][1]);
+                const uint32_t mx0 = med9(E[0][0], s1a, s3b, E[4][2], E[0][2], s1b, s3a, E[4][0], c0);
+                const uint32_t o0 = med3(mp0, mx0, c0);
+                const uint32_t c1 = E[2][2];
+                const uint32_t mp1 = med9(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
+                const uint32_t mx1 = med9(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
+                const uint32_t o1 = med3(mp1, mx1, c1);
+                store(row_o, o0, o1);
+            }
+        } else {
+            if (row_e >= it.ys && row_e < it.ye) store(row_e, e0, e1);
+        }
+    };
+
+    // ---- walk every row of the current item ---------------------------------
+    auto walk = [&](auto fix_tag) {
+        constexpr bool FIX = decltype(fix_tag)::value;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][0][i] = acc[j][1][i] = acc[j][2][i] = acc[j][3][i] = 0.0f;
+        PA = NA = PB = NB = Um = Up = Ung = 0;
+        V = 0;
+        if constexpr (!FIX) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) zRing[k * 32 + lane] = 0;
+        }
+        __syncwarp();
+        float rX[2][4], rY[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rX[j][i] = rY[j][i] = 0.0f;
+
+        const int rho_end = it.ye + kLag;
+        for (int rho = it.ys - kLag; rho < rho_end; rho += kR) {
+            // wait for the ring stages holding this chunk's input rows
+            const int st = (prow(rho + kR - 1) - it.plo) >> 3;
+            while (waited < st) {
+                ++waited;
+                const uint32_t g = g_base + waited;
+                mbar_wait(&full[g % kS], (g / kS) & 1);
+            }
+            const int n = min(kR, rho_end - rho);
+            for (int k = 0; k < n; k += 2) {
+                step(fix_tag, rho + k, rX, rY);
+                step(fix_tag, rho + k + 1, rY, rX);
+            }
+            // release ring stages that no later step reads (the E stage reads row rho-5)
+            const int next_e = prow(rho + n - 5);
+            __syncwarp();
+            while (released < it.nst && it.plo + (released + 1) * kR <= next_e) {
+                if (lane == 0) mbar_arrive(&empty[(g_base + released) % kS]);
+                ++released;
+                ++rel_w;
+            }
+            if (threadIdx.x == 0) prod.run(rel_w);
+            __syncwarp();
+        }
+    };
+
+    // ---- item loop -------------------------------------------------------------
+    for (;;) {
+        mbar_wait(&full[g_base % kS], (g_base / kS) & 1);  // first stage of the next item (or the sentinel)
+        const int id = queue[c_idx % kQ];
+        if (id < 0) break;
+        ++c_idx;
+        it = item_geo<kLag>(a, id);
+        waited = 0;
+        released = 0;
+        const int xw = it.xo - kHaloX + warp * kWarpOut;  // image column of this warp's column 0
+        x0 = xw + 4 * lane;
+        fx.oobL = fx.oobR = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             fx.oobL |= (x0 + i < 0 ? 1u : 0u) << i;
@@ -346,10 +787,6 @@ __global__ void __launch_bounds__(kThreads, 3)
         const int dr = W - 1 - xw;
         fx.laneR = (xw + 128 > W && dr >= 0) ? dr >> 2 : -1;
         fx.pxR = dr & 3;
-        fx.any = fx.laneL >= 0 || fx.laneR >= 0;
-        const bool warp_live = xw + kHaloX < W;  // has output columns inside the image
-        // bits of this lane's input words that belong to pixels inside the image (ERANGE check)
-        uint32_t in_lo = 0, in_hi = 0;
         if constexpr (IN16) {
             in_lo = (x0 < W ? 0xFFFFu : 0u) | (x0 + 1 < W ? 0xFFFF0000u : 0u);
             in_hi = (x0 + 2 < W ? 0xFFFFu : 0u) | (x0 + 3 < W ? 0xFFFF0000u : 0u);
@@ -358,406 +795,21 @@ __global__ void __launch_bounds__(kThreads, 3)
                     (x0 + 3 < W ? 0xFF000000u : 0u);
         }
         if (x0 < 0) in_lo = in_hi = 0;
-
-        // ---- per-item stage state ----
-        float acc[2][4][4];
-        float rA[2][4], rB[2][4];
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[j][0][i] = acc[j][1][i] = acc[j][2][i] = acc[j][3][i] = 0.0f;
-                rA[j][i] = rB[j][i] = 0.0f;
-            }
-        uint32_t PA = 0, NA = 0, PB = 0, NB = 0, Um = 0, Up = 0, Ung = 0;
-        uint32_t Zw[5] = {0, 0, 0, 0, 0};
-        uint32_t E[5][4];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) E[k][0] = E[k][1] = E[k][2] = E[k][3] = 0;
-
-        int waited = -1, released = 0;
-
-        for (int rho = ys - kLag; rho < ye + kLag; ++rho) {
-            // ---------------- input row ----------------
-            const int pin = min(max(rho, 0), H - 1);
-            const int st = (pin - plo) / kR;
-            while (waited < st) {
-                ++waited;
-                const uint32_t g = g_base + waited;
-                mbar_wait(&full[g % kS], (g / kS) & 1);
-            }
-            const unsigned char *rowp = ring + ((g_base + st) % kS) * stage_bytes + ((pin - plo) % kR) * row_bytes;
-            float I[8];  // columns x0-2 .. x0+5
-            if constexpr (IN16) {
-                const uint2 own = *reinterpret_cast<const uint2 *>(rowp + off_own);
-                range_acc |= (own.x & in_lo) | (own.y & in_hi);
-                I[2] = lo16f(own.x);
-                I[3] = hi16f(own.x);
-                I[4] = lo16f(own.y);
-                I[5] = hi16f(own.y);
-                if (!fx.any) {
-                    const uint32_t wl = *reinterpret_cast<const uint32_t *>(rowp + off_l);
-                    const uint32_t wr = *reinterpret_cast<const uint32_t *>(rowp + off_r);
-                    I[0] = lo16f(wl);
-                    I[1] = hi16f(wl);
-                    I[6] = lo16f(wr);
-                    I[7] = hi16f(wr);
-                }
-            } else {
-                const uint32_t own = *reinterpret_cast<const uint32_t *>(rowp + off_own);
-                range_acc |= own & in_lo;
-                I[2] = byte_f(own, 0x5440);
-                I[3] = byte_f(own, 0x5441);
-                I[4] = byte_f(own, 0x5442);
-                I[5] = byte_f(own, 0x5443);
-                if (!fx.any) {
-                    const uint32_t wl = *reinterpret_cast<const uint16_t *>(rowp + off_l);
-                    const uint32_t wr = *reinterpret_cast<const uint16_t *>(rowp + off_r);
-                    I[0] = byte_f(wl, 0x5440);
-                    I[1] = byte_f(wl, 0x5441);
-                    I[6] = byte_f(wr, 0x5440);
-                    I[7] = byte_f(wr, 0x5441);
-                }
-            }
-            if (fx.any) {
-                float own4[4] = {I[2], I[3], I[4], I[5]};
-                fix_floats(fx, own4);
-                I[2] = own4[0];
-                I[3] = own4[1];
-                I[4] = own4[2];
-                I[5] = own4[3];
-                I[0] = __shfl_up_sync(0xffffffffu, I[4], 1);
-                I[1] = __shfl_up_sync(0xffffffffu, I[5], 1);
-                I[6] = __shfl_down_sync(0xffffffffu, I[2], 1);
-                I[7] = __shfl_down_sync(0xffffffffu, I[3], 1);
-            }
-
-            // ---------------- LoG x 2, streaming over rows ----------------
-            float rC[2][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float x = I[i + 2], h1 = I[i + 1] + I[i + 3], h2 = I[i] + I[i + 4];
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const float A = fmaf(c00[j], x, fmaf(c10[j], h1, fmaf(c20[j], h2, acc[j][2][i])));
-                    const float B = fmaf(c21[j], h2, fmaf(c11[j], h1, fmaf(c10[j], x, 0.0f)));
-                    const float C = fmaf(c22[j], h2, fmaf(c21[j], h1, fmaf(c20[j], x, 0.0f)));
-                    rC[j][i] = acc[j][0][i] + C;
-                    acc[j][0][i] = acc[j][1][i] + B;
-                    acc[j][1][i] = A;
-                    acc[j][2][i] = acc[j][3][i] + B;
-                    acc[j][3][i] = C;
-                }
-            }
-            const int row_r = rho - 2;  // image row of rC
-            if (row_r > H - 1) {        // past the bottom: r(H..) = r(H-1)
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) rC[j][i] = rB[j][i];
-            } else if (fx.any) {
-                fix_floats(fx, rC[0]);
-                fix_floats(fx, rC[1]);
-            }
-
-            // ---------------- zero crossings of row rho-3 (rule R*) ----------------
-            float rBr[2];  // r of the pixel right of this lane's pixel 3
-            rBr[0] = __shfl_down_sync(0xffffffffu, rB[0][0], 1);
-            rBr[1] = __shfl_down_sync(0xffffffffu, rB[1][0], 1);
-            float t[2][4];
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = 0.0f - rC[j][i];
-            const uint32_t PC = pack_signs(t), NC = pack_signs(rC);
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = rB[j][i] + rC[j][i];
-            const uint32_t Dm = pack_signs(t);
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = -rB[j][i] - rC[j][i];
-            const uint32_t Dp = pack_signs(t);
-            uint32_t Dng = 0;
-            if constexpr (GAP) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) t[j][i] = fabsf(rB[j][i] - rC[j][i]) - a.tg[j];
-                Dng = pack_signs(t);
-            }
-            float rn[2][4];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                rn[j][0] = rB[j][1];
-                rn[j][1] = rB[j][2];
-                rn[j][2] = rB[j][3];
-                rn[j][3] = rBr[j];
-            }
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = rB[j][i] + rn[j][i];
-            const uint32_t Rm = pack_signs(t);
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = -rB[j][i] - rn[j][i];
-            const uint32_t Rp = pack_signs(t);
-            uint32_t Rng = 0;
-            if constexpr (GAP) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) t[j][i] = fabsf(rB[j][i] - rn[j][i]) - a.tg[j];
-                Rng = pack_signs(t);
-            }
-            // neighbours' flag bytes across lanes
-            const uint32_t PBl = __shfl_up_sync(0xffffffffu, PB, 1), NBl = __shfl_up_sync(0xffffffffu, NB, 1);
-            const uint32_t Rml = __shfl_up_sync(0xffffffffu, Rm, 1), Rpl = __shfl_up_sync(0xffffffffu, Rp, 1);
-            const uint32_t PBr = __shfl_down_sync(0xffffffffu, PB, 1), NBr = __shfl_down_sync(0xffffffffu, NB, 1);
-            const uint32_t PL = prmt(PB, PBl, 0x2107), NL = prmt(NB, NBl, 0x2107);
-            const uint32_t PR = prmt(PB, PBr, 0x4321), NR = prmt(NB, NBr, 0x4321);
-            const uint32_t Lm = prmt(Rm, Rml, 0x2107), Lp = prmt(Rp, Rpl, 0x2107);
-            // violations: an opposite-sign neighbour of smaller magnitude (R7, ties allowed R8)
-            const uint32_t X = (NA & Up) | (NC & Dp) | (NR & Rp) | (NL & Lp);
-            const uint32_t Y = (PA & Um) | (PC & Dm) | (PR & Rm) | (PL & Lm);
-            uint32_t XG, YG;
-            if constexpr (GAP) {
-                const uint32_t Lng = prmt(Rng, __shfl_up_sync(0xffffffffu, Rng, 1), 0x2107);
-                XG = (NA & ~Ung) | (NC & ~Dng) | (NR & ~Rng) | (NL & ~Lng);
-                YG = (PA & ~Ung) | (PC & ~Dng) | (PR & ~Rng) | (PL & ~Lng);
-            } else {
-                XG = NA | NC | NR | NL;
-                YG = PA | PC | PR | PL;
-            }
-            uint32_t Z = (PB & ~X & XG) | (NB & ~Y & YG);
-            // a pixel exactly at zero: a positive and a negative neighbour (R6)
-            const uint32_t z0 = ~PB & ~NB & (PA | PC | PR | PL) & (NA | NC | NR | NL) & 0x88888888u;
-            if constexpr (!GAP) {
-                Z |= z0;
-            } else {
-                if (__any_sync(0xffffffffu, z0 != 0)) {  // rare: also needs max - min >= t
-                    const float rBl0 = __shfl_up_sync(0xffffffffu, rB[0][3], 1);
-                    const float rBl1 = __shfl_up_sync(0xffffffffu, rB[1][3], 1);
-                    if (z0) {
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                if (!(z0 >> (8 * i + 3 + 4 * j) & 1)) continue;
-                                const float left = i == 0 ? (j == 0 ? rBl0 : rBl1) : rB[j][i > 0 ? i - 1 : 0];
-                                const float mx = fmaxf(fmaxf(rA[j][i], rC[j][i]), fmaxf(left, rn[j][i]));
-                                const float mn = fminf(fminf(rA[j][i], rC[j][i]), fminf(left, rn[j][i]));
-                                if (mx - mn >= a.tg[j]) Z |= 1u << (8 * i + 3 + 4 * j);
-                            }
-                    }
-                }
-            }
-            const int row_z = rho - 3;
-            Z >>= 3;  // Z at bit 0 (branch 0) / bit 4 (branch 1) of each pixel byte: counts add up per byte
-            if (fx.any) Z = fix_bytes(fx, Z);
-            // shift the ZC window
-            PA = PB;
-            NA = NB;
-            PB = PC;
-            NB = NC;
-            Um = Dm;
-            Up = Dp;
-            Ung = Dng;
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    rA[j][i] = rB[j][i];
-                    rB[j][i] = rC[j][i];
-                }
-            if (row_r == 0) {  // top edge reached by r: r(-1) := r(0)
-                PA = PB;
-                NA = NB;
-                Um = NB;
-                Up = PB;
-                Ung = a.ung_top;
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) rA[j][i] = rB[j][i];
-            }
-
-            // ---------------- Z window (rows rho-7 .. rho-3) ----------------
-            Zw[0] = Zw[1];
-            Zw[1] = Zw[2];
-            Zw[2] = Zw[3];
-            Zw[3] = Zw[4];
-            Zw[4] = row_z > H - 1 ? Zw[3] : Z;
-            if (row_z == 0) Zw[2] = Zw[3] = Zw[4];
-
-            // ---------------- std gate + merge for row rho-5 ----------------
-            const int row_e = rho - 5;
-            const uint32_t V = Zw[0] + Zw[1] + Zw[2] + Zw[3] + Zw[4];
-            const uint32_t V0 = V & 0x0F0F0F0Fu, V1 = (V >> 4) & 0x0F0F0F0Fu;
-            const uint32_t Lw = __shfl_up_sync(0xffffffffu, prmt(V0, V1, 0x7632), 1);
-            const uint32_t Rw = __shfl_down_sync(0xffffffffu, prmt(V0, V1, 0x5410), 1);
-            const uint32_t K0 = V0 + prmt(V0, Lw, 0x2105) + prmt(V0, Lw, 0x1054) + prmt(V0, Rw, 0x4321) + prmt(V0, Rw, 0x5432);
-            const uint32_t K1 = V1 + prmt(V1, Lw, 0x2107) + prmt(V1, Lw, 0x1076) + prmt(V1, Rw, 0x6321) + prmt(V1, Rw, 0x7632);
-            const uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
-            const uint32_t pass1 = (K1 + a.add_lo[1]) & ~(K1 + a.add_hi[1]) & 0x80808080u;
-            const uint32_t Zc = Zw[2];
-            const uint32_t M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
-            uint32_t e0, e1;                                              // E pairs of row rho-5
-            {
-                const int pe = max(min(max(row_e, 0), H - 1), plo);
-                const int ste = (pe - plo) / kR;
-                const unsigned char *rp = ring + ((g_base + ste) % kS) * stage_bytes + ((pe - plo) % kR) * row_bytes;
-                uint32_t i0, i1;
-                if constexpr (MASKOUT) {
-                    i0 = i1 = 0x00FF00FFu;
-                } else if constexpr (IN16) {
-                    const uint2 own = *reinterpret_cast<const uint2 *>(rp + off_own);
-                    i0 = own.x;
-                    i1 = own.y;
-                } else {
-                    const uint32_t own = *reinterpret_cast<const uint32_t *>(rp + off_own);
-                    i0 = prmt(own, 0, 0x4140);
-                    i1 = prmt(own, 0, 0x4342);
-                }
-                e0 = i0 & prmt(M7, 0, 0x9988);
-                e1 = i1 & prmt(M7, 0, 0xBBAA);
-                if (fx.any) {
-                    // E at outside columns = E at the edge column (MASK/extract values alike)
-                    fix_pairs(fx, e0, e1);
-                }
-            }
-            if (row_e > H - 1) {  // past the bottom: repeat the last row
-                e0 = E[4][1];
-                e1 = E[4][2];
-            }
-
-            if constexpr (HM) {
-                const uint32_t eL = __shfl_up_sync(0xffffffffu, e1, 1);
-                const uint32_t eR = __shfl_down_sync(0xffffffffu, e0, 1);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) E[k][q] = E[k + 1][q];
-                }
-                if (row_e > H - 1) {
-                    // already the repeated last row
-                    E[4][0] = E[3][0];
-                    E[4][3] = E[3][3];
-                    E[4][1] = E[3][1];
-                    E[4][2] = E[3][2];
-                } else {
-                    E[4][0] = eL;
-                    E[4][1] = e0;
-                    E[4][2] = e1;
-                    E[4][3] = eR;
-                }
-                if (row_e == 0) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) E[2][q] = E[3][q] = E[4][q];
-                }
-
-                // ---------------- hybrid median for row rho-7 ----------------
-                const int row_o = rho - 7;
-                if (row_o >= ys && warp_live) {
-                    // E[k] = rows row_o-2+k; per row: [0]=(x-2,x-1) [1]=(x,x+1) [2]=(x+2,x+3) [3]=(x+4,x+5)
-                    const uint32_t s2a = sh1(E[2][0], E[2][1]), s2b = sh1(E[2][1], E[2][2]), s2c = sh1(E[2][2], E[2][3]);
-                    const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
-                    const uint32_t s3a = sh1(E[3][0], E[3][1]), s3b = sh1(E[3][1], E[3][2]), s3c = sh1(E[3][2], E[3][3]);
-                    // pair 0 = pixels (x, x+1)
-                    const uint32_t c0 = E[2][1];
-                    const uint32_t mp0 = med9(E[2][0], s2a, c0, s2b, E[2][2], E[0][1], E[1][1], E[3][1], E[4][1]);
-                    const uint32_t mx0 = med9(E[0][0], s1a, s3b, E[4][2], E[0][2], s1b, s3a, E[4][0], c0);
-                    const uint32_t o0 = med3(mp0, mx0, c0);
-                    // pair 1 = pixels (x+2, x+3)
-                    const uint32_t c1 = E[2][2];
-                    const uint32_t mp1 = med9(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
-                    const uint32_t mx1 = med9(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
-                    const uint32_t o1 = med3(mp1, mx1, c1);
-                    // store
-                    char *orow = reinterpret_cast<char *>(a.out) + (long long)(row_o - a.o0) * a.out_pitch;
-                    if (lane >= 2 && lane < 30) {
-                        if (IN16 && !MASKOUT) {
-                            if (x0 + 3 < W) {
-                                *reinterpret_cast<uint2 *>(orow + 2LL * x0) = make_uint2(o0, o1);
-                            } else {
-                                uint16_t *p = reinterpret_cast<uint16_t *>(orow);
-                                if (x0 < W) p[x0] = (uint16_t)o0;
-                                if (x0 + 1 < W) p[x0 + 1] = (uint16_t)(o0 >> 16);
-                                if (x0 + 2 < W) p[x0 + 2] = (uint16_t)o1;
-                            }
-                        } else {
-                            const uint32_t b = prmt(o0, o1, 0x6420);
-                            if (x0 + 3 < W) {
-                                *reinterpret_cast<uint32_t *>(orow + x0) = b;
-                            } else {
-                                uint8_t *p = reinterpret_cast<uint8_t *>(orow);
-                                if (x0 < W) p[x0] = (uint8_t)b;
-                                if (x0 + 1 < W) p[x0 + 1] = (uint8_t)(b >> 8);
-                                if (x0 + 2 < W) p[x0 + 2] = (uint8_t)(b >> 16);
-                            }
-                        }
-                    }
-                }
-            } else {
-                // no median: the merged image is the output (row rho-5)
-                if (row_e >= ys && row_e < ye && warp_live) {
-                    char *orow = reinterpret_cast<char *>(a.out) + (long long)(row_e - a.o0) * a.out_pitch;
-                    if (lane >= 2 && lane < 30) {
-                        if (IN16 && !MASKOUT) {
-                            if (x0 + 3 < W) {
-                                *reinterpret_cast<uint2 *>(orow + 2LL * x0) = make_uint2(e0, e1);
-                            } else {
-                                uint16_t *p = reinterpret_cast<uint16_t *>(orow);
-                                if (x0 < W) p[x0] = (uint16_t)e0;
-                                if (x0 + 1 < W) p[x0 + 1] = (uint16_t)(e0 >> 16);
-                                if (x0 + 2 < W) p[x0 + 2] = (uint16_t)e1;
-                            }
-                        } else {
-                            const uint32_t b = prmt(e0, e1, 0x6420);
-                            if (x0 + 3 < W) {
-                                *reinterpret_cast<uint32_t *>(orow + x0) = b;
-                            } else {
-                                uint8_t *p = reinterpret_cast<uint8_t *>(orow);
-                                if (x0 < W) p[x0] = (uint8_t)b;
-                                if (x0 + 1 < W) p[x0 + 1] = (uint8_t)(b >> 8);
-                                if (x0 + 2 < W) p[x0 + 2] = (uint8_t)(b >> 16);
-                            }
-                        }
-                    }
-                }
-            }
-
-            // ---------------- release ring stages no future step reads ----------------
-            {
-                const int next_min = max(min(max(rho + 1 - 5, 0), H - 1), plo);
-                while (released < nst && next_min >= plo + (released + 1) * kR) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[(g_base + released) % kS]);
-                    ++released;
-                    if (warp == 0) ++rel0;
-                }
-                if (threadIdx.x == 0) produce();
-            }
-        }
-        // release whatever is left of this item
-        while (released < nst) {
-            if (waited < released) {  // never waited (cannot happen for read stages) -- keep parity in step
-                ++waited;
-                const uint32_t g = g_base + waited;
-                mbar_wait(&full[g % kS], (g / kS) & 1);
-                continue;
-            }
-            __syncwarp();
+        const bool border = xw < 0 || xw + 128 > W || it.ys - kLag < 0 || it.ye + kLag > H;
+        if (border)
+            walk(std::integral_constant<bool, true>{});
+        else
+            walk(std::integral_constant<bool, false>{});
+        // release what is left of the item
+        __syncwarp();
+        while (released < it.nst) {
             if (lane == 0) mbar_arrive(&empty[(g_base + released) % kS]);
             ++released;
-            if (warp == 0) ++rel0;
+            ++rel_w;
         }
-        g_base += nst;
-        if (threadIdx.x == 0) produce();
+        g_base += it.nst;
+        if (threadIdx.x == 0) prod.run(rel_w);
+        __syncwarp();
     }
     if (a.range_mask) {
         if (__any_sync(0xffffffffu, (range_acc & a.range_mask) != 0) && lane == 0) atomicOr(err_flag, 1);
@@ -802,11 +854,17 @@ bool interval_of(uint64_t lut, int L, int *lo, int *hi)
     return true;
 }
 
+template <bool IN16>
+constexpr size_t fused_smem()
+{
+    return kHdr + (size_t)kS * (IN16 ? 2 * 232 * 2 : 480) * kR + (size_t)kWarps * (kEBytes + kZBytes + kRBytes);
+}
+
 template <bool IN16, bool HM, bool MASKOUT, bool GAP>
 cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
 {
     auto kfn = fused_kernel<IN16, HM, MASKOUT, GAP>;
-    const size_t smem = 128 + (size_t)kS * (IN16 ? 2 * 232 * 2 : 480) * kR;
+    constexpr size_t smem = fused_smem<IN16>();
     static int grid_cap = 0;
     if (!grid_cap) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -817,6 +875,8 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
         grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int grid = fa.items < grid_cap ? fa.items : grid_cap;
+    cudaError_t e = cudaMemsetAsync(fa.work, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
     kfn<<<grid, kThreads, smem, s>>>(map, fa, err_flag);
     return cudaGetLastError();
 }
@@ -865,9 +925,9 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     fa.seg_rows = tile_h > 0 ? tile_h : 128;
     const int segs = (g.o1 - g.o0 + fa.seg_rows - 1) / fa.seg_rows;
     fa.items = fa.col_groups * segs;
-    fa.boxw = in16 ? 232 : 240;
     fa.out = g.out;
     fa.out_pitch = g.out_pitch;
+    fa.work = err_flag + 1;
     if (fa.items <= 0) return cudaSuccess;
 
     CUtensorMap map;
@@ -875,12 +935,11 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     // so the pair holding an odd last pixel stays inside the row)
     const cuuint64_t dims[2] = {(cuuint64_t)(in16 ? g.width : (g.width + 1) / 2), (cuuint64_t)g.Hv};
     const cuuint64_t strides[1] = {(cuuint64_t)g.in_pitch};
-    const cuuint32_t box[2] = {(cuuint32_t)fa.boxw, (cuuint32_t)kR};
+    const cuuint32_t box[2] = {(cuuint32_t)(in16 ? 232 : 240), (cuuint32_t)kR};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
-                             const_cast<void *>(g.in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void *>(g.in), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
 
     const bool hm = kp.hm, mask = kp.out_mode == LFE_OUT_MASK, gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0;

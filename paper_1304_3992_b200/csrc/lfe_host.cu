@@ -299,7 +299,8 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
     kp.out_mode = p->out_mode;
     kp.halo = kp.RL + 1 + kp.Rs + kp.Rm;
 
-    if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) {
+    // d_err[0]: sticky ERANGE flag; d_err[1]: the fused kernel's work-queue counter
+    if (cudaMalloc(&c->d_err, 2 * sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, 2 * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         delete c;
         return fail(LFE_ENOMEM, "device error flag");

@@ -59,6 +59,7 @@ struct LaunchCfg {
 // kernel launchers (return cudaGetLastError())
 cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
                           int *err_flag, cudaStream_t s);
+// err_flag[0] = sticky ERANGE flag, err_flag[1] = scratch work counter (fused kernel)
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
                          int *err_flag, cudaStream_t s);
 bool fused_supports(const KParams &kp, int bit_depth);

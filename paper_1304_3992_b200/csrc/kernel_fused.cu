@@ -3,19 +3,22 @@
 // none): one persistent kernel, every stage fused, no HBM
 // traffic between stages.
 //
-// Work decomposition.  A work item is a 448-column x `seg_rows`-row output
-// tile; CTAs take items from a global queue (atomic counter).  The CTA stages
-// the tile plus its combined halo (8 columns, 7 rows = LoG 2 + ZC 1 + std 2 +
+// Work decomposition.  One CTA of 12 warps per SM (co-resident CTAs starve each
+// other under the hardware's highest-warp-first arbitration; warps of ONE CTA
+// that share a TMA ring stay in lockstep instead).  The (column group of 1344
+// output columns, output row) space is split into equal contiguous ranges, one
+// per CTA (static, balanced to one row), walked top to bottom.  The CTA stages
+// its rows plus the combined halo (8 columns, 7 rows = LoG 2 + ZC 1 + std 2 +
 // median 2; north_star) into a shared-memory ring with TMA
-// (cp.async.bulk.tensor + mbarrier complete_tx), 8 rows per stage.  Each of
-// its 4 warps walks a 128-column strip (112 output columns + 8 + 8 halo) down
-// the rows; lane l owns 4 adjacent columns.  Per input row rho:
+// (cp.async.bulk.tensor + mbarrier complete_tx), 8 rows per stage.  Each warp
+// walks a 128-column strip (112 output columns + 8 + 8 halo) down the rows;
+// lane l owns 4 adjacent columns.  Per input row rho, four independent stages:
 //
 //   row rho  -> I, h1, h2 (fp32)      -> LoG x2, streaming  -> r(rho-2)   registers
 //   r        -> ZC flags, rule R*     -> Z(rho-3)           (R6-R9) -> Z ring (smem)
 //   Z ring   -> 5x5 counts, Eq. 2     -> keep, OR           (R10-R14)
-//            -> E(rho-5) = I or 0     (R15)                                      -> E ring (smem)
-//   E ring   -> hybrid median         -> out(rho-7)         (R16)   -> HBM
+//            -> E(rho-6) = I or 0     (R15)                                      -> E ring (smem)
+//   E ring   -> hybrid median         -> out(rho-9)         (R16)   -> HBM
 //
 // Arithmetic.  Integer masks (R3) keep every partial LoG sum below 2^24, so the
 // LoG runs exactly in fp32 FFMA (FMA pipe).  The zero-crossing edge tests
@@ -35,6 +38,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -43,19 +48,20 @@
 namespace lfe {
 namespace {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 12;                  // one CTA per SM; all warps share one TMA ring
 constexpr int kThreads = kWarps * 32;
 constexpr int kWarpOut = 112;               // output columns per warp
 constexpr int kHaloX = 8;                   // computed columns left of the output
-constexpr int kCtaOut = kWarps * kWarpOut;  // 448
+constexpr int kCtaOut = kWarps * kWarpOut;  // 1344 output columns per item
+constexpr int kProdThread = kThreads - 32;  // producer: lane 0 of the highest (highest-priority) warp
 constexpr int kR = 8;                       // rows per TMA stage (= rows per chunk)
 constexpr int kS = 4;                       // ring stages
-constexpr int kQ = 8;                       // item queue entries
 constexpr int kERow = 264;                  // bytes per E ring row: 128 px + 2 px pad each side
 constexpr int kEBytes = 8 * kERow;          // 8-row E ring per warp
 constexpr int kZBytes = 8 * 32 * 4;         // 8-row Z ring per warp
 constexpr int kRBytes = 2 * 32 * 32;        // 2-row r ring per warp (zero-pixel slow path)
-constexpr int kHdr = 128;                   // barriers + item queue
+constexpr int kHdr = 128;                   // mbarriers
+constexpr int kEdge = 16;                   // rows near the image top/bottom walked separately
 
 struct FusedArgs {
     float c[2][6];          // orbit coefficients (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
@@ -66,11 +72,20 @@ struct FusedArgs {
     uint32_t range_mask;    // input bits that must be zero (ERANGE); 0 = no check
     int W, H;               // virtual image
     int o0, o1;             // output rows
-    int col_groups, seg_rows, items;
+    int col_groups;
+    int cap;                // max rows per piece (0 = whole contiguous range; tuning/tests)
     void *out;
     long long out_pitch;
-    int *work;              // work-queue counter (zeroed before the launch)
+    unsigned long long *dbg;  // optional per-CTA [start, end, items] globaltimer record (LFE_DEBUG_TIMING)
+    int dbg_nofix;            // timing experiments only: never take the column-fix path (wrong borders)
 };
+
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -247,58 +262,72 @@ __device__ __forceinline__ void fix_pairs(const Fix &f, uint32_t &p0, uint32_t &
     }
 }
 
-// ---- work items ---------------------------------------------------------------
+// ---- work partition -------------------------------------------------------------
+// The work is (column group, output row) units, column-group major.  CTA b owns
+// the contiguous unit range [b*U/grid, (b+1)*U/grid): one or two (or, for tiny
+// images, a few) walks of consecutive rows, each cut into pieces of at most
+// `cap` rows when the tuning option sets one.  Every CTA gets the same number
+// of rows +-1 and pays the pipeline warm-up once per piece.
 struct Item {
     int ys, ye, plo, phi, xo, nst;
 };
 
-template <int kLag>
-__device__ __forceinline__ Item item_geo(const FusedArgs &a, int id)
-{
-    Item it;
-    const int rs = id / a.col_groups, cg = id - rs * a.col_groups;
-    it.ys = a.o0 + rs * a.seg_rows;
-    it.ye = min(it.ys + a.seg_rows, a.o1);
-    it.plo = max(0, it.ys - kLag);
-    it.phi = min(a.H, it.ye + kLag);
-    it.xo = cg * kCtaOut;
-    it.nst = (it.phi - it.plo + kR - 1) / kR;
-    return it;
-}
+struct Pieces {
+    long long u, u1;
+    __device__ __forceinline__ void init(const FusedArgs &a)
+    {
+        const long long U = (long long)a.col_groups * (a.o1 - a.o0);
+        u = U * blockIdx.x / gridDim.x;
+        u1 = U * (blockIdx.x + 1) / gridDim.x;
+    }
+    template <int kHalo>
+    __device__ __forceinline__ bool next(const FusedArgs &a, Item &it)
+    {
+        if (u >= u1) return false;
+        const int R = a.o1 - a.o0;
+        const int cg = (int)(u / R), r0 = (int)(u - (long long)cg * R);
+        int n = (int)min((long long)(R - r0), u1 - u);
+        if (a.cap > 0) n = min(n, a.cap);
+        // keep the rows within kEdge of the virtual top/bottom in pieces of their
+        // own, so that only those short pieces take the row-clamping path
+        const int ys = a.o0 + r0;
+        if (ys < kEdge && ys + n > kEdge) n = kEdge - ys;
+        if (ys < a.H - kEdge && ys + n > a.H - kEdge) n = a.H - kEdge - ys;
+        u += n;
+        it.ys = a.o0 + r0;
+        it.ye = it.ys + n;
+        it.xo = cg * kCtaOut;
+        it.plo = max(0, it.ys - kHalo);
+        it.phi = min(a.H, it.ye + kHalo);
+        it.nst = (it.phi - it.plo + kR - 1) / kR;
+        return true;
+    }
+};
 
-// ---- TMA producer (thread 0 only) ----------------------------------------------
-template <bool IN16, int kLag, int kStageBytes, int kBoxBytes, int kBoxCols>
+// ---- TMA producer (lane 0 of the last warp) -------------------------------------------
+template <bool IN16, int kHalo, int kStageBytes, int kBoxBytes, int kBoxCols, int kNBox>
 struct Producer {
     const FusedArgs *a;
     const CUtensorMap *map;
     uint64_t *full, *empty;
-    int *queue;
     unsigned char *ring;
+    Pieces pcs;
     Item it;
-    int id = -1, k = 0;
-    uint32_t g = 0, idx = 0;
-    bool done = false;
+    int k = 0;
+    bool have = false, done = false;
+    uint32_t g = 0;
 
     // issue stages while fewer than kS are outstanding beyond `released`
     __device__ __forceinline__ void run(uint32_t released)
     {
         while (!done && g < released + kS) {
-            if (id < 0) {
-                const int nid = atomicAdd(a->work, 1);
-                const int slot = g % kS;
-                const uint32_t use = g / kS;
-                if (nid >= a->items) {  // no more work: post the sentinel on its own ring slot
-                    queue[idx % kQ] = -1;
-                    if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
-                    mbar_arrive(&full[slot]);
+            if (!have) {
+                if (!pcs.template next<kHalo>(*a, it)) {
                     done = true;
                     return;
                 }
-                id = nid;
-                it = item_geo<kLag>(*a, id);
+                have = true;
                 k = 0;
-                queue[idx % kQ] = id;
-                ++idx;
             }
             const int slot = g % kS;
             const uint32_t use = g / kS;
@@ -306,29 +335,31 @@ struct Producer {
             mbar_expect_tx(&full[slot], kStageBytes);
             unsigned char *dst = ring + slot * kStageBytes;
             const int y = it.plo + k * kR;
-            if constexpr (IN16) {
-                tma_load_2d(dst, map, it.xo - kHaloX, y, &full[slot]);
-                tma_load_2d(dst + kBoxBytes, map, it.xo - kHaloX + kBoxCols, y, &full[slot]);
-            } else {
-                tma_load_2d(dst, map, (it.xo - 2 * kHaloX) / 2, y, &full[slot]);
+#pragma unroll
+            for (int b = 0; b < kNBox; ++b) {
+                if constexpr (IN16)
+                    tma_load_2d(dst + b * kBoxBytes, map, it.xo - kHaloX + b * kBoxCols, y, &full[slot]);
+                else
+                    tma_load_2d(dst + b * kBoxBytes, map, (it.xo - 2 * kHaloX + b * kBoxCols) / 2, y, &full[slot]);
             }
             ++g;
-            if (++k == it.nst) id = -1;
+            if (++k == it.nst) have = false;
         }
     }
 };
 
 template <bool IN16, bool HM, bool MASKOUT, bool GAP>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ FusedArgs a, int *err_flag)
 {
     constexpr int kElem = IN16 ? 2 : 1;
-    constexpr int kLag = HM ? 7 : 5;  // output row = input row - kLag (= row halo)
-    // u16 images: two 232-pixel boxes per row starting at column xo-8.  u8 images
-    // are loaded through a u16 view of the same bytes: one 240-element (480-pixel)
-    // box per row starting at column xo-16 -- a TMA box must start on a 16-byte
-    // boundary (measured: scripts/tma_probe.cu).
-    constexpr int kNBox = IN16 ? 2 : 1;
+    constexpr int kHalo = HM ? 7 : 5;  // input rows needed beyond the output rows (LoG 2 + ZC 1 + std 2 + HM 2)
+    constexpr int kLag = HM ? 9 : 6;   // pipeline delay: output row = input row - kLag
+    // u16 images: 232-pixel boxes per row starting at column xo-8.  u8 images are
+    // loaded through a u16 view of the same bytes: 240-element (480-pixel) boxes
+    // starting at column xo-16 -- a TMA box must start on a 16-byte boundary
+    // (measured: scripts/tma_probe.cu).  Enough boxes to cover kCtaOut + 16 columns.
+    constexpr int kNBox = IN16 ? (kCtaOut + 2 * kHaloX + 231) / 232 : (kCtaOut + 3 * kHaloX + 479) / 480;
     constexpr int kBoxCols = IN16 ? 232 : 480;
     constexpr int kColOrg = IN16 ? 0 : 8;
     constexpr int kBoxBytes = kBoxCols * kR * kElem;
@@ -338,7 +369,6 @@ __global__ void __launch_bounds__(kThreads, 3)
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + kS;
-    int *queue = reinterpret_cast<int *>(empty + kS);
     unsigned char *ring = smem + kHdr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *eRing = ring + kS * kStageBytes + warp * (kEBytes + kZBytes + kRBytes);
@@ -346,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     float4 *rRing = reinterpret_cast<float4 *>(eRing + kEBytes + kZBytes);  // [2 rows][32 lanes][2 float4]
     const int W = a.W, H = a.H;
 
+    const unsigned long long t_start = gtime();
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], 1);
@@ -356,19 +387,19 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     __syncthreads();
 
-    Producer<IN16, kLag, kStageBytes, kBoxBytes, kBoxCols> prod;
+    Producer<IN16, kHalo, kStageBytes, kBoxBytes, kBoxCols, kNBox> prod;
     prod.a = &a;
     prod.map = &tmap;
     prod.full = full;
     prod.empty = empty;
-    prod.queue = queue;
+    prod.pcs.init(a);
     prod.ring = ring;
     uint32_t rel_w = 0;  // stages this warp has released (thread 0: throttles the producer)
-    if (threadIdx.x == 0) prod.run(0);
+    if (threadIdx.x == kProdThread) prod.run(0);
 
     auto col_off = [&](int c) {
         c = max(0, min(c + kColOrg, kNBox * kBoxCols - 4));
-        const int b = c >= kBoxCols;
+        const int b = c / kBoxCols;
         return b * kBoxBytes + (c - b * kBoxCols) * kElem;
     };
     const int cl = warp * kWarpOut + 4 * lane;  // CTA-local column of this lane's pixel 0
@@ -386,11 +417,15 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
 
     uint32_t g_base = 0, c_idx = 0, range_acc = 0;
+    Pieces pcs;
+    pcs.init(a);
 
     // ---- per-item state, shared by the step lambda --------------------------
     Item it;
     int waited = 0, released = 0, x0 = 0;
     Fix fx;
+    bool isL = false, isR = false;
+    uint32_t zmask = 0x88888888u;  // flag bits of this lane's pixels inside the image
     uint32_t in_lo = 0, in_hi = 0;
     float acc[2][4][4];
     uint32_t PA, NA, PB, NB, Um, Up, Ung, V;
@@ -426,9 +461,96 @@ __global__ void __launch_bounds__(kThreads, 3)
         }
     };
 
-    // ---- one row step: input row rho, centre r row rB = r(rho-3), new r row rC = r(rho-2)
+    // ---- one row step.  Input row rho; centre r row rB = r(rho-3); new r row rC =
+    // r(rho-2).  The four stages of a step are independent of each other (each
+    // reads only what earlier steps left in registers / the smem rings), so the
+    // compiler can interleave them: std+merge for row rho-6, hybrid median for row
+    // rho-9, input+LoG for row rho, zero crossings for row rho-3.
     auto step = [&](auto fix_tag, int rho, float(&rB)[2][4], float(&rC)[2][4]) {
-        constexpr bool FIX = decltype(fix_tag)::value;
+        constexpr bool XF = decltype(fix_tag)::value & 1, YF = decltype(fix_tag)::value & 2;
+        // Cheap column edges (W % 4 == 0), in the interior code itself (branch-free selects,
+        // so one hot loop fits the instruction cache).  The lane holding column 0
+        // (isL) / column W-1 at its pixel 3 (isR) substitutes its own edge values for the
+        // neighbours across the edge -- per-stage replicate padding without touching the
+        // outside columns.
+        const int row_z = rho - 3, row_e = rho - 6;
+        // ---------------- std gate + merge for row rho-6 (Z rows rho-8 .. rho-4) ----------------
+        uint32_t Zc;
+        if constexpr (!YF) {
+            const uint32_t z_new = zRing[((row_e + 2) & 7) * 32 + lane];
+            const uint32_t z_old = zRing[((row_e - 3) & 7) * 32 + lane];
+            V = V + z_new - z_old;  // running 5-row count (bytes; <= 5 per nibble, no carries)
+            Zc = zRing[(row_e & 7) * 32 + lane];
+        } else {
+            V = 0;
+#pragma unroll
+            for (int k = -2; k <= 2; ++k) V += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
+            Zc = zRing[(min(max(row_e, 0), H - 1) & 7) * 32 + lane];
+        }
+        const uint32_t V0 = V & 0x0F0F0F0Fu, V1 = (V >> 4) & 0x0F0F0F0Fu;
+        uint32_t Lw = __shfl_up_sync(0xffffffffu, prmt(V0, V1, 0x7632), 1);
+        uint32_t Rw = __shfl_down_sync(0xffffffffu, prmt(V0, V1, 0x5410), 1);
+        Lw = isL ? prmt(V0, V1, 0x4400) : Lw;
+        Rw = isR ? prmt(V0, V1, 0x7733) : Rw;
+        const uint32_t K0 = V0 + prmt(V0, Lw, 0x2105) + prmt(V0, Lw, 0x1054) + prmt(V0, Rw, 0x4321) + prmt(V0, Rw, 0x5432);
+        const uint32_t K1 = V1 + prmt(V1, Lw, 0x2107) + prmt(V1, Lw, 0x1076) + prmt(V1, Rw, 0x6321) + prmt(V1, Rw, 0x7632);
+        const uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
+        const uint32_t pass1 = (K1 + a.add_lo[1]) & ~(K1 + a.add_hi[1]) & 0x80808080u;
+        const uint32_t M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
+        uint32_t e0, e1;                                              // E pairs of row rho-6
+        {
+            uint32_t i0, i1;
+            if constexpr (MASKOUT) {
+                i0 = i1 = 0x00FF00FFu;
+            } else {
+                const unsigned char *rp = row_ptr(prow(row_e));
+                if constexpr (IN16) {
+                    const uint2 own = *reinterpret_cast<const uint2 *>(rp + off_own);
+                    i0 = own.x;
+                    i1 = own.y;
+                } else {
+                    const uint32_t own = *reinterpret_cast<const uint32_t *>(rp + off_own);
+                    i0 = prmt(own, 0, 0x4140);
+                    i1 = prmt(own, 0, 0x4342);
+                }
+            }
+            e0 = i0 & prmt(M7, 0, 0x9988);
+            e1 = i1 & prmt(M7, 0, 0xBBAA);
+            if constexpr (XF) fix_pairs(fx, e0, e1);
+        }
+
+        // ---------------- hybrid median for row rho-9 (E rows rho-11 .. rho-7) ----------------
+        uint32_t o0 = 0, o1 = 0;
+        if constexpr (HM) {
+            const int row_o = rho - 9;
+            uint32_t E[5][4];  // rows row_o-2 .. row_o+2: (x-2,x-1) (x,x+1) (x+2,x+3) (x+4,x+5)
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                int r = row_o - 2 + k;
+                if constexpr (YF) r = min(max(r, 0), H - 1);
+                const unsigned char *b = eRing + (r & 7) * kERow + 8 * lane;
+                const uint2 lo = *reinterpret_cast<const uint2 *>(b);
+                const uint2 hi = *reinterpret_cast<const uint2 *>(b + 8);
+                E[k][0] = lo.x;
+                E[k][1] = lo.y;
+                E[k][2] = hi.x;
+                E[k][3] = hi.y;
+                E[k][0] = isL ? prmt(E[k][1], 0, 0x1010) : E[k][0];
+                E[k][3] = isR ? prmt(E[k][2], 0, 0x3232) : E[k][3];
+            }
+            const uint32_t s2a = sh1(E[2][0], E[2][1]), s2b = sh1(E[2][1], E[2][2]), s2c = sh1(E[2][2], E[2][3]);
+            const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
+            const uint32_t s3a = sh1(E[3][0], E[3][1]), s3b = sh1(E[3][1], E[3][2]), s3c = sh1(E[3][2], E[3][3]);
+            const uint32_t c0 = E[2][1];
+            const uint32_t mp0 = med9(E[2][0], s2a, c0, s2b, E[2][2], E[0][1], E[1][1], E[3][1], E[4][1]);
+            const uint32_t mx0 = med9(E[0][0], s1a, s3b, E[4][2], E[0][2], s1b, s3a, E[4][0], c0);
+            o0 = med3(mp0, mx0, c0);
+            const uint32_t c1 = E[2][2];
+            const uint32_t mp1 = med9(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
+            const uint32_t mx1 = med9(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
+            o1 = med3(mp1, mx1, c1);
+        }
+
         // ---------------- input row ----------------
         const unsigned char *rowp = row_ptr(prow(rho));
         float I[8];  // columns x0-2 .. x0+5
@@ -439,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             I[3] = hi16f(own.x);
             I[4] = lo16f(own.y);
             I[5] = hi16f(own.y);
-            if constexpr (!FIX) {
+            if constexpr (!XF) {
                 const uint32_t wl = *reinterpret_cast<const uint32_t *>(rowp + off_l);
                 const uint32_t wr = *reinterpret_cast<const uint32_t *>(rowp + off_r);
                 I[0] = lo16f(wl);
@@ -454,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             I[3] = byte_f(own, 0x5441);
             I[4] = byte_f(own, 0x5442);
             I[5] = byte_f(own, 0x5443);
-            if constexpr (!FIX) {
+            if constexpr (!XF) {
                 const uint32_t wl = *reinterpret_cast<const uint16_t *>(rowp + off_l);
                 const uint32_t wr = *reinterpret_cast<const uint16_t *>(rowp + off_r);
                 I[0] = byte_f(wl, 0x5440);
@@ -463,7 +585,11 @@ __global__ void __launch_bounds__(kThreads, 3)
                 I[7] = byte_f(wr, 0x5441);
             }
         }
-        if constexpr (FIX) {
+        I[0] = isL ? I[2] : I[0];
+        I[1] = isL ? I[2] : I[1];
+        I[6] = isR ? I[5] : I[6];
+        I[7] = isR ? I[5] : I[7];
+        if constexpr (XF) {
             float own4[4] = {I[2], I[3], I[4], I[5]};
             fix_floats(fx, own4);
             I[2] = own4[0];
@@ -494,15 +620,16 @@ __global__ void __launch_bounds__(kThreads, 3)
             }
         }
         const int row_r = rho - 2;
-        if constexpr (FIX) {
+        if constexpr (XF) {
+            fix_floats(fx, rC[0]);
+            fix_floats(fx, rC[1]);
+        }
+        if constexpr (YF) {
             if (row_r > H - 1) {  // past the bottom: r(H..) = r(H-1)
 #pragma unroll
                 for (int j = 0; j < 2; ++j)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) rC[j][i] = rB[j][i];
-            } else {
-                fix_floats(fx, rC[0]);
-                fix_floats(fx, rC[1]);
             }
         }
 
@@ -514,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             rn[j][1] = rB[j][2];
             rn[j][2] = rB[j][3];
             rn[j][3] = __shfl_down_sync(0xffffffffu, rB[j][0], 1);
+            rn[j][3] = isR ? rB[j][3] : rn[j][3];
         }
         float t[2][4];
 #pragma unroll
@@ -557,18 +685,27 @@ __global__ void __launch_bounds__(kThreads, 3)
             Rng = pack_signs(t);
         }
         // neighbours' flag bytes across lanes
-        const uint32_t PL = prmt(PB, __shfl_up_sync(0xffffffffu, PB, 1), 0x2107);
-        const uint32_t NL = prmt(NB, __shfl_up_sync(0xffffffffu, NB, 1), 0x2107);
-        const uint32_t PR = prmt(PB, __shfl_down_sync(0xffffffffu, PB, 1), 0x4321);
-        const uint32_t NR = prmt(NB, __shfl_down_sync(0xffffffffu, NB, 1), 0x4321);
-        const uint32_t Lm = prmt(Rm, __shfl_up_sync(0xffffffffu, Rm, 1), 0x2107);
-        const uint32_t Lp = prmt(Rp, __shfl_up_sync(0xffffffffu, Rp, 1), 0x2107);
+        uint32_t PBl = __shfl_up_sync(0xffffffffu, PB, 1), NBl = __shfl_up_sync(0xffffffffu, NB, 1);
+        uint32_t Rml = __shfl_up_sync(0xffffffffu, Rm, 1), Rpl = __shfl_up_sync(0xffffffffu, Rp, 1);
+        uint32_t PBr = __shfl_down_sync(0xffffffffu, PB, 1), NBr = __shfl_down_sync(0xffffffffu, NB, 1);
+        // column -1 := column 0 (the edge between them joins equal values); column W := W-1
+        PBl = isL ? PB << 24 : PBl;
+        NBl = isL ? NB << 24 : NBl;
+        Rml = isL ? NB << 24 : Rml;
+        Rpl = isL ? PB << 24 : Rpl;
+        PBr = isR ? PB >> 24 : PBr;
+        NBr = isR ? NB >> 24 : NBr;
+        const uint32_t PL = prmt(PB, PBl, 0x2107), NL = prmt(NB, NBl, 0x2107);
+        const uint32_t PR = prmt(PB, PBr, 0x4321), NR = prmt(NB, NBr, 0x4321);
+        const uint32_t Lm = prmt(Rm, Rml, 0x2107), Lp = prmt(Rp, Rpl, 0x2107);
         // violations: an opposite-sign neighbour of smaller magnitude (R7; ties allowed, R8)
         const uint32_t X = (NA & Up) | (NC & Dp) | (NR & Rp) | (NL & Lp);
         const uint32_t Y = (PA & Um) | (PC & Dm) | (PR & Rm) | (PL & Lm);
         uint32_t XG, YG;
         if constexpr (GAP) {
-            const uint32_t Lng = prmt(Rng, __shfl_up_sync(0xffffffffu, Rng, 1), 0x2107);
+            uint32_t Rngl = __shfl_up_sync(0xffffffffu, Rng, 1);
+            Rngl = isL ? a.ung_top : Rngl;
+            const uint32_t Lng = prmt(Rng, Rngl, 0x2107);
             XG = (NA & ~Ung) | (NC & ~Dng) | (NR & ~Rng) | (NL & ~Lng);
             YG = (PA & ~Ung) | (PC & ~Dng) | (PR & ~Rng) | (PL & ~Lng);
         } else {
@@ -577,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         }
         uint32_t Z = (PB & ~X & XG) | (NB & ~Y & YG);
         // a pixel exactly at zero: a positive and a negative neighbour (R6)
-        const uint32_t z0 = ~PB & ~NB & (PA | PC | PR | PL) & (NA | NC | NR | NL) & 0x88888888u;
+        const uint32_t z0 = ~PB & ~NB & (PA | PC | PR | PL) & (NA | NC | NR | NL) & zmask;
         if constexpr (!GAP) {
             Z |= z0;
         } else {
@@ -585,8 +722,10 @@ __global__ void __launch_bounds__(kThreads, 3)
                 const float4 *up = rRing + (((rho - 4) & 1) * 32 + lane) * 2;  // r(rho-4), stored last step
                 const float4 u0 = up[0], u1 = up[1];
                 const float rU[2][4] = {{u0.x, u0.y, u0.z, u0.w}, {u1.x, u1.y, u1.z, u1.w}};
-                const float l0 = __shfl_up_sync(0xffffffffu, rB[0][3], 1);
-                const float l1 = __shfl_up_sync(0xffffffffu, rB[1][3], 1);
+                float l0 = __shfl_up_sync(0xffffffffu, rB[0][3], 1);
+                float l1 = __shfl_up_sync(0xffffffffu, rB[1][3], 1);
+                l0 = isL ? rB[0][0] : l0;
+                l1 = isL ? rB[1][0] : l1;
                 if (z0) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j)
@@ -604,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             float4 *me = rRing + (((rho - 3) & 1) * 32 + lane) * 2;
             me[0] = make_float4(rB[0][0], rB[0][1], rB[0][2], rB[0][3]);
             me[1] = make_float4(rB[1][0], rB[1][1], rB[1][2], rB[1][3]);
-            if constexpr (FIX) {
+            if constexpr (YF) {
                 if (row_r == 0) {
                     float4 *m2 = rRing + (((rho - 3) & 1) * 32 + lane) * 2;  // slot read as r(-1) next step
                     m2[0] = make_float4(rC[0][0], rC[0][1], rC[0][2], rC[0][3]);
@@ -613,8 +752,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             }
         }
         Z >>= 3;  // Z at bit 0 (branch 0) / bit 4 (branch 1) of each pixel byte: counts add per byte
-        if constexpr (FIX) Z = fix_bytes(fx, Z);
-        const int row_z = rho - 3;
+        if constexpr (XF) Z = fix_bytes(fx, Z);
         // shift the ZC state
         PA = PB;
         NA = NB;
@@ -623,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         Um = Dm;
         Up = Dp;
         Ung = Dng;
-        if constexpr (FIX) {
+        if constexpr (YF) {
             if (row_r == 0) {  // top edge reached by r: r(-1) := r(0)
                 PA = PB;
                 NA = NB;
@@ -633,102 +771,31 @@ __global__ void __launch_bounds__(kThreads, 3)
             }
         }
 
-        // ---------------- Z ring + std gate + merge for row rho-5 ----------------
-        const int row_e = rho - 5;
-        uint32_t Zc;
-        if constexpr (!FIX) {
-            const uint32_t z_old = zRing[((row_z - 5) & 7) * 32 + lane];
-            zRing[(row_z & 7) * 32 + lane] = Z;
-            V = V + Z - z_old;  // running 5-row count (bytes, no carries: <= 5 per nibble)
-            Zc = zRing[((row_z - 2) & 7) * 32 + lane];
-        } else {
-            if (row_z >= 0 && row_z <= H - 1) zRing[(row_z & 7) * 32 + lane] = Z;
-            V = 0;
-#pragma unroll
-            for (int k = -2; k <= 2; ++k) V += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
-            Zc = zRing[(min(max(row_e, 0), H - 1) & 7) * 32 + lane];
-        }
-        const uint32_t V0 = V & 0x0F0F0F0Fu, V1 = (V >> 4) & 0x0F0F0F0Fu;
-        const uint32_t Lw = __shfl_up_sync(0xffffffffu, prmt(V0, V1, 0x7632), 1);
-        const uint32_t Rw = __shfl_down_sync(0xffffffffu, prmt(V0, V1, 0x5410), 1);
-        const uint32_t K0 = V0 + prmt(V0, Lw, 0x2105) + prmt(V0, Lw, 0x1054) + prmt(V0, Rw, 0x4321) + prmt(V0, Rw, 0x5432);
-        const uint32_t K1 = V1 + prmt(V1, Lw, 0x2107) + prmt(V1, Lw, 0x1076) + prmt(V1, Rw, 0x6321) + prmt(V1, Rw, 0x7632);
-        const uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
-        const uint32_t pass1 = (K1 + a.add_lo[1]) & ~(K1 + a.add_hi[1]) & 0x80808080u;
-        const uint32_t M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
-        uint32_t e0, e1;                                              // E pairs of row rho-5
-        {
-            uint32_t i0, i1;
-            if constexpr (MASKOUT) {
-                i0 = i1 = 0x00FF00FFu;
-            } else {
-                const unsigned char *rp = row_ptr(prow(row_e));
-                if constexpr (IN16) {
-                    const uint2 own = *reinterpret_cast<const uint2 *>(rp + off_own);
-                    i0 = own.x;
-                    i1 = own.y;
-                } else {
-                    const uint32_t own = *reinterpret_cast<const uint32_t *>(rp + off_own);
-                    i0 = prmt(own, 0, 0x4140);
-                    i1 = prmt(own, 0, 0x4342);
-                }
-            }
-            e0 = i0 & prmt(M7, 0, 0x9988);
-            e1 = i1 & prmt(M7, 0, 0xBBAA);
-            if constexpr (FIX) fix_pairs(fx, e0, e1);
-        }
-
+        // ---------------- ring writes and the output row ----------------
+        if (!YF || (row_z >= 0 && row_z <= H - 1)) zRing[(row_z & 7) * 32 + lane] = Z;
         if constexpr (HM) {
-            uint32_t *erow = reinterpret_cast<uint32_t *>(eRing + (row_e & 7) * kERow + 4 + 8 * lane);
-            if (!FIX || (row_e >= 0 && row_e <= H - 1)) {
+            if (!YF || (row_e >= 0 && row_e <= H - 1)) {
+                uint32_t *erow = reinterpret_cast<uint32_t *>(eRing + (row_e & 7) * kERow + 4 + 8 * lane);
                 erow[0] = e0;
                 erow[1] = e1;
             }
-            __syncwarp();
-            // ---------------- hybrid median for row rho-7 ----------------
-            const int row_o = rho - 7;
-            if (row_o >= it.ys && row_o < it.ye) {
-                uint32_t E[5][4];  // rows row_o-2 .. row_o+2: (x-2,x-1) (x,x+1) (x+2,x+3) (x+4,x+5)
-#pragma unroll
-                for (int k = 0; k < 5; ++k) {
-                    int r = row_o - 2 + k;
-                    if constexpr (FIX) r = min(max(r, 0), H - 1);
-                    const unsigned char *b = eRing + (r & 7) * kERow + 8 * lane;
-                    const uint2 lo = *reinterpret_cast<const uint2 *>(b);
-                    const uint2 hi = *reinterpret_cast<const uint2 *>(b + 8);
-                    E[k][0] = lo.x;
-                    E[k][1] = lo.y;
-                    E[k][2] = hi.x;
-                    E[k][3] = hi.y;
-                }
-                const uint32_t s2a = sh1(E[2][0], E[2][1]), s2b = sh1(E[2][1], E[2][2]), s2c = sh1(E[2][2], E[2][3]);
-                const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
-                const uint32_t s3a = sh1(E[3][0], E[3][1]), s3b = sh1(E[3][1], E[3][2]), s3c = sh1(E[3][2], E[3][3]);
-                const uint32_t c0 = E[2][1];
-                const uint32_t mp0 = med9(E[2][0], s2a, c0, s2b, E[2][2], E[0][1], E[1][1], E[3][1], E[4][1]);
-                const uint32_t mx0 = med9(E[0][0], s1a, s3b, E[4][2], E[0][2], s1b, s3a, E[4][0], c0);
-                const uint32_t o0 = med3(mp0, mx0, c0);
-                const uint32_t c1 = E[2][2];
-                const uint32_t mp1 = med9(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
-                const uint32_t mx1 = med9(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
-                const uint32_t o1 = med3(mp1, mx1, c1);
-                store(row_o, o0, o1);
-            }
+            if (rho - 9 >= it.ys && rho - 9 < it.ye) store(rho - 9, o0, o1);
         } else {
             if (row_e >= it.ys && row_e < it.ye) store(row_e, e0, e1);
         }
+        __syncwarp();
     };
 
     // ---- walk every row of the current item ---------------------------------
     auto walk = [&](auto fix_tag) {
-        constexpr bool FIX = decltype(fix_tag)::value;
+        constexpr bool YF = decltype(fix_tag)::value & 2;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int i = 0; i < 4; ++i) acc[j][0][i] = acc[j][1][i] = acc[j][2][i] = acc[j][3][i] = 0.0f;
         PA = NA = PB = NB = Um = Up = Ung = 0;
         V = 0;
-        if constexpr (!FIX) {
+        if constexpr (!YF) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) zRing[k * 32 + lane] = 0;
         }
@@ -740,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             for (int i = 0; i < 4; ++i) rX[j][i] = rY[j][i] = 0.0f;
 
         const int rho_end = it.ye + kLag;
-        for (int rho = it.ys - kLag; rho < rho_end; rho += kR) {
+        for (int rho = it.ys - kHalo; rho < rho_end; rho += kR) {
             // wait for the ring stages holding this chunk's input rows
             const int st = (prow(rho + kR - 1) - it.plo) >> 3;
             while (waited < st) {
@@ -753,26 +820,23 @@ __global__ void __launch_bounds__(kThreads, 3)
                 step(fix_tag, rho + k, rX, rY);
                 step(fix_tag, rho + k + 1, rY, rX);
             }
-            // release ring stages that no later step reads (the E stage reads row rho-5)
-            const int next_e = prow(rho + n - 5);
+            // release ring stages that no later step reads (the E stage reads row rho-6)
+            const int next_e = prow(rho + n - 6);
             __syncwarp();
             while (released < it.nst && it.plo + (released + 1) * kR <= next_e) {
                 if (lane == 0) mbar_arrive(&empty[(g_base + released) % kS]);
                 ++released;
                 ++rel_w;
             }
-            if (threadIdx.x == 0) prod.run(rel_w);
+            if (threadIdx.x == kProdThread) prod.run(rel_w);
             __syncwarp();
         }
     };
 
     // ---- item loop -------------------------------------------------------------
-    for (;;) {
-        mbar_wait(&full[g_base % kS], (g_base / kS) & 1);  // first stage of the next item (or the sentinel)
-        const int id = queue[c_idx % kQ];
-        if (id < 0) break;
+    while (pcs.next<kHalo>(a, it)) {
+        mbar_wait(&full[g_base % kS], (g_base / kS) & 1);  // first stage of this piece
         ++c_idx;
-        it = item_geo<kLag>(a, id);
         waited = 0;
         released = 0;
         const int xw = it.xo - kHaloX + warp * kWarpOut;  // image column of this warp's column 0
@@ -795,11 +859,21 @@ __global__ void __launch_bounds__(kThreads, 3)
                     (x0 + 3 < W ? 0xFF000000u : 0u);
         }
         if (x0 < 0) in_lo = in_hi = 0;
-        const bool border = xw < 0 || xw + 128 > W || it.ys - kLag < 0 || it.ye + kLag > H;
-        if (border)
-            walk(std::integral_constant<bool, true>{});
-        else
-            walk(std::integral_constant<bool, false>{});
+        zmask = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (x0 + i >= 0 && x0 + i < W) zmask |= 0x88u << (8 * i);
+        isL = xw < 0 && lane == ((-xw) >> 2);
+        isR = xw + 128 > W && dr >= 0 && lane == (dr >> 2);
+        // path: 0 interior; 4 cheap column edges (W % 4 == 0); 3 general fix-ups (edge rows,
+        // or column edges of widths that are not a multiple of 4)
+        const bool xedge = (xw < 0 || xw + 128 > W) && !a.dbg_nofix;
+        if (it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge && (W & 3))) {
+            isL = isR = false;
+            walk(std::integral_constant<int, 3>{});
+        } else {
+            walk(std::integral_constant<int, 0>{});
+        }
         // release what is left of the item
         __syncwarp();
         while (released < it.nst) {
@@ -808,11 +882,19 @@ __global__ void __launch_bounds__(kThreads, 3)
             ++rel_w;
         }
         g_base += it.nst;
-        if (threadIdx.x == 0) prod.run(rel_w);
+        if (threadIdx.x == kProdThread) prod.run(rel_w);
         __syncwarp();
     }
     if (a.range_mask) {
         if (__any_sync(0xffffffffu, (range_acc & a.range_mask) != 0) && lane == 0) atomicOr(err_flag, 1);
+    }
+    if (a.dbg && threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        a.dbg[4 * blockIdx.x + 0] = t_start;
+        a.dbg[4 * blockIdx.x + 1] = gtime();
+        a.dbg[4 * blockIdx.x + 2] = c_idx;
+        a.dbg[4 * blockIdx.x + 3] = sm;
     }
 }
 
@@ -857,7 +939,8 @@ bool interval_of(uint64_t lut, int L, int *lo, int *hi)
 template <bool IN16>
 constexpr size_t fused_smem()
 {
-    return kHdr + (size_t)kS * (IN16 ? 2 * 232 * 2 : 480) * kR + (size_t)kWarps * (kEBytes + kZBytes + kRBytes);
+    constexpr int nbox = IN16 ? (kCtaOut + 2 * kHaloX + 231) / 232 : (kCtaOut + 3 * kHaloX + 479) / 480;
+    return kHdr + (size_t)kS * nbox * (IN16 ? 232 * 2 : 480) * kR + (size_t)kWarps * (kEBytes + kZBytes + kRBytes);
 }
 
 template <bool IN16, bool HM, bool MASKOUT, bool GAP>
@@ -874,11 +957,28 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads, smem);
         grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     }
-    const int grid = fa.items < grid_cap ? fa.items : grid_cap;
-    cudaError_t e = cudaMemsetAsync(fa.work, 0, sizeof(int), s);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, kThreads, smem, s>>>(map, fa, err_flag);
-    return cudaGetLastError();
+    const long long units = (long long)fa.col_groups * (fa.o1 - fa.o0);
+    const int grid = units < grid_cap ? (int)units : grid_cap;
+    cudaError_t e = cudaSuccess;
+    static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
+    FusedArgs fb = fa;
+    fb.dbg = nullptr;
+    if (dbg_path) cudaMalloc(&fb.dbg, sizeof(unsigned long long) * 4 * grid);
+    kfn<<<grid, kThreads, smem, s>>>(map, fb, err_flag);
+    e = cudaGetLastError();
+    if (dbg_path && fb.dbg) {  // debug only: synchronous dump of the per-CTA timeline
+        cudaStreamSynchronize(s);
+        unsigned long long *h = new unsigned long long[4 * grid];
+        cudaMemcpy(h, fb.dbg, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(dbg_path, "a")) {
+            for (int i = 0; i < grid; ++i) fprintf(f, "%d %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            fprintf(f, "---\n");
+            fclose(f);
+        }
+        delete[] h;
+        cudaFree(fb.dbg);
+    }
+    return e;
 }
 
 }  // namespace
@@ -922,13 +1022,12 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     fa.o0 = g.o0;
     fa.o1 = g.o1;
     fa.col_groups = (g.width + kCtaOut - 1) / kCtaOut;
-    fa.seg_rows = tile_h > 0 ? tile_h : 128;
-    const int segs = (g.o1 - g.o0 + fa.seg_rows - 1) / fa.seg_rows;
-    fa.items = fa.col_groups * segs;
+    fa.cap = tile_h > 0 ? tile_h : 0;
     fa.out = g.out;
     fa.out_pitch = g.out_pitch;
-    fa.work = err_flag + 1;
-    if (fa.items <= 0) return cudaSuccess;
+    fa.dbg = nullptr;
+    fa.dbg_nofix = getenv("LFE_DEBUG_NOFIX") != nullptr;
+    if (g.o1 <= g.o0 || g.width <= 0) return cudaSuccess;
 
     CUtensorMap map;
     // u8 rows are fetched as u16 pairs (the row pitch is a multiple of 16 bytes,

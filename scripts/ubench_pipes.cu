@@ -28,6 +28,10 @@ __device__ __forceinline__ void op(uint32_t (&a)[CHAINS], uint32_t k1, uint32_t 
         if (OP == 10) asm volatile("shf.l.wrap.b32 %0, %0, %1, 1;" : "+r"(x) : "r"(k1));          // SHF
         if (OP == 11) { uint32_t y; asm volatile("min.u32 %0, %1, %2;" : "=r"(y) : "r"(x), "r"(k1)); x = y; }  // IMNMX
         if (OP == 12) asm volatile("{.reg .s32 t; add.s32 t, %0, %1; max.s32 %0, t, %2;}" : "+r"(x) : "r"(k1), "r"(k2));                                  // VIADDMNMX
+        if (OP == 14) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x) : "r"(k1));                   // IMAD.HI
+        if (OP == 15) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(x) : "r"(k1), "r"(k2));      // IMAD.HI + acc
+        if (OP == 16) asm volatile("mul.rn.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));                   // FMUL
+        if (OP == 17) asm volatile("add.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));                      // FADD
         if (OP == 13) { int p; asm volatile("{.reg .pred q; setp.lt.s32 q, %1, %2; selp.b32 %0, 1, 0, q;}" : "=r"(p) : "r"(x), "r"(k1)); x += p; }  // ISETP+SEL+IADD
         a[c] = x;
     }
@@ -90,6 +94,15 @@ int main()
     run<9, -1>("PRMT");
     run<10, -1>("SHF");
     run<13, -1>("ISETP+SEL+IADD (3 inst)");
+    run<14, -1>("IMAD.HI");
+    run<15, -1>("IMAD.HI+acc");
+    run<16, -1>("FMUL");
+    run<17, -1>("FADD");
+    run<14, 1>("IMAD.HI + LOP3");
+    run<15, 3>("IMAD.HI+acc + FFMA");
+    run<16, 1>("FMUL + LOP3");
+    run<17, 1>("FADD + LOP3");
+    run<10, 3>("SHF + FFMA");
     run<4, 3>("VIMNMX3.U16x2 + FFMA");
     run<4, 2>("VIMNMX3.U16x2 + IMAD");
     run<4, 1>("VIMNMX3.U16x2 + LOP3");

@@ -286,3 +286,17 @@ def test_fused_equals_staged_on_c3_strip():
     img = scenes.scene_c3(size=3000, height=700)
     p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
     assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), run_gpu(img, p, lfe.LFE_KERNEL_STAGED), "c3 strip")
+
+
+@pytest.mark.parametrize("W", [4, 8, 12, 116, 120, 124, 128, 132, 236, 448, 452, 456, 1344, 1348, 1352, 2696])
+def test_fused_column_edges_multiple_of_4(W):
+    """Widths that are multiples of 4 take the cheap column-edge path (edge lanes
+    substitute their own values); every position of column W-1 relative to the
+    warp strips must still match the oracle."""
+    rng = np.random.default_rng(W)
+    for bd, H in [(8, 40), (10, 23)]:
+        p = lfe.Params(bit_depth=bd, zc_threshold=(0.01, 0.0))
+        img = scenes.random_image(rng, H, W, bd, "mixed")
+        assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), f"W={W} b={bd}")
+        p2 = lfe.Params(bit_depth=bd, hybrid_median=False, out_mode=lfe.LFE_OUT_MASK)
+        assert_same(run_gpu(img, p2, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p2)), f"W={W} b={bd} nohm")

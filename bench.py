@@ -147,11 +147,13 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(img, p, rows=2048):
+def cpu_baseline(img, p, rows=None):
     """The oracle as it stands, on the host cores, on a bounded sample of the
-    same workload: `rows` full-width rows (+7 halo rows each side)."""
+    same workload: `rows` full-width rows (+7 halo rows each side); default the
+    whole scene (about 6 s on 16 cores)."""
     import oracle
     H = img.shape[0]
+    rows = H if rows is None else min(rows, H)
     a = H // 2 - rows // 2
     lo, hi = max(0, a - 7), min(H, a + rows + 7)
     band = img[lo:hi].copy()

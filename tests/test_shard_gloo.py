@@ -1,0 +1,99 @@
+"""Multi-process (gloo, CPU) tests of the row-strip sharding host logic used by
+multi-GPU runs: strip planning, the NCCL-style neighbour halo exchange through
+torch.distributed, and the band schedule handed to lfe_extract_rows.  The
+compute on each band is the CPU oracle here (no GPU); the GPU-side equality of
+lfe_extract_rows with lfe_extract is tested in test_gpu_parity.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_1304_3992_b200 import scenes
+from paper_1304_3992_b200.shard import StripShard, plan_strips
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_plan_strips_covers_and_balances():
+    for H in (7, 8, 100, 12000, 12001):
+        for world in (1, 2, 3, 4, 8):
+            if world > 1 and H // world < 7:
+                with pytest.raises(ValueError):
+                    plan_strips(H, world, 7)
+                continue
+            p = plan_strips(H, world, 7)
+            assert p[0][0] == 0 and p[-1][1] == H
+            assert all(a1 == b0 for (_, a1), (b0, _) in zip(p, p[1:]))
+            sizes = [b - a for a, b in p]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_bands_partition_each_strip():
+    for world in (1, 2, 3, 8):
+        for r in range(world):
+            sh = StripShard(12000, 64, r, world, 7)
+            bands = sh.bands()
+            rows = sorted((s, s + n) for s, n, *_ in bands)
+            assert rows[0][0] == 0 and rows[-1][1] == sh.rows
+            assert all(a1 == b0 for (_, a1), (b0, _) in zip(rows, rows[1:]))
+            # the first band never needs the exchange (it overlaps it)
+            assert bands[0][5] is False
+
+
+def _worker(rank, world, port, H, W, hm, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = scenes.scene_c1(size=max(H, W))[:H, :W].copy()
+        p = O.Params(bit_depth=8, zc_threshold=(0.01, 0.01), hybrid_median=hm)
+        halo = 7 if hm else 5
+        sh = StripShard(H, W, rank, world, halo)
+        buf = sh.alloc(torch.uint8, "cpu")
+        sh.load_owned(img)
+        for w in sh.exchange():
+            w.wait()
+        # received halos equal the neighbours' boundary rows
+        if sh.ha:
+            assert np.array_equal(buf[:sh.ha].numpy(), img[sh.a - sh.ha:sh.a])
+        if sh.hb:
+            assert np.array_equal(buf[sh.ha + sh.rows:].numpy(), img[sh.b:sh.b + sh.hb])
+        # run every band the way bench.py hands it to lfe_extract_rows
+        out = np.zeros((sh.rows, W), np.uint8)
+        B = buf.numpy()
+        for s, n, ha, hb, flags, _ in sh.bands():
+            r0 = sh.ha + s
+            sub = np.ascontiguousarray(B[r0 - ha:r0 + n + hb])
+            out[s:s + n] = O.run(sub, p)[ha:ha + n]
+        q.put((rank, sh.a, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,H,hm", [(2, 96, True), (3, 61, True), (2, 40, False)])
+def test_gloo_strips_reproduce_whole_image(world, H, hm):
+    W = 72
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, hm, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=240) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    img = scenes.scene_c1(size=max(H, W))[:H, :W].copy()
+    whole = O.run(img, O.Params(bit_depth=8, zc_threshold=(0.01, 0.01), hybrid_median=hm))
+    full = np.zeros_like(whole)
+    for _, a, out in got:
+        full[a:a + out.shape[0]] = out
+    np.testing.assert_array_equal(full, whole)

@@ -23,8 +23,9 @@
 // Arithmetic.  Integer masks (R3) keep every partial LoG sum below 2^24, so the
 // LoG runs exactly in fp32 FFMA (FMA pipe).  The zero-crossing edge tests
 // (signs of r_p + r_n, |r_p - r_n| - t) are fp32 adds whose SIGN is exact;
-// their sign bits are packed into flag words (byte per pixel, bit 3/7 per
-// branch) and rule R* is evaluated bit-sliced, 8 pixel-branches per LOP3.  The
+// FADD.SAT turns them into 0/1 flags which FFMAs assemble into flag words (byte
+// per pixel, bit 3/7 per branch) -- all on the FMA pipe -- and rule R* is
+// evaluated bit-sliced, 8 pixel-branches per LOP3.  The
 // std gate counts zero crossings in bytes (exact integers) and tests the
 // interval {k : 25k - k^2 > 600 T^2} (R11).  The hybrid median is a sorting
 // network on packed u16x2 (VIMNMX3.U16x2).
@@ -41,6 +42,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "lfe_internal.h"
@@ -62,6 +64,7 @@ constexpr int kZBytes = 8 * 32 * 4;         // 8-row Z ring per warp
 constexpr int kRBytes = 2 * 32 * 32;        // 2-row r ring per warp (zero-pixel slow path)
 constexpr int kHdr = 128;                   // mbarriers
 constexpr int kEdge = 16;                   // rows near the image top/bottom walked separately
+constexpr int kMaxGrid = 192;               // largest grid the weighted partition table serves
 
 struct FusedArgs {
     float c[2][6];          // orbit coefficients (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
@@ -74,6 +77,8 @@ struct FusedArgs {
     int o0, o1;             // output rows
     int col_groups;
     int cap;                // max rows per piece (0 = whole contiguous range; tuning/tests)
+    int nb;                 // > 0: CTA b owns units [bounds[b], bounds[b+1]) (cost-weighted partition)
+    int bounds[kMaxGrid + 1];
     void *out;
     long long out_pitch;
     unsigned long long *dbg;  // optional per-CTA [start, end, items] globaltimer record (LFE_DEBUG_TIMING)
@@ -171,19 +176,16 @@ __device__ __forceinline__ uint32_t med9(uint32_t v0, uint32_t v1, uint32_t v2, 
 // pixel pair shifted by one: (a.hi, b.lo)
 __device__ __forceinline__ uint32_t sh1(uint32_t a, uint32_t b) { return prmt(a, b, 0x5432); }
 
-// Sign bits of v[branch][px] -> flag layout: byte px, bit 3 + 4*branch (a
-// funnel shift by 4 leaves each sign at the top of its nibble).
-__device__ __forceinline__ uint32_t pack_signs(const float (&v)[2][4])
+// Flags f[branch][px] in {0.0, 1.0} (from FADD.SAT on exact integers) -> the same
+// layout, assembled on the FMA pipe: 2^23 + 8 f[0][2k] + 128 f[1][2k] + 2048 f[0][2k+1]
+// + 32768 f[1][2k+1] is exact, so its low mantissa bytes ARE the flag bytes of pixels
+// 2k and 2k+1; one PRMT joins the two halves.
+__device__ __forceinline__ uint32_t pack_flags(const float (&f)[2][4])
 {
-    uint32_t w = __float_as_uint(v[1][3]) >> 28;
-    w = __funnelshift_l(__float_as_uint(v[0][3]), w, 4);
-    w = __funnelshift_l(__float_as_uint(v[1][2]), w, 4);
-    w = __funnelshift_l(__float_as_uint(v[0][2]), w, 4);
-    w = __funnelshift_l(__float_as_uint(v[1][1]), w, 4);
-    w = __funnelshift_l(__float_as_uint(v[0][1]), w, 4);
-    w = __funnelshift_l(__float_as_uint(v[1][0]), w, 4);
-    w = __funnelshift_l(__float_as_uint(v[0][0]), w, 4);
-    return w & 0x88888888u;
+    const float m = 8388608.0f;
+    const float lo = fmaf(f[1][1], 32768.0f, fmaf(f[0][1], 2048.0f, fmaf(f[1][0], 128.0f, fmaf(f[0][0], 8.0f, m))));
+    const float hi = fmaf(f[1][3], 32768.0f, fmaf(f[0][3], 2048.0f, fmaf(f[1][2], 128.0f, fmaf(f[0][2], 8.0f, m))));
+    return prmt(__float_as_uint(lo), __float_as_uint(hi), 0x5410);
 }
 
 // u16 / u8 -> exact fp32 (2^23 + v, minus 2^23)
@@ -276,6 +278,11 @@ struct Pieces {
     long long u, u1;
     __device__ __forceinline__ void init(const FusedArgs &a)
     {
+        if (a.nb > 0) {
+            u = a.bounds[blockIdx.x];
+            u1 = a.bounds[blockIdx.x + 1];
+            return;
+        }
         const long long U = (long long)a.col_groups * (a.o1 - a.o0);
         u = U * blockIdx.x / gridDim.x;
         u1 = U * (blockIdx.x + 1) / gridDim.x;
@@ -468,8 +475,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // rho-9, input+LoG for row rho, zero crossings for row rho-3.
     auto step = [&](auto fix_tag, int rho, float(&rB)[2][4], float(&rC)[2][4]) {
         constexpr bool XF = decltype(fix_tag)::value & 1, YF = decltype(fix_tag)::value & 2;
-        // Cheap column edges (W % 4 == 0), in the interior code itself (branch-free selects,
-        // so one hot loop fits the instruction cache).  The lane holding column 0
+        constexpr bool XQ = decltype(fix_tag)::value & 4;
+        // XQ: cheap column edges (W % 4 == 0; chosen per CTA piece, so all warps of an SM
+        // run the same code).  The lane holding column 0
         // (isL) / column W-1 at its pixel 3 (isR) substitutes its own edge values for the
         // neighbours across the edge -- per-stage replicate padding without touching the
         // outside columns.
@@ -490,8 +498,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t V0 = V & 0x0F0F0F0Fu, V1 = (V >> 4) & 0x0F0F0F0Fu;
         uint32_t Lw = __shfl_up_sync(0xffffffffu, prmt(V0, V1, 0x7632), 1);
         uint32_t Rw = __shfl_down_sync(0xffffffffu, prmt(V0, V1, 0x5410), 1);
-        Lw = isL ? prmt(V0, V1, 0x4400) : Lw;
-        Rw = isR ? prmt(V0, V1, 0x7733) : Rw;
+        if constexpr (XQ) Lw = isL ? prmt(V0, V1, 0x4400) : Lw;
+        if constexpr (XQ) Rw = isR ? prmt(V0, V1, 0x7733) : Rw;
         const uint32_t K0 = V0 + prmt(V0, Lw, 0x2105) + prmt(V0, Lw, 0x1054) + prmt(V0, Rw, 0x4321) + prmt(V0, Rw, 0x5432);
         const uint32_t K1 = V1 + prmt(V1, Lw, 0x2107) + prmt(V1, Lw, 0x1076) + prmt(V1, Rw, 0x6321) + prmt(V1, Rw, 0x7632);
         const uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
@@ -535,8 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 E[k][1] = lo.y;
                 E[k][2] = hi.x;
                 E[k][3] = hi.y;
-                E[k][0] = isL ? prmt(E[k][1], 0, 0x1010) : E[k][0];
-                E[k][3] = isR ? prmt(E[k][2], 0, 0x3232) : E[k][3];
+                if constexpr (XQ) E[k][0] = isL ? prmt(E[k][1], 0, 0x1010) : E[k][0];
+                if constexpr (XQ) E[k][3] = isR ? prmt(E[k][2], 0, 0x3232) : E[k][3];
             }
             const uint32_t s2a = sh1(E[2][0], E[2][1]), s2b = sh1(E[2][1], E[2][2]), s2c = sh1(E[2][2], E[2][3]);
             const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
@@ -585,10 +593,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 I[7] = byte_f(wr, 0x5441);
             }
         }
-        I[0] = isL ? I[2] : I[0];
-        I[1] = isL ? I[2] : I[1];
-        I[6] = isR ? I[5] : I[6];
-        I[7] = isR ? I[5] : I[7];
+        if constexpr (XQ) I[0] = isL ? I[2] : I[0];
+        if constexpr (XQ) I[1] = isL ? I[2] : I[1];
+        if constexpr (XQ) I[6] = isR ? I[5] : I[6];
+        if constexpr (XQ) I[7] = isR ? I[5] : I[7];
         if constexpr (XF) {
             float own4[4] = {I[2], I[3], I[4], I[5]};
             fix_floats(fx, own4);
@@ -641,60 +649,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             rn[j][1] = rB[j][2];
             rn[j][2] = rB[j][3];
             rn[j][3] = __shfl_down_sync(0xffffffffu, rB[j][0], 1);
-            rn[j][3] = isR ? rB[j][3] : rn[j][3];
+            if constexpr (XQ) rn[j][3] = isR ? rB[j][3] : rn[j][3];
         }
         float t[2][4];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = 0.0f - rC[j][i];
-        const uint32_t PC = pack_signs(t), NC = pack_signs(rC);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rC[j][i]);
+        const uint32_t PC = pack_flags(t);
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = rB[j][i] + rC[j][i];
-        const uint32_t Dm = pack_signs(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rC[j][i]);
+        const uint32_t NC = pack_flags(t);
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = -rB[j][i] - rC[j][i];
-        const uint32_t Dp = pack_signs(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rB[j][i] - rC[j][i]);
+        const uint32_t Dm = pack_flags(t);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rB[j][i] + rC[j][i]);
+        const uint32_t Dp = pack_flags(t);
         uint32_t Dng = 0, Rng = 0;
         if constexpr (GAP) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = fabsf(rB[j][i] - rC[j][i]) - a.tg[j];
-            Dng = pack_signs(t);
+                for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(a.tg[j] - fabsf(rB[j][i] - rC[j][i]));
+            Dng = pack_flags(t);
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = rB[j][i] + rn[j][i];
-        const uint32_t Rm = pack_signs(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rB[j][i] - rn[j][i]);
+        const uint32_t Rm = pack_flags(t);
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = -rB[j][i] - rn[j][i];
-        const uint32_t Rp = pack_signs(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rB[j][i] + rn[j][i]);
+        const uint32_t Rp = pack_flags(t);
         if constexpr (GAP) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = fabsf(rB[j][i] - rn[j][i]) - a.tg[j];
-            Rng = pack_signs(t);
+                for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(a.tg[j] - fabsf(rB[j][i] - rn[j][i]));
+            Rng = pack_flags(t);
         }
         // neighbours' flag bytes across lanes
         uint32_t PBl = __shfl_up_sync(0xffffffffu, PB, 1), NBl = __shfl_up_sync(0xffffffffu, NB, 1);
         uint32_t Rml = __shfl_up_sync(0xffffffffu, Rm, 1), Rpl = __shfl_up_sync(0xffffffffu, Rp, 1);
         uint32_t PBr = __shfl_down_sync(0xffffffffu, PB, 1), NBr = __shfl_down_sync(0xffffffffu, NB, 1);
         // column -1 := column 0 (the edge between them joins equal values); column W := W-1
-        PBl = isL ? PB << 24 : PBl;
-        NBl = isL ? NB << 24 : NBl;
-        Rml = isL ? NB << 24 : Rml;
-        Rpl = isL ? PB << 24 : Rpl;
-        PBr = isR ? PB >> 24 : PBr;
-        NBr = isR ? NB >> 24 : NBr;
+        if constexpr (XQ) PBl = isL ? PB << 24 : PBl;
+        if constexpr (XQ) NBl = isL ? NB << 24 : NBl;
+        if constexpr (XQ) Rml = isL ? NB << 24 : Rml;
+        if constexpr (XQ) Rpl = isL ? PB << 24 : Rpl;
+        if constexpr (XQ) PBr = isR ? PB >> 24 : PBr;
+        if constexpr (XQ) NBr = isR ? NB >> 24 : NBr;
         const uint32_t PL = prmt(PB, PBl, 0x2107), NL = prmt(NB, NBl, 0x2107);
         const uint32_t PR = prmt(PB, PBr, 0x4321), NR = prmt(NB, NBr, 0x4321);
         const uint32_t Lm = prmt(Rm, Rml, 0x2107), Lp = prmt(Rp, Rpl, 0x2107);
@@ -704,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t XG, YG;
         if constexpr (GAP) {
             uint32_t Rngl = __shfl_up_sync(0xffffffffu, Rng, 1);
-            Rngl = isL ? a.ung_top : Rngl;
+            if constexpr (XQ) Rngl = isL ? a.ung_top : Rngl;
             const uint32_t Lng = prmt(Rng, Rngl, 0x2107);
             XG = (NA & ~Ung) | (NC & ~Dng) | (NR & ~Rng) | (NL & ~Lng);
             YG = (PA & ~Ung) | (PC & ~Dng) | (PR & ~Rng) | (PL & ~Lng);
@@ -724,8 +737,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float rU[2][4] = {{u0.x, u0.y, u0.z, u0.w}, {u1.x, u1.y, u1.z, u1.w}};
                 float l0 = __shfl_up_sync(0xffffffffu, rB[0][3], 1);
                 float l1 = __shfl_up_sync(0xffffffffu, rB[1][3], 1);
-                l0 = isL ? rB[0][0] : l0;
-                l1 = isL ? rB[1][0] : l1;
+                if constexpr (XQ) l0 = isL ? rB[0][0] : l0;
+                if constexpr (XQ) l1 = isL ? rB[1][0] : l1;
                 if (z0) {
 #pragma unroll
                     for (int j = 0; j < 2; ++j)
@@ -816,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&full[g % kS], (g / kS) & 1);
             }
             const int n = min(kR, rho_end - rho);
-            for (int k = 0; k < n; k += 2) {
+            for (int k = 0; k < n; k += 2) {  // x2: the centre / new r rows swap roles without moves
                 step(fix_tag, rho + k, rX, rY);
                 step(fix_tag, rho + k + 1, rY, rX);
             }
@@ -867,10 +880,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         isR = xw + 128 > W && dr >= 0 && lane == (dr >> 2);
         // path: 0 interior; 4 cheap column edges (W % 4 == 0); 3 general fix-ups (edge rows,
         // or column edges of widths that are not a multiple of 4)
-        const bool xedge = (xw < 0 || xw + 128 > W) && !a.dbg_nofix;
-        if (it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge && (W & 3))) {
+        // CTA-uniform path choice (one code path per SM at a time keeps the hot loop in
+        // the instruction cache): 0 interior; 4 cheap column edges (W % 4 == 0); 3 general
+        // fix-ups (edge rows, or column edges of other widths)
+        const bool xedge_cta = (it.xo - kHaloX < 0 || it.xo - kHaloX + (kWarps - 1) * kWarpOut + 128 > W) && !a.dbg_nofix;
+        if (it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge_cta && (W & 3))) {
             isL = isR = false;
             walk(std::integral_constant<int, 3>{});
+        } else if (xedge_cta) {
+            walk(std::integral_constant<int, 4>{});
         } else {
             walk(std::integral_constant<int, 0>{});
         }
@@ -891,10 +909,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (a.dbg && threadIdx.x == 0) {
         unsigned sm;
         asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
-        a.dbg[4 * blockIdx.x + 0] = t_start;
-        a.dbg[4 * blockIdx.x + 1] = gtime();
-        a.dbg[4 * blockIdx.x + 2] = c_idx;
-        a.dbg[4 * blockIdx.x + 3] = sm;
+        Pieces pr;
+        pr.init(a);
+        a.dbg[6 * blockIdx.x + 0] = t_start;
+        a.dbg[6 * blockIdx.x + 1] = gtime();
+        a.dbg[6 * blockIdx.x + 2] = c_idx;
+        a.dbg[6 * blockIdx.x + 3] = sm;
+        a.dbg[6 * blockIdx.x + 4] = pr.u;
+        a.dbg[6 * blockIdx.x + 5] = pr.u1;
     }
 }
 
@@ -936,6 +958,79 @@ bool interval_of(uint64_t lut, int L, int *lo, int *hi)
     return true;
 }
 
+// Cost-weighted static partition of the (column group, row) unit line over the
+// grid.  cost(u0, u1) replays the device's piece splitting: every piece pays a
+// pipeline warm-up, edge-row pieces run the general path, and units of the two
+// edge column groups run the column-edge code.  A greedy fill with a binary
+// search on the per-CTA cost cap balances the CTAs.  Constants fitted to a
+// per-CTA globaltimer trace (LFE_DEBUG_TIMING, scripts/partition_fit.py).
+namespace part {
+constexpr double kPiece = 35.0;      // row-equivalents per piece (pipeline warm-up)
+constexpr double kEdgePiece = 17.0;  // extra for an edge-row piece (general path)
+constexpr double kEdgeCol = 1.066;   // column-edge group, cheap path (W % 4 == 0)
+constexpr double kEdgeColGen = 1.40; // column-edge group, general path
+
+double cost(const FusedArgs &fa, long long u0, long long u1, int halo)
+{
+    const int G = fa.col_groups, R = fa.o1 - fa.o0;
+    double c = 0.0;
+    long long u = u0;
+    while (u < u1) {
+        const int g = (int)(u / R), r0 = (int)(u - (long long)g * R);
+        const int n = (int)std::min<long long>(R - r0, u1 - u);
+        const double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kEdgeCol) : 1.0;
+        int ys = fa.o0 + r0;
+        const int ye_all = ys + n;
+        while (ys < ye_all) {  // the kernel's split at kEdge rows from the virtual top/bottom
+            int ye = ye_all;
+            if (ys < kEdge && ye > kEdge) ye = kEdge;
+            if (ys < fa.H - kEdge && ye > fa.H - kEdge) ye = fa.H - kEdge;
+            const bool edge = ys - halo < 0 || ye + halo > fa.H;
+            c += f * ((ye - ys) + kPiece + (edge ? kEdgePiece : 0.0));
+            ys = ye;
+        }
+        u += n;
+    }
+    return c;
+}
+
+// CTAs needed when no CTA may exceed cost `cap` (filling bounds when given)
+int fill(const FusedArgs &fa, double cap, int halo, int grid, int *bounds)
+{
+    const long long U = (long long)fa.col_groups * (fa.o1 - fa.o0);
+    long long u = 0;
+    int b = 0;
+    if (bounds) bounds[0] = 0;
+    while (u < U) {
+        if (b >= grid) return grid + 1;
+        long long lo = u + 1, hi = U;  // largest u1 with cost(u, u1) <= cap (at least one unit)
+        while (lo < hi) {
+            const long long mid = (lo + hi + 1) / 2;
+            if (cost(fa, u, mid, halo) <= cap) lo = mid; else hi = mid - 1;
+        }
+        u = lo;
+        ++b;
+        if (bounds) bounds[b] = (int)u;
+    }
+    if (bounds)
+        for (int i = b + 1; i <= grid; ++i) bounds[i] = (int)U;
+    return b;
+}
+}  // namespace part
+
+void weighted_partition(FusedArgs &fa, int grid, int halo)
+{
+    const long long U = (long long)fa.col_groups * (fa.o1 - fa.o0);
+    fa.nb = 0;
+    if (grid > kMaxGrid || grid < 2 || fa.cap > 0 || U >= (1LL << 31) || U < 4LL * grid) return;
+    double lo = part::cost(fa, 0, U, halo) / grid, hi = part::cost(fa, 0, U, halo);
+    for (int it = 0; it < 40 && hi - lo > 0.5; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (part::fill(fa, mid, halo, grid, nullptr) <= grid) hi = mid; else lo = mid;
+    }
+    if (part::fill(fa, hi, halo, grid, fa.bounds) <= grid) fa.nb = grid;
+}
+
 template <bool IN16>
 constexpr size_t fused_smem()
 {
@@ -960,18 +1055,22 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
     const long long units = (long long)fa.col_groups * (fa.o1 - fa.o0);
     const int grid = units < grid_cap ? (int)units : grid_cap;
     cudaError_t e = cudaSuccess;
+    FusedArgs fw = fa;
+    weighted_partition(fw, grid, HM ? 7 : 5);
     static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
-    FusedArgs fb = fa;
+    FusedArgs fb = fw;
     fb.dbg = nullptr;
-    if (dbg_path) cudaMalloc(&fb.dbg, sizeof(unsigned long long) * 4 * grid);
+    if (dbg_path) cudaMalloc(&fb.dbg, sizeof(unsigned long long) * 6 * grid);
     kfn<<<grid, kThreads, smem, s>>>(map, fb, err_flag);
     e = cudaGetLastError();
     if (dbg_path && fb.dbg) {  // debug only: synchronous dump of the per-CTA timeline
         cudaStreamSynchronize(s);
-        unsigned long long *h = new unsigned long long[4 * grid];
-        cudaMemcpy(h, fb.dbg, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost);
+        unsigned long long *h = new unsigned long long[6 * grid];
+        cudaMemcpy(h, fb.dbg, sizeof(unsigned long long) * 6 * grid, cudaMemcpyDeviceToHost);
         if (FILE *f = fopen(dbg_path, "a")) {
-            for (int i = 0; i < grid; ++i) fprintf(f, "%d %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            for (int i = 0; i < grid; ++i)
+                fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", i, h[6 * i], h[6 * i + 1], h[6 * i + 2], h[6 * i + 3],
+                        h[6 * i + 4], h[6 * i + 5]);
             fprintf(f, "---\n");
             fclose(f);
         }

@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         return b * kBoxBytes + (c - b * kBoxCols) * kElem;
     };
     const int cl = warp * kWarpOut + 4 * lane;  // CTA-local column of this lane's pixel 0
-    const int off_own = col_off(cl), off_l = col_off(cl - 2), off_r = col_off(cl + 4);
+    const int off_own = col_off(cl);
 
     float c00[2], c10[2], c20[2], c11[2], c21[2], c22[2];
 #pragma unroll
@@ -569,14 +569,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             I[3] = hi16f(own.x);
             I[4] = lo16f(own.y);
             I[5] = hi16f(own.y);
-            if constexpr (!XF) {
-                const uint32_t wl = *reinterpret_cast<const uint32_t *>(rowp + off_l);
-                const uint32_t wr = *reinterpret_cast<const uint32_t *>(rowp + off_r);
-                I[0] = lo16f(wl);
-                I[1] = hi16f(wl);
-                I[6] = lo16f(wr);
-                I[7] = hi16f(wr);
-            }
         } else {
             const uint32_t own = *reinterpret_cast<const uint32_t *>(rowp + off_own);
             range_acc |= own & in_lo;
@@ -584,19 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             I[3] = byte_f(own, 0x5441);
             I[4] = byte_f(own, 0x5442);
             I[5] = byte_f(own, 0x5443);
-            if constexpr (!XF) {
-                const uint32_t wl = *reinterpret_cast<const uint16_t *>(rowp + off_l);
-                const uint32_t wr = *reinterpret_cast<const uint16_t *>(rowp + off_r);
-                I[0] = byte_f(wl, 0x5440);
-                I[1] = byte_f(wl, 0x5441);
-                I[6] = byte_f(wr, 0x5440);
-                I[7] = byte_f(wr, 0x5441);
-            }
         }
-        if constexpr (XQ) I[0] = isL ? I[2] : I[0];
-        if constexpr (XQ) I[1] = isL ? I[2] : I[1];
-        if constexpr (XQ) I[6] = isR ? I[5] : I[6];
-        if constexpr (XQ) I[7] = isR ? I[5] : I[7];
         if constexpr (XF) {
             float own4[4] = {I[2], I[3], I[4], I[5]};
             fix_floats(fx, own4);
@@ -604,11 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             I[3] = own4[1];
             I[4] = own4[2];
             I[5] = own4[3];
-            I[0] = __shfl_up_sync(0xffffffffu, I[4], 1);
-            I[1] = __shfl_up_sync(0xffffffffu, I[5], 1);
-            I[6] = __shfl_down_sync(0xffffffffu, I[2], 1);
-            I[7] = __shfl_down_sync(0xffffffffu, I[3], 1);
         }
+        // the two pixels left/right of this lane's four come from the neighbouring lanes
+        // (lane 0's left and lane 31's right values only feed halo columns never used)
+        I[0] = __shfl_up_sync(0xffffffffu, I[4], 1);
+        I[1] = __shfl_up_sync(0xffffffffu, I[5], 1);
+        I[6] = __shfl_down_sync(0xffffffffu, I[2], 1);
+        I[7] = __shfl_down_sync(0xffffffffu, I[3], 1);
+        if constexpr (XQ) I[0] = isL ? I[2] : I[0];
+        if constexpr (XQ) I[1] = isL ? I[2] : I[1];
+        if constexpr (XQ) I[6] = isR ? I[5] : I[6];
+        if constexpr (XQ) I[7] = isR ? I[5] : I[7];
 
         // ---------------- LoG x 2, streaming over rows ----------------
 #pragma unroll

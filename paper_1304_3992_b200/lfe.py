@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblfe.so")
+LIB_PATH = os.environ.get("LFE_LIB") or os.path.join(_PKG, "liblfe.so")  # LFE_LIB: A/B experiments only
 
 LFE_OK, LFE_EINVAL, LFE_EUNSUPPORTED, LFE_ENOMEM, LFE_ENODEV, LFE_ECUDA, LFE_ERANGE = range(7)
 LFE_STD_ZC, LFE_STD_INTENSITY = 0, 1

@@ -491,9 +491,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             Zc = zRing[(row_e & 7) * 32 + lane];
         } else {
             V = 0;
+            Zc = 0;
+            if (row_e >= 0) {  // rows above the image only feed discarded outputs (and row 0 may be in flight)
 #pragma unroll
-            for (int k = -2; k <= 2; ++k) V += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
-            Zc = zRing[(min(max(row_e, 0), H - 1) & 7) * 32 + lane];
+                for (int k = -2; k <= 2; ++k) V += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
+                Zc = zRing[(min(row_e, H - 1) & 7) * 32 + lane];
+            }
         }
         const uint32_t V0 = V & 0x0F0F0F0Fu, V1 = (V >> 4) & 0x0F0F0F0Fu;
         uint32_t Lw = __shfl_up_sync(0xffffffffu, prmt(V0, V1, 0x7632), 1);
@@ -537,8 +540,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int r = row_o - 2 + k;
                 if constexpr (YF) r = min(max(r, 0), H - 1);
                 const unsigned char *b = eRing + (r & 7) * kERow + 8 * lane;
-                const uint2 lo = *reinterpret_cast<const uint2 *>(b);
-                const uint2 hi = *reinterpret_cast<const uint2 *>(b + 8);
+                uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
+                if (!YF || row_o >= 0) {  // (YF) outputs above the image are discarded; row 0 may be in flight
+                    lo = *reinterpret_cast<const uint2 *>(b);
+                    hi = *reinterpret_cast<const uint2 *>(b + 8);
+                }
                 E[k][0] = lo.x;
                 E[k][1] = lo.y;
                 E[k][2] = hi.x;

@@ -1,0 +1,25 @@
+"""Small runs of both kernels for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from paper_1304_3992_b200 import lfe, scenes
+cases = [(scenes.scene_c1(), lfe.Params(bit_depth=8, zc_threshold=(0.02, 0.02))),
+         (scenes.scene_c3(size=1400, height=300), lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))),
+         (scenes.random_image(np.random.default_rng(1), 37, 53, 8), lfe.Params(bit_depth=8))]
+for kernel in (lfe.LFE_KERNEL_FUSED, lfe.LFE_KERNEL_STAGED):
+    for img, p in cases:
+        with lfe.Context(p) as ctx:
+            ctx.set_option(lfe.LFE_OPT_KERNEL, kernel)
+            H, W = img.shape
+            esz = img.dtype.itemsize
+            Wp = ((W * esz + 15) // 16) * 16 // esz
+            d = torch.zeros((H, Wp), dtype=torch.uint8 if esz == 1 else torch.uint16, device='cuda')[:, :W]
+            d.copy_(torch.from_numpy(img))
+            out = torch.zeros_like(d)
+            try:
+                ctx.extract(d, out)
+                ctx.check()
+                print('ok', kernel, img.shape)
+            except lfe.LfeError as e:
+                print('skip', kernel, img.shape, e)

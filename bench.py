@@ -8,6 +8,7 @@ OR merge -> hybrid median) over the c3 scene: 12000 x 12000 uint16 (10-bit),
 Cartosat-1-like synthetic PAN, resident in HBM.  At N > 1 (torchrun, one
 process per GPU) the scene is split into N row strips with an NCCL halo
 exchange of 7 boundary rows per neighbour (strong scaling: the scene is fixed).
+--median2 3 adds the water pipeline's second median level (8-row halo).
 Rank 0 prints one JSON line.  See DESIGN.md "Measurement".
 """
 from __future__ import annotations
@@ -40,29 +41,49 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--size", type=int, default=12000, help="scene side (default: c3's 12000)")
     ap.add_argument("--tile", type=str, default="", help="TWxTH override (tuning only)")
+    ap.add_argument("--median2", type=int, default=0, choices=[0, 3, 5, 7],
+                    help="second hybrid-median level (the water pipeline, PAPER.md:102); 0 = the c3 metric config")
     return ap.parse_args()
 
 
-def workload_params():
+def workload_params(median2=0):
     from paper_1304_3992_b200 import lfe
     # SURVEY.md 8(c) defaults for benchmark scenes: ZC gap 0.02 (normalised),
     # std source = ZC image, 5x5 window, T = 0.3, hybrid median on, extract.
     return lfe.Params(bit_depth=10, sigma=(0.5, 20.0), log_size=(5, 5), zc_threshold=(0.02, 0.02),
                       std_source=lfe.LFE_STD_ZC, std_window=5, std_threshold=(0.3, 0.3),
                       std3_threshold=(-1.0, -1.0), hybrid_median=True, median_window=5,
-                      out_mode=lfe.LFE_OUT_EXTRACT)
+                      out_mode=lfe.LFE_OUT_EXTRACT, median_window2=median2)
+
+
+def oracle_params(p):
+    import oracle
+    return oracle.Params(bit_depth=p.bit_depth, sigma=p.sigma, log_size=p.log_size, zc_threshold=p.zc_threshold,
+                         std_source=p.std_source, std_window=p.std_window, std_threshold=p.std_threshold,
+                         std3_threshold=p.std3_threshold, hybrid_median=p.hybrid_median,
+                         median_window=p.median_window, out_mode=p.out_mode, median_window2=p.median_window2)
+
+
+def halo_rows(p):
+    """Rows of real input an output band needs above/below (north_star's halo)."""
+    h = max(p.log_size) // 2 + 1 + p.std_window // 2
+    if p.hybrid_median:
+        h += p.median_window // 2 + p.median_window2 // 2
+    return h
 
 
 def config_dict(size, world, p):
+    hm = "5x5 hybrid median" + (f" + {p.median_window2}x{p.median_window2} second level" if p.median_window2 else "")
     return {
         "workload": f"c3: {size}x{size} uint16 (10-bit) synthetic Cartosat-1-like PAN scene, "
-                    "dual LoG (sigma 0.5, 20; 5x5) + ZC (gap 0.02) + 5x5 std gate (T=0.3) + OR + 5x5 hybrid median, extract",
+                    f"dual LoG (sigma 0.5, 20; 5x5) + ZC (gap 0.02) + 5x5 std gate (T=0.3) + OR + {hm}, extract",
         "width": size, "height": size, "bit_depth": 10, "bands": 1,
-        "parallelism": f"row strips x{world}, 7-row NCCL halo exchange" if world > 1 else "single GPU",
+        "parallelism": f"row strips x{world}, {halo_rows(p)}-row NCCL halo exchange" if world > 1 else "single GPU",
         "l2": "inputs larger than L2 (288 MB in + 288 MB out per step > 126 MB L2); no flush",
         "params": {"sigma": list(p.sigma), "log_size": list(p.log_size), "zc_threshold": list(p.zc_threshold),
                    "std_source": "zc", "std_window": p.std_window, "std_threshold": list(p.std_threshold),
-                   "hybrid_median": bool(p.hybrid_median), "median_window": p.median_window, "out_mode": "extract"},
+                   "hybrid_median": bool(p.hybrid_median), "median_window": p.median_window,
+                   "median_window2": p.median_window2, "out_mode": "extract"},
     }
 
 
@@ -149,24 +170,22 @@ def dist_setup(args):
 
 def cpu_baseline(img, p, rows=None):
     """The oracle as it stands, on the host cores, on a bounded sample of the
-    same workload: `rows` full-width rows (+7 halo rows each side); default the
+    same workload: `rows` full-width rows (+ halo rows each side); default the
     whole scene (about 6 s on 16 cores)."""
     import oracle
     H = img.shape[0]
+    h = halo_rows(p)
     rows = H if rows is None else min(rows, H)
     a = H // 2 - rows // 2
-    lo, hi = max(0, a - 7), min(H, a + rows + 7)
+    lo, hi = max(0, a - h), min(H, a + rows + h)
     band = img[lo:hi].copy()
-    op = oracle.Params(bit_depth=p.bit_depth, sigma=p.sigma, log_size=p.log_size, zc_threshold=p.zc_threshold,
-                       std_source=p.std_source, std_window=p.std_window, std_threshold=p.std_threshold,
-                       std3_threshold=p.std3_threshold, hybrid_median=p.hybrid_median,
-                       median_window=p.median_window, out_mode=p.out_mode)
+    op = oracle_params(p)
     t0 = time.perf_counter()
     oracle.run(band, op)
     dt = time.perf_counter() - t0
     px = rows * img.shape[1]  # output rows counted (halo rows are overhead)
     return {"value": round(px / dt / 1e6, 3), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"{rows} x {img.shape[1]} rows of the c3 scene (+7 halo rows each side), one run, "
+            "sample": f"{rows} x {img.shape[1]} rows of the c3 scene (+{h} halo rows each side), one run, "
                       f"{dt:.2f} s, plain C oracle -O2 OpenMP over rows"}
 
 
@@ -178,18 +197,16 @@ def run_reference(args, world, rank):
 
     import oracle
     from paper_1304_3992_b200 import scenes
-    p = workload_params()
+    p = workload_params(args.median2)
     img = scenes.scene_c3(size=args.size)
     rows = 512
     H, W = img.shape
-    op = oracle.Params(bit_depth=p.bit_depth, sigma=p.sigma, log_size=p.log_size, zc_threshold=p.zc_threshold,
-                       std_source=p.std_source, std_window=p.std_window, std_threshold=p.std_threshold,
-                       std3_threshold=p.std3_threshold, hybrid_median=p.hybrid_median,
-                       median_window=p.median_window, out_mode=p.out_mode)
+    h = halo_rows(p)
+    op = oracle_params(p)
     times = []
     for i in range(args.warmup + args.steps):
         a = (H // 2 - rows // 2 + 977 * i) % (H - rows)
-        band = np.ascontiguousarray(img[max(0, a - 7):min(H, a + rows + 7)])
+        band = np.ascontiguousarray(img[max(0, a - h):min(H, a + rows + h)])
         t0 = time.perf_counter()
         oracle.run(band, op)
         if i >= args.warmup:
@@ -201,7 +218,7 @@ def run_reference(args, world, rank):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": config_dict(args.size, world, p),
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
-                             "sample": f"each step: {rows} x {W} rows of c3 (+7 halo rows), plain C oracle -O2 OpenMP"},
+                             "sample": f"each step: {rows} x {W} rows of c3 (+{h} halo rows), plain C oracle -O2 OpenMP"},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -225,7 +242,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    p = workload_params()
+    p = workload_params(args.median2)
     size = args.size
     img = scenes.scene_c3(size=size)                      # host, numpy uint16
     H, W = img.shape
@@ -236,6 +253,7 @@ def main():
         ctx.set_option(lfe.LFE_OPT_TILE_W, tw)
         ctx.set_option(lfe.LFE_OPT_TILE_H, th)
     halo = ctx.halo
+    assert halo == halo_rows(p)
     shard = StripShard(H, W, rank, world, halo)
     buf = shard.alloc(torch.uint16, dev)
     shard.load_owned(img)

@@ -79,14 +79,17 @@ typedef struct lfe_params {
     int32_t hybrid_median;      /* 0 / 1                              */
     int32_t median_window;      /* odd 3, 5 or 7 (paper: 5x5)                             */
     int32_t out_mode;           /* LFE_OUT_EXTRACT (default) or LFE_OUT_MASK              */
-    int32_t reserved1;          /* must be 0                                             */
+    int32_t median_window2;     /* 0, or odd 3/5/7: a second hybrid-median level applied  */
+                                /* to the first one's output -- the water-body pipeline's */
+                                /* "multiple levels of higher and lower dimensions"       */
+                                /* (reading R17); needs hybrid_median = 1   */
 } lfe_params;
 
 typedef struct lfe_ctx lfe_ctx;
 
 /* Defaults of DESIGN.md: sigma (0.5, 20) sigma-direct, 5x5 masks, ZC threshold
- * 0, std source ZC, 5x5 window, T = 0.3, re-check off, hybrid median on (5x5),
- * extract mode, bit_depth 8. */
+ * 0, std source ZC, 5x5 window, T = 0.3, re-check off, hybrid median on (5x5,
+ * one level), extract mode, bit_depth 8. */
 void lfe_params_default(lfe_params *p);
 
 /* Validates p and synthesises both integer masks (Eq. 1 -> DC correction ->
@@ -132,7 +135,8 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch_bytes
                             int32_t height, void *h_out, int64_t out_pitch_bytes);
 
 /* Rows of real input needed above/below a strip for a bit-exact result:
- * LoG radius + 1 (ZC) + std radius + median radius (0 if off). */
+ * LoG radius + 1 (ZC) + std radius + median radius (0 if off) + second-level
+ * median radius (0 if none). */
 int32_t lfe_halo(const lfe_ctx *c);
 
 /* The integer mask of branch 0/1 (R3): coeffs[n*n] row-major (caller buffer

@@ -50,7 +50,7 @@ class _Params(ctypes.Structure):
         ("hybrid_median", ctypes.c_int32),
         ("median_window", ctypes.c_int32),
         ("out_mode", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("median_window2", ctypes.c_int32),
     ]
 
 
@@ -195,6 +195,7 @@ class Params:
     hybrid_median: bool = True
     median_window: int = 5
     out_mode: int = 0
+    median_window2: int = 0
 
     def to_c(self) -> _Params:
         p = _Params()
@@ -210,6 +211,7 @@ class Params:
         p.hybrid_median = int(bool(self.hybrid_median))
         p.median_window = self.median_window
         p.out_mode = self.out_mode
+        p.median_window2 = self.median_window2
         return p
 
 

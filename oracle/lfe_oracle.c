@@ -322,7 +322,7 @@ typedef struct lfo_params {
     int32_t hybrid_median;
     int32_t median_window;
     int32_t out_mode;     /* 0 = extract intensities, 1 = 0/255 mask */
-    int32_t pad_;
+    int32_t median_window2; /* 0 or a second hybrid-median level (R17) */
 } lfo_params;
 
 /* Optional intermediates (any may be NULL): r0/r1 int64[W*H], z0/z1, k0/k1
@@ -372,10 +372,18 @@ int lfo_run(const lfo_params *p, const uint16_t *I, int W, int H, uint16_t *out,
         if (k1o) memcpy(k1o, K[1], N);
         lfo_merge(K[0], K[1], I, W, H, p->out_mode, E);
         if (Eo) memcpy(Eo, E, N * sizeof(uint16_t));
-        if (p->hybrid_median)
+        if (p->hybrid_median) {
             lfo_hybrid_median(E, W, H, p->median_window, out);
-        else
+            if (p->median_window2 > 0) {
+                /* "passing through a hybrid median filter in multiple levels of higher
+                 * and lower dimensions": the next level filters the
+                 * previous level's output, padding it by replication again */
+                memcpy(E, out, N * sizeof(uint16_t));
+                lfo_hybrid_median(E, W, H, p->median_window2, out);
+            }
+        } else {
             memcpy(out, E, N * sizeof(uint16_t));
+        }
     }
     free(r); free(Z); free(K[0]); free(K[1]); free(E); free(src);
     return rc;

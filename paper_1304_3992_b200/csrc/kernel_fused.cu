@@ -62,6 +62,7 @@ constexpr int kERow = 264;                  // bytes per E ring row: 128 px + 2 
 constexpr int kEBytes = 8 * kERow;          // 8-row E ring per warp
 constexpr int kZBytes = 8 * 32 * 4;         // 8-row Z ring per warp
 constexpr int kRBytes = 2 * 32 * 32;        // 2-row r ring per warp (zero-pixel slow path)
+constexpr int kHBytes = 4 * kERow;          // 4-row ring of first-median-level rows (second level only)
 constexpr int kHdr = 128;                   // mbarriers
 constexpr int kEdge = 16;                   // rows near the image top/bottom walked separately
 constexpr int kMaxGrid = 192;               // largest grid the weighted partition table serves
@@ -171,6 +172,14 @@ __device__ __forceinline__ uint32_t med9(uint32_t v0, uint32_t v1, uint32_t v2, 
     uint32_t l2 = vmin2(vmin2(v6, v7), v8), h2 = vmax2(vmax2(v6, v7), v8), m2 = v6 ^ v7 ^ v8 ^ l2 ^ h2;
     uint32_t L = vmax2(vmax2(l0, l1), l2), Hh = vmin2(vmin2(h0, h1), h2);
     return med3(L, med3(m0, m1, m2), Hh);
+}
+
+// median of five: med3(max(min(a,b), min(c,d)), min(max(a,b), max(c,d)), e) -- the
+// larger of the two pair minima and the smaller of the two pair maxima bracket the
+// median of {a,b,c,d} with e (checked exhaustively on 5^5 inputs)
+__device__ __forceinline__ uint32_t med5(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e)
+{
+    return med3(vmax2(vmin2(a, b), vmin2(c, d)), vmin2(vmax2(a, b), vmax2(c, d)), e);
 }
 
 // pixel pair shifted by one: (a.hi, b.lo)
@@ -355,13 +364,20 @@ struct Producer {
     }
 };
 
-template <bool IN16, bool HM, bool MASKOUT, bool GAP>
+// rows of input needed beyond the output rows: LoG 2 + ZC 1 + std 2 (+ HM 2) (+ second level 1)
+__host__ __device__ constexpr int halo_of(int hml) { return hml == 2 ? 8 : hml == 1 ? 7 : 5; }
+__host__ __device__ constexpr int warp_bytes(int hml) { return kEBytes + kZBytes + kRBytes + (hml == 2 ? kHBytes : 0); }
+
+// HML: hybrid-median levels -- 0 none, 1 the 5x5 filter, 2 the 5x5 filter followed
+// by a 3x3 one on its output (the water pipeline's second level, R17)
+template <bool IN16, int HML, bool MASKOUT, bool GAP>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ FusedArgs a, int *err_flag)
 {
+    constexpr bool HM = HML >= 1, HM2 = HML == 2;
     constexpr int kElem = IN16 ? 2 : 1;
-    constexpr int kHalo = HM ? 7 : 5;  // input rows needed beyond the output rows (LoG 2 + ZC 1 + std 2 + HM 2)
-    constexpr int kLag = HM ? 9 : 6;   // pipeline delay: output row = input row - kLag
+    constexpr int kHalo = halo_of(HML);
+    constexpr int kLag = HM2 ? 11 : HM ? 9 : 6;  // pipeline delay: output row = input row - kLag
     // u16 images: 232-pixel boxes per row starting at column xo-8.  u8 images are
     // loaded through a u16 view of the same bytes: 240-element (480-pixel) boxes
     // starting at column xo-16 -- a TMA box must start on a 16-byte boundary
@@ -378,9 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *empty = full + kS;
     unsigned char *ring = smem + kHdr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char *eRing = ring + kS * kStageBytes + warp * (kEBytes + kZBytes + kRBytes);
+    unsigned char *eRing = ring + kS * kStageBytes + warp * warp_bytes(HML);
     uint32_t *zRing = reinterpret_cast<uint32_t *>(eRing + kEBytes);
     float4 *rRing = reinterpret_cast<float4 *>(eRing + kEBytes + kZBytes);  // [2 rows][32 lanes][2 float4]
+    unsigned char *hRing = eRing + kEBytes + kZBytes + kRBytes;              // (HM2) rows like the E ring
     const int W = a.W, H = a.H;
 
     const unsigned long long t_start = gtime();
@@ -563,6 +580,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t mp1 = med9(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
             const uint32_t mx1 = med9(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
             o1 = med3(mp1, mx1, c1);
+            if constexpr (XF && HM2) fix_pairs(fx, o0, o1);  // replicate-pad the first level's output too
+        }
+
+        // ---------------- second median level (3x3) for row rho-11 (first-level rows rho-12 .. rho-10) ----------------
+        uint32_t q0 = 0, q1 = 0;
+        if constexpr (HM2) {
+            const int row_q = rho - 11;
+            uint32_t Hq[3][4];  // rows row_q-1 .. row_q+1, pairs as in E above
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                int r = row_q - 1 + k;
+                if constexpr (YF) r = min(max(r, 0), H - 1);
+                const unsigned char *b = hRing + (r & 3) * kERow + 8 * lane;
+                uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
+                if (!YF || row_q >= 0) {
+                    lo = *reinterpret_cast<const uint2 *>(b);
+                    hi = *reinterpret_cast<const uint2 *>(b + 8);
+                }
+                Hq[k][0] = lo.x;
+                Hq[k][1] = lo.y;
+                Hq[k][2] = hi.x;
+                Hq[k][3] = hi.y;
+                if constexpr (XQ) Hq[k][0] = isL ? prmt(Hq[k][1], 0, 0x1010) : Hq[k][0];
+                if constexpr (XQ) Hq[k][3] = isR ? prmt(Hq[k][2], 0, 0x3232) : Hq[k][3];
+            }
+            // '+' group (centre, left, right, up, down) and 'x' group (centre, 4 diagonals), R16
+            const uint32_t u01 = sh1(Hq[0][0], Hq[0][1]), u12 = sh1(Hq[0][1], Hq[0][2]), u23 = sh1(Hq[0][2], Hq[0][3]);
+            const uint32_t m01 = sh1(Hq[1][0], Hq[1][1]), m12 = sh1(Hq[1][1], Hq[1][2]), m23 = sh1(Hq[1][2], Hq[1][3]);
+            const uint32_t d01 = sh1(Hq[2][0], Hq[2][1]), d12 = sh1(Hq[2][1], Hq[2][2]), d23 = sh1(Hq[2][2], Hq[2][3]);
+            const uint32_t c0 = Hq[1][1], c1 = Hq[1][2];
+            q0 = med3(med5(m01, m12, Hq[0][1], Hq[2][1], c0), med5(u01, u12, d01, d12, c0), c0);
+            q1 = med3(med5(m12, m23, Hq[0][2], Hq[2][2], c1), med5(u12, u23, d12, d23, c1), c1);
         }
 
         // ---------------- input row ----------------
@@ -784,7 +833,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 erow[0] = e0;
                 erow[1] = e1;
             }
-            if (rho - 9 >= it.ys && rho - 9 < it.ye) store(rho - 9, o0, o1);
+            if constexpr (HM2) {
+                const int row_o = rho - 9;
+                if (!YF || (row_o >= 0 && row_o <= H - 1)) {
+                    uint32_t *hrow = reinterpret_cast<uint32_t *>(hRing + (row_o & 3) * kERow + 4 + 8 * lane);
+                    hrow[0] = o0;
+                    hrow[1] = o1;
+                }
+                if (rho - 11 >= it.ys && rho - 11 < it.ye) store(rho - 11, q0, q1);
+            } else {
+                if (rho - 9 >= it.ys && rho - 9 < it.ye) store(rho - 9, o0, o1);
+            }
         } else {
             if (row_e >= it.ys && row_e < it.ye) store(row_e, e0, e1);
         }
@@ -1023,18 +1082,18 @@ void weighted_partition(FusedArgs &fa, int grid, int halo)
     if (part::fill(fa, hi, halo, grid, fa.bounds) <= grid) fa.nb = grid;
 }
 
-template <bool IN16>
+template <bool IN16, int HML>
 constexpr size_t fused_smem()
 {
     constexpr int nbox = IN16 ? (kCtaOut + 2 * kHaloX + 231) / 232 : (kCtaOut + 3 * kHaloX + 479) / 480;
-    return kHdr + (size_t)kS * nbox * (IN16 ? 232 * 2 : 480) * kR + (size_t)kWarps * (kEBytes + kZBytes + kRBytes);
+    return kHdr + (size_t)kS * nbox * (IN16 ? 232 * 2 : 480) * kR + (size_t)kWarps * warp_bytes(HML);
 }
 
-template <bool IN16, bool HM, bool MASKOUT, bool GAP>
+template <bool IN16, int HML, bool MASKOUT, bool GAP>
 cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HM, MASKOUT, GAP>;
-    constexpr size_t smem = fused_smem<IN16>();
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP>;
+    constexpr size_t smem = fused_smem<IN16, HML>();
     static int grid_cap = 0;
     if (!grid_cap) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1048,7 +1107,7 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
     const int grid = units < grid_cap ? (int)units : grid_cap;
     cudaError_t e = cudaSuccess;
     FusedArgs fw = fa;
-    weighted_partition(fw, grid, HM ? 7 : 5);
+    weighted_partition(fw, grid, halo_of(HML));
     static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
     FusedArgs fb = fw;
     fb.dbg = nullptr;
@@ -1081,6 +1140,7 @@ bool fused_supports(const KParams &kp, int bit_depth)
     if (kp.std_source != LFE_STD_ZC || kp.w != 5) return false;
     if (kp.recheck[0] || kp.recheck[1]) return false;
     if (kp.hm && kp.m != 5) return false;
+    if (kp.m2 && !(kp.hm && kp.m == 5 && kp.m2 == 3)) return false;
     for (int j = 0; j < 2; ++j) {
         if (kp.zc_t[j] >= (1 << 24)) return false;
         int lo, hi;
@@ -1132,25 +1192,32 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
 
-    const bool hm = kp.hm, mask = kp.out_mode == LFE_OUT_MASK, gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0;
+    const int hml = kp.m2 ? 2 : kp.hm ? 1 : 0;
+    const bool mask = kp.out_mode == LFE_OUT_MASK;
+    // the GAP variant is exact for t = 0 as well; the two-level filter only has that one
+    const bool gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || hml == 2;
 #define LFE_DISPATCH(A, B, C, D) \
-    if (in16 == A && hm == B && mask == C && gap == D) return launch_t<A, B, C, D>(fa, map, err_flag, s);
-    LFE_DISPATCH(true, true, false, true)
-    LFE_DISPATCH(true, true, false, false)
-    LFE_DISPATCH(true, true, true, true)
-    LFE_DISPATCH(true, true, true, false)
-    LFE_DISPATCH(true, false, false, true)
-    LFE_DISPATCH(true, false, false, false)
-    LFE_DISPATCH(true, false, true, true)
-    LFE_DISPATCH(true, false, true, false)
-    LFE_DISPATCH(false, true, false, true)
-    LFE_DISPATCH(false, true, false, false)
-    LFE_DISPATCH(false, true, true, true)
-    LFE_DISPATCH(false, true, true, false)
-    LFE_DISPATCH(false, false, false, true)
-    LFE_DISPATCH(false, false, false, false)
-    LFE_DISPATCH(false, false, true, true)
-    LFE_DISPATCH(false, false, true, false)
+    if (in16 == A && hml == B && mask == C && gap == D) return launch_t<A, B, C, D>(fa, map, err_flag, s);
+    LFE_DISPATCH(true, 1, false, true)
+    LFE_DISPATCH(true, 1, false, false)
+    LFE_DISPATCH(true, 1, true, true)
+    LFE_DISPATCH(true, 1, true, false)
+    LFE_DISPATCH(true, 0, false, true)
+    LFE_DISPATCH(true, 0, false, false)
+    LFE_DISPATCH(true, 0, true, true)
+    LFE_DISPATCH(true, 0, true, false)
+    LFE_DISPATCH(false, 1, false, true)
+    LFE_DISPATCH(false, 1, false, false)
+    LFE_DISPATCH(false, 1, true, true)
+    LFE_DISPATCH(false, 1, true, false)
+    LFE_DISPATCH(false, 0, false, true)
+    LFE_DISPATCH(false, 0, false, false)
+    LFE_DISPATCH(false, 0, true, true)
+    LFE_DISPATCH(false, 0, true, false)
+    LFE_DISPATCH(true, 2, false, true)
+    LFE_DISPATCH(true, 2, true, true)
+    LFE_DISPATCH(false, 2, false, true)
+    LFE_DISPATCH(false, 2, true, true)
 #undef LFE_DISPATCH
     return cudaErrorNotSupported;
 }

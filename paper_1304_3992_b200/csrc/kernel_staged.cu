@@ -9,7 +9,8 @@
 //   r  (tile + h - RL) -> zero crossing x2 PAPER.md:60 (Sec. 3.2), rule R*
 //   Z  (tile + Rs + Rm)-> std gate x 2     PAPER.md:64-72 (Eq. 2), :94
 //                      -> OR merge         PAPER.md:94 "combined together"
-//   E  (tile + Rm)     -> hybrid median    PAPER.md:76 (Sec. 3.4)
+//   E  (tile + Rm+Rm2) -> hybrid median    PAPER.md:76 (Sec. 3.4)
+//   M  (tile + Rm2)    -> 2nd median level PAPER.md:102 (reading R17), optional
 //   out (tile)         -> HBM
 //
 // Border semantics (reading R5): each stage pads ITS OWN input by replication.
@@ -61,6 +62,37 @@ __device__ __forceinline__ uint32_t median_n(uint32_t *v, int n)
     return v[n / 2];
 }
 
+// Hybrid median of region S at (vy, vx) with radius R (R16, R17):
+// med3(median of the '+' group, median of the 'x' group, centre), both groups
+// including the centre; neighbours at clamped coordinates (R5).
+__device__ __forceinline__ uint32_t hybrid_median_at(const uint16_t *S, const Region &RS, int vy, int vx, int R,
+                                                     int W, int Hv)
+{
+    uint32_t P[13], X[13];
+    int np = 0;
+    const uint32_t c = S[RS.idx(vy, vx)];
+    P[np] = c;
+    X[np] = c;
+    ++np;
+    for (int d = 1; d <= R; ++d) {
+        int ym = clampi(vy - d, 0, Hv - 1), yp = clampi(vy + d, 0, Hv - 1);
+        int xm = clampi(vx - d, 0, W - 1), xp = clampi(vx + d, 0, W - 1);
+        P[np] = S[RS.idx(vy, xm)];
+        X[np++] = S[RS.idx(ym, xm)];
+        P[np] = S[RS.idx(vy, xp)];
+        X[np++] = S[RS.idx(ym, xp)];
+        P[np] = S[RS.idx(ym, vx)];
+        X[np++] = S[RS.idx(yp, xm)];
+        P[np] = S[RS.idx(yp, vx)];
+        X[np++] = S[RS.idx(yp, xp)];
+    }
+    uint32_t a = median_n(P, np), b = median_n(X, np), cc = c;
+    cswap(a, b);
+    cswap(b, cc);
+    cswap(a, b);
+    return b;  // median of three
+}
+
 template <typename Tin>
 __global__ void __launch_bounds__(kThreads)
     staged_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, int TW, int TH,
@@ -73,12 +105,14 @@ __global__ void __launch_bounds__(kThreads)
     const int h = kp.halo;
     const int hr = h - kp.RL;      // LoG-response halo
     const int hz = hr - 1;         // ZC halo (= Rs + Rm)
-    const int he = kp.Rm;          // merged-image halo
+    const int hm2 = kp.Rm2;        // first-median-output halo (second level)
+    const int he = kp.Rm + hm2;    // merged-image halo
 
     const Region RI{y0 - h, x0 - h, TH + 2 * h, TW + 2 * h};
     const Region RR{y0 - hr, x0 - hr, TH + 2 * hr, TW + 2 * hr};
     const Region RZ{y0 - hz, x0 - hz, TH + 2 * hz, TW + 2 * hz};
     const Region RE{y0 - he, x0 - he, TH + 2 * he, TW + 2 * he};
+    const Region RM{y0 - hm2, x0 - hm2, TH + 2 * hm2, TW + 2 * hm2};
 
     uint16_t *sI = reinterpret_cast<uint16_t *>(smem);
     size_t off = ((size_t)RI.h * RI.w * sizeof(uint16_t) + 15) & ~(size_t)15;
@@ -87,6 +121,8 @@ __global__ void __launch_bounds__(kThreads)
     uint8_t *sZ = smem + off;
     off += ((size_t)2 * RZ.h * RZ.w + 15) & ~(size_t)15;
     uint16_t *sE = reinterpret_cast<uint16_t *>(smem + off);
+    off += ((size_t)RE.h * RE.w * sizeof(uint16_t) + 15) & ~(size_t)15;
+    uint16_t *sM = reinterpret_cast<uint16_t *>(smem + off);  // used only if kp.m2
 
     // ---- stage 0: input tile + halo, edge-replicated ("padded with 2 rows/columns")
     int bad = 0;
@@ -214,36 +250,26 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
 
-    // ---- stage 4: hybrid median (R16, R17) and store
+    // ---- stage 4 (second median level only): first level over tile + Rm2
+    if (kp.m2) {
+        for (int i = threadIdx.x; i < RM.h * RM.w; i += kThreads) {
+            int cy = clampi(RM.oy + i / RM.w, 0, Hv - 1);
+            int cx = clampi(RM.ox + i % RM.w, 0, W - 1);
+            sM[i] = (uint16_t)hybrid_median_at(sE, RE, cy, cx, kp.Rm, W, Hv);
+        }
+        __syncthreads();
+    }
+
+    // ---- stage 5: hybrid median (R16, R17) -- the first level, or
+    // the second one on the first level's output -- and store
     for (int i = threadIdx.x; i < TH * TW; i += kThreads) {
         int vy = y0 + i / TW, vx = x0 + i % TW;
         if (vy >= g.o1 || vx >= W) continue;
         uint32_t o;
-        if (kp.hm) {
-            const int R = kp.Rm;
-            uint32_t P[13], X[13];
-            int np = 0;
-            P[np] = sE[RE.idx(vy, vx)];
-            X[np] = P[np];
-            ++np;
-            for (int d = 1; d <= R; ++d) {
-                int ym = clampi(vy - d, 0, Hv - 1), yp = clampi(vy + d, 0, Hv - 1);
-                int xm = clampi(vx - d, 0, W - 1), xp = clampi(vx + d, 0, W - 1);
-                P[np] = sE[RE.idx(vy, xm)];
-                X[np++] = sE[RE.idx(ym, xm)];
-                P[np] = sE[RE.idx(vy, xp)];
-                X[np++] = sE[RE.idx(ym, xp)];
-                P[np] = sE[RE.idx(ym, vx)];
-                X[np++] = sE[RE.idx(yp, xm)];
-                P[np] = sE[RE.idx(yp, vx)];
-                X[np++] = sE[RE.idx(yp, xp)];
-            }
-            uint32_t c = sE[RE.idx(vy, vx)];
-            uint32_t a = median_n(P, np), b = median_n(X, np);
-            cswap(a, b);
-            cswap(b, c);
-            cswap(a, b);
-            o = b;  // median of three
+        if (kp.m2) {
+            o = hybrid_median_at(sM, RM, vy, vx, kp.Rm2, W, Hv);
+        } else if (kp.hm) {
+            o = hybrid_median_at(sE, RE, vy, vx, kp.Rm, W, Hv);
         } else {
             o = sE[RE.idx(vy, vx)];
         }
@@ -257,11 +283,12 @@ __global__ void __launch_bounds__(kThreads)
 
 size_t staged_smem(const KParams &kp, int TW, int TH)
 {
-    int h = kp.halo, hr = h - kp.RL, hz = hr - 1, he = kp.Rm;
+    int h = kp.halo, hr = h - kp.RL, hz = hr - 1, hm2 = kp.Rm2, he = kp.Rm + hm2;
     size_t s = (((size_t)(TH + 2 * h) * (TW + 2 * h) * 2) + 15) & ~(size_t)15;
     s += (size_t)2 * (TH + 2 * hr) * (TW + 2 * hr) * 4;
     s += ((size_t)2 * (TH + 2 * hz) * (TW + 2 * hz) + 15) & ~(size_t)15;
-    s += (size_t)(TH + 2 * he) * (TW + 2 * he) * 2;
+    s += (((size_t)(TH + 2 * he) * (TW + 2 * he) * 2) + 15) & ~(size_t)15;
+    if (kp.m2) s += (size_t)(TH + 2 * hm2) * (TW + 2 * hm2) * 2;
     return s;
 }
 
@@ -273,6 +300,7 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
     int TW = tile_w > 0 ? tile_w : 64;
     int TH = tile_h > 0 ? tile_h : 32;
     size_t smem = staged_smem(kp, TW, TH);
+    if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;  // tile too large for this halo
     dim3 grid((g.width + TW - 1) / TW, (g.o1 - g.o0 + TH - 1) / TH);
     if (grid.y == 0 || grid.x == 0) return cudaSuccess;
     if (in16) {

@@ -104,7 +104,7 @@ lfe_status validate(const lfe_params *p)
     if (!p) return fail(LFE_EINVAL, "params is NULL");
     if (p->abi_size != sizeof(lfe_params))
         return fail(LFE_EINVAL, "abi_size %u != sizeof(lfe_params) %zu", p->abi_size, sizeof(lfe_params));
-    if (p->reserved0 || p->reserved1) return fail(LFE_EINVAL, "reserved fields must be 0");
+    if (p->reserved0) return fail(LFE_EINVAL, "reserved fields must be 0");
     if (p->bit_depth < 1 || p->bit_depth > 16) return fail(LFE_EINVAL, "bit_depth %d not in 1..16", p->bit_depth);
     if (p->sigma_is_variance != 0 && p->sigma_is_variance != 1)
         return fail(LFE_EINVAL, "sigma_is_variance must be 0 or 1");
@@ -132,6 +132,12 @@ lfe_status validate(const lfe_params *p)
         return fail(LFE_EUNSUPPORTED, "median_window %d not in {3,5,7}", p->median_window);
     if (p->out_mode != LFE_OUT_EXTRACT && p->out_mode != LFE_OUT_MASK)
         return fail(LFE_EINVAL, "out_mode must be LFE_OUT_EXTRACT or LFE_OUT_MASK");
+    if (p->median_window2 != 0) {
+        if (!p->hybrid_median) return fail(LFE_EINVAL, "median_window2 needs hybrid_median = 1");
+        if (p->median_window2 < 1 || !(p->median_window2 & 1)) return fail(LFE_EINVAL, "median_window2 must be 0 or odd");
+        if (!odd_in(p->median_window2, 3, kMaxMedianWindow))
+            return fail(LFE_EUNSUPPORTED, "median_window2 %d not in {3,5,7}", p->median_window2);
+    }
     return LFE_OK;
 }
 
@@ -296,8 +302,10 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
     kp.hm = p->hybrid_median;
     kp.m = p->median_window;
     kp.Rm = p->hybrid_median ? p->median_window / 2 : 0;
+    kp.m2 = p->hybrid_median ? p->median_window2 : 0;
+    kp.Rm2 = kp.m2 / 2;
     kp.out_mode = p->out_mode;
-    kp.halo = kp.RL + 1 + kp.Rs + kp.Rm;
+    kp.halo = kp.RL + 1 + kp.Rs + kp.Rm + kp.Rm2;
 
     // d_err[0]: sticky ERANGE flag; d_err[1]: the fused kernel's work-queue counter
     if (cudaMalloc(&c->d_err, 2 * sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, 2 * sizeof(int)) != cudaSuccess) {

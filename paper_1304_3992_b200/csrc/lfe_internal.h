@@ -31,9 +31,11 @@ struct KParams {
     int32_t hm;                    // hybrid median on/off
     int32_t m;                     // median window side
     int32_t Rm;                    // median radius (0 if off)
+    int32_t m2;                    // second median level window (0 = none)
+    int32_t Rm2;                   // its radius
     int32_t out_mode;              // LFE_OUT_EXTRACT / LFE_OUT_MASK
     int32_t maxv;                  // 2^b - 1
-    int32_t halo;                  // RL + 1 + Rs + Rm
+    int32_t halo;                  // RL + 1 + Rs + Rm + Rm2
     // orbit coefficients of 5x5 masks for the fused kernel: (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
     int32_t orb[2][6];
 };

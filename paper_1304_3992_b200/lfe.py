@@ -52,7 +52,7 @@ class lfe_params(ctypes.Structure):
         ("hybrid_median", ctypes.c_int32),
         ("median_window", ctypes.c_int32),
         ("out_mode", ctypes.c_int32),
-        ("reserved1", ctypes.c_int32),
+        ("median_window2", ctypes.c_int32),
     ]
 
 
@@ -211,6 +211,7 @@ class Params:
     hybrid_median: bool = True
     median_window: int = 5
     out_mode: int = LFE_OUT_EXTRACT
+    median_window2: int = 0  # second hybrid-median level (water-body pipeline)
 
     def to_c(self) -> lfe_params:
         p = lfe_params()
@@ -227,6 +228,7 @@ class Params:
         p.hybrid_median = int(bool(self.hybrid_median))
         p.median_window = self.median_window
         p.out_mode = self.out_mode
+        p.median_window2 = self.median_window2
         return p
 
 

@@ -52,7 +52,7 @@ def test_abi_version_and_params_default():
     assert p.abi_size == ctypes.sizeof(lfe.lfe_params) == 112
     assert (p.bit_depth, p.sigma[0], p.sigma[1], p.log_size[0], p.log_size[1]) == (8, 0.5, 20.0, 5, 5)
     assert (p.std_source, p.std_window, p.std_threshold[0], p.std3_threshold[0]) == (0, 5, 0.3, -1.0)
-    assert (p.hybrid_median, p.median_window, p.out_mode) == (1, 5, 0)
+    assert (p.hybrid_median, p.median_window, p.out_mode, p.median_window2) == (1, 5, 0, 0)
     assert lfe.lfe_test_validate(p) == lfe.LFE_OK
     # the Python mirror of the defaults is the same struct
     q = lfe.Params().to_c()
@@ -92,6 +92,11 @@ def _with(**kw):
     (dict(median_window=11), lfe.LFE_EUNSUPPORTED),
     (dict(out_mode=3), lfe.LFE_EINVAL),
     (dict(reserved0=1), lfe.LFE_EINVAL),
+    (dict(median_window2=4), lfe.LFE_EINVAL),
+    (dict(median_window2=-3), lfe.LFE_EINVAL),
+    (dict(median_window2=9), lfe.LFE_EUNSUPPORTED),
+    (dict(median_window2=1), lfe.LFE_EUNSUPPORTED),
+    (dict(hybrid_median=0, median_window2=3), lfe.LFE_EINVAL),
 ])
 def test_validation_errors(kw, status):
     p = _with(**kw)

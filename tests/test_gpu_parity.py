@@ -28,7 +28,8 @@ def _oparams(p: lfe.Params) -> O.Params:
                     log_size=tuple(p.log_size), zc_threshold=tuple(p.zc_threshold),
                     std_source=p.std_source, std_window=p.std_window,
                     std_threshold=tuple(p.std_threshold), std3_threshold=tuple(p.std3_threshold),
-                    hybrid_median=p.hybrid_median, median_window=p.median_window, out_mode=p.out_mode)
+                    hybrid_median=p.hybrid_median, median_window=p.median_window, out_mode=p.out_mode,
+                    median_window2=p.median_window2)
 
 
 def _pitched(shape, dtype):
@@ -58,7 +59,8 @@ def run_gpu(img: np.ndarray, p: lfe.Params, kernel=lfe.LFE_KERNEL_AUTO, tile=Non
 
 def fused_ok(p: lfe.Params) -> bool:
     return (tuple(p.log_size) == (5, 5) and p.std_source == lfe.LFE_STD_ZC and p.std_window == 5
-            and max(p.std3_threshold) < 0 and (not p.hybrid_median or p.median_window == 5))
+            and max(p.std3_threshold) < 0 and (not p.hybrid_median or p.median_window == 5)
+            and (p.median_window2 == 0 or (p.hybrid_median and p.median_window == 5 and p.median_window2 == 3)))
 
 
 def assert_same(got, want, what=""):
@@ -98,12 +100,18 @@ def _param_cases():
                      std_window=7)
     yield lfe.Params(bit_depth=8, hybrid_median=False, std_threshold=(0.0, 0.0))
     yield lfe.Params(bit_depth=12, sigma=(1.0, 2.0), zc_threshold=(0.005, 0.0), out_mode=lfe.LFE_OUT_MASK)
+    # second hybrid-median level (water pipeline; reading R17)
+    yield lfe.Params(bit_depth=8, median_window=5, median_window2=3, zc_threshold=(0.01, 0.0))
+    yield lfe.Params(bit_depth=10, log_size=(7, 3), median_window=7, median_window2=7, std_window=7,
+                     out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=12, median_window=3, median_window2=5, std_source=lfe.LFE_STD_INTENSITY,
+                     std_threshold=(40.0, 90.0))
 
 
 SHAPES = [(1, 1), (1, 17), (23, 1), (2, 2), (5, 7), (37, 53), (64, 64), (65, 129), (130, 257), (300, 200)]
 
 
-@pytest.mark.parametrize("ci", range(12))
+@pytest.mark.parametrize("ci", range(15))
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_random_images_param_sweep(ci, kernel):
     p = list(_param_cases())[ci]
@@ -132,7 +140,7 @@ def _sampled_rows(img, p, got, bands):
     """Compare rows [a, b) of a full-size GPU result with the oracle run on the
     band plus a halo of real rows (clamped only at the true image edge)."""
     H = img.shape[0]
-    halo = 3 + 1 + 3 + 3 + 1  # >= any configuration's halo
+    halo = 3 + 1 + 3 + 3 + 3 + 1  # >= any configuration's halo (second median level included)
     for a, b in bands:
         lo, hi = max(0, a - halo), min(H, b + halo)
         ref = O.run(np.ascontiguousarray(img[lo:hi]), _oparams(p))
@@ -180,6 +188,31 @@ def test_strips_equal_whole_image(kernel):
                 ctx.extract_rows(strip, ha, b - a, ha, hb, flags, out, out_row0=a)
             ctx.check()
             assert_same(out.cpu().numpy(), whole, f"cuts {cuts}")
+
+
+@pytest.mark.parametrize("m2", [3, 7])
+def test_two_level_median_strips_and_host_path(m2):
+    """Second median level: whole image, row strips with the enlarged halo, and
+    the host-buffer strip pipeline all equal the oracle."""
+    img = scenes.scene_c1(size=160)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.01), median_window2=m2)
+    want = O.run(img, _oparams(p))
+    H, W = img.shape
+    with lfe.Context(p) as ctx:
+        h = ctx.halo
+        assert h == 7 + m2 // 2
+        d = torch.from_numpy(img).cuda()
+        assert_same(ctx.extract(d).cpu().numpy(), want, "whole")
+        out = torch.zeros_like(d)
+        for a, b in zip([0, 11, 80, 150], [11, 80, 150, 160]):
+            ha, hb = min(h, a), min(h, H - b)
+            flags = (lfe.LFE_TOP_IS_EDGE if a - ha == 0 else 0) | (lfe.LFE_BOTTOM_IS_EDGE if b + hb == H else 0)
+            ctx.extract_rows(d[a - ha:b + hb].clone(), ha, b - a, ha, hb, flags, out, out_row0=a)
+        ctx.check()
+        assert_same(out.cpu().numpy(), want, "strips")
+        for strip in (16, 64):
+            ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, strip)
+            assert_same(ctx.extract_host(img), want, f"host strips {strip}")
 
 
 def test_strip_halo_validation():
@@ -253,7 +286,7 @@ def test_dihedral_covariance_on_device():
 
 
 # ------------------------------------------------ fused-kernel specifics ----
-@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4, 10])
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4, 10, 12])
 def test_fused_random_images(ci):
     """The fused kernel forced on every shape (pitched buffers), bit-exact."""
     p = list(_param_cases())[ci]
@@ -300,3 +333,37 @@ def test_fused_column_edges_multiple_of_4(W):
         assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), f"W={W} b={bd}")
         p2 = lfe.Params(bit_depth=bd, hybrid_median=False, out_mode=lfe.LFE_OUT_MASK)
         assert_same(run_gpu(img, p2, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p2)), f"W={W} b={bd} nohm")
+
+
+# ------------------------------------- fused two-level hybrid median (5 then 3) ----
+@pytest.mark.parametrize("bd,mode,thr", [(8, lfe.LFE_OUT_EXTRACT, 0.0), (10, lfe.LFE_OUT_MASK, 0.01),
+                                         (16, lfe.LFE_OUT_EXTRACT, 0.02), (8, lfe.LFE_OUT_MASK, 0.0)])
+def test_fused_two_level_median(bd, mode, thr):
+    """The water pipeline's 5x5 + 3x3 hybrid median in the fused
+    kernel: every shape, both input widths, both output modes, bit-exact."""
+    p = lfe.Params(bit_depth=bd, zc_threshold=(thr, thr), median_window2=3, out_mode=mode)
+    assert fused_ok(p)
+    rng = np.random.default_rng(300 + bd + mode)
+    for (H, W), kind in itertools.product(SHAPES + [(33, 452), (9, 900), (129, 463), (40, 1348)], ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, bd, kind)
+        assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), f"{H}x{W} {kind}")
+
+
+@pytest.mark.parametrize("seg", [1, 5, 16, 33, 1000])
+def test_fused_two_level_segments_and_edges(seg):
+    img = scenes.scene_c1(size=300)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.01), median_window2=3)
+    want = O.run(img, _oparams(p))
+    assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED, (0, seg)), want, f"seg {seg}")
+    rng = np.random.default_rng(seg)
+    for W in (116, 120, 124, 1344, 1352):
+        im = scenes.random_image(rng, 30, W, 8, "mixed")
+        assert_same(run_gpu(im, p, lfe.LFE_KERNEL_FUSED, (0, seg)), O.run(im, _oparams(p)), f"W {W}")
+
+
+def test_fused_two_level_c3_sampled():
+    """c3 at full size with the two-level filter (AUTO picks the fused kernel)."""
+    img = scenes.scene_c3()
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), median_window2=3)
+    got = run_gpu(img, p)
+    _sampled_rows(img, p, got, [(0, 30), (7001, 7033), (11970, 12000)])

@@ -384,6 +384,33 @@ def test_hm_brute_force(m):
         np.testing.assert_array_equal(O.hybrid_median(E, m), _hm_brute(E, m))
 
 
+@pytest.mark.parametrize("m1,m2", [(5, 3), (3, 5), (7, 7), (5, 5)])
+def test_two_level_hm_is_the_composition(m1, m2):
+    """the water pipeline passes the merged image "through a hybrid
+    median filter in multiple levels"; reading R17 makes level 2 the same filter
+    (window m2, replicate padding) applied to level 1's output.  Checked against
+    the independent brute force applied twice to the oracle's merged image E."""
+    rng = np.random.default_rng(40 + m1 * 8 + m2)
+    I = scenes.random_image(rng, 13, 17, 8)
+    p = O.Params(bit_depth=8, median_window=m1, median_window2=m2, zc_threshold=(0.005, 0.0))
+    res = O.run(I, p, intermediates=True)
+    np.testing.assert_array_equal(res.out, _hm_brute(_hm_brute(res.E, m1), m2))
+    # the single-level run shares E and differs only in the last filter
+    one = O.run(I, O.Params(bit_depth=8, median_window=m1, zc_threshold=(0.005, 0.0)))
+    np.testing.assert_array_equal(one, _hm_brute(res.E, m1))
+
+
+def test_two_level_hm_keeps_thin_lines():
+    """The hybrid median's line preservation holds at every
+    level: a 1-px horizontal and a 1-px diagonal line survive 5 then 3."""
+    E = np.zeros((17, 17), np.uint16)
+    E[8, :] = 90
+    np.fill_diagonal(E, 90)
+    two = _hm_brute(_hm_brute(E, 5), 3)
+    assert (two[8, :] == 90).all()
+    assert (np.diag(two)[2:-2] == 90).all()
+
+
 def test_hm_output_values_come_from_window():
     rng = np.random.default_rng(8)
     E = rng.integers(0, 1000, (12, 12)).astype(np.uint16)
@@ -429,9 +456,10 @@ def _pipeline_cases():
     yield O.Params(bit_depth=8, out_mode=1, zc_threshold=(0.02, 0.01))
     yield O.Params(bit_depth=10, std_source=1, std_threshold=(20.0, 40.0), std3_threshold=(10.0, -1.0))
     yield O.Params(bit_depth=12, log_size=(3, 7), std_window=3, median_window=3)
+    yield O.Params(bit_depth=8, median_window=5, median_window2=3, zc_threshold=(0.01, 0.0))
 
 
-@pytest.mark.parametrize("pi", range(4))
+@pytest.mark.parametrize("pi", range(5))
 def test_pipeline_dihedral_covariance(pi):
     """Masks are 8-fold symmetric, N4 / square windows / +,x groups are dihedral
     invariant and replicate padding commutes: f(T I) = T f(I)."""
@@ -456,13 +484,14 @@ def test_pipeline_negation_keeps_the_kept_set():
         np.testing.assert_array_equal(O.run(Ineg, p), O.run(I, p))
 
 
-@pytest.mark.parametrize("hm,halo", [(True, 7), (False, 5)])
-def test_pipeline_strip_invariance_with_halo(hm, halo):
+@pytest.mark.parametrize("hm,m2,halo", [(True, 0, 7), (False, 0, 5), (True, 3, 8), (True, 7, 10)])
+def test_pipeline_strip_invariance_with_halo(hm, m2, halo):
     """Row strips with `halo` real rows above/below (clamping only at the true
     image edge) reproduce the whole-image result: the dependency cone of an
-    output row is LoG 2 + ZC 1 + std 2 (+ HM 2) rows."""
+    output row is LoG 2 + ZC 1 + std 2 (+ HM 2) (+ second HM level m2 // 2)
+    rows."""
     I = scenes.scene_c1(size=128)
-    p = O.Params(bit_depth=8, hybrid_median=hm, zc_threshold=(0.01, 0.01))
+    p = O.Params(bit_depth=8, hybrid_median=hm, median_window2=m2, zc_threshold=(0.01, 0.01))
     whole = O.run(I, p)
     H = I.shape[0]
     for a, b in [(0, 9), (9, 40), (40, 41), (41, 100), (100, 128), (57, 64)]:

@@ -51,6 +51,8 @@ class _Params(ctypes.Structure):
         ("median_window", ctypes.c_int32),
         ("out_mode", ctypes.c_int32),
         ("median_window2", ctypes.c_int32),
+        ("adaptive", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
     ]
 
 
@@ -78,6 +80,15 @@ def lib():
         L.lfo_run.argtypes = [ctypes.POINTER(_Params), P, ctypes.c_int, ctypes.c_int, P,
                               P, P, P, P, P, P, P]
         L.lfo_run.restype = ctypes.c_int
+        L.lfo_global_std_parts.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.c_uint64]
+        L.lfo_global_std_parts.restype = ctypes.c_double
+        L.lfo_std_of_response.argtypes = [P, ctypes.c_size_t]
+        L.lfo_std_of_response.restype = ctypes.c_double
+        L.lfo_std_of_intensity.argtypes = [P, ctypes.c_size_t]
+        L.lfo_std_of_intensity.restype = ctypes.c_double
+        L.lfo_adaptive_zc_threshold.argtypes = [ctypes.c_double, ctypes.c_double]
+        L.lfo_adaptive_zc_threshold.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -179,6 +190,30 @@ def hybrid_median(E: np.ndarray, m: int = 5) -> np.ndarray:
     return out
 
 
+# ------------------------------------------------- adaptive thresholds ----
+def global_std(n: int, s1: int, s2: int) -> float:
+    """R21: sqrt(n*S2 - S1^2) / n from exact integer sums (Python ints)."""
+    m = (1 << 64) - 1
+    s1u = s1 & ((1 << 128) - 1)
+    return float(lib().lfo_global_std_parts(int(n), s1u >> 64, s1u & m, (s2 >> 64) & m, s2 & m))
+
+
+def std_of_response(r: np.ndarray) -> float:
+    """global (population) standard deviation of a LoG response."""
+    r = np.ascontiguousarray(r, dtype=np.int64)
+    return float(lib().lfo_std_of_response(_ptr(r), r.size))
+
+
+def std_of_intensity(I: np.ndarray) -> float:
+    """global (population) standard deviation of the band."""
+    I = np.ascontiguousarray(I, dtype=np.uint16)
+    return float(lib().lfo_std_of_intensity(_ptr(I), I.size))
+
+
+def adaptive_zc_threshold(k: float, sigma_r: float) -> int:
+    return int(lib().lfo_adaptive_zc_threshold(float(k), float(sigma_r)))
+
+
 # ------------------------------------------------------------- pipeline ----
 @dataclass
 class Params:
@@ -196,6 +231,7 @@ class Params:
     median_window: int = 5
     out_mode: int = 0
     median_window2: int = 0
+    adaptive: int = 0  # bit 0: ZC gap k * sigma_r (R21); bit 1: std thresholds k * sigma_I (R22)
 
     def to_c(self) -> _Params:
         p = _Params()
@@ -212,6 +248,7 @@ class Params:
         p.median_window = self.median_window
         p.out_mode = self.out_mode
         p.median_window2 = self.median_window2
+        p.adaptive = self.adaptive
         return p
 
 

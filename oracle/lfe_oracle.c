@@ -309,6 +309,56 @@ void lfo_hybrid_median(const uint16_t *E, int W, int H, int m, uint16_t *out)
 /* ------------------------------------------------------------------ */
 /* Whole pipeline (Fig. 1 / Fig. 2 flow)              */
 /* ------------------------------------------------------------------ */
+/* ------------------------------------------------------------------ */
+/* O6 adaptive thresholds (NEXT-2) -- readings R21, R22 */
+/* ------------------------------------------------------------------ */
+/* Population standard deviation of n values from their exact sums S1 = sum v,
+ * S2 = sum v^2 (R21): sigma = sqrt(n*S2 - S1^2) / n, evaluated as written --
+ * the integer n*S2 - S1^2 exactly (128-bit), rounded once to double, sqrt, / n. */
+double lfo_global_std(int64_t n, __int128 S1, unsigned __int128 S2)
+{
+    if (n < 1) return 0.0;
+    __int128 D = (__int128)n * (__int128)S2 - S1 * S1;
+    return sqrt((double)D) / (double)n;
+}
+
+/* the same from (hi, lo) 64-bit halves, for the ctypes wrapper */
+double lfo_global_std_parts(int64_t n, int64_t s1_hi, uint64_t s1_lo, uint64_t s2_hi, uint64_t s2_lo)
+{
+    __int128 S1 = (__int128)(((unsigned __int128)(uint64_t)s1_hi << 64) | s1_lo);
+    unsigned __int128 S2 = ((unsigned __int128)s2_hi << 64) | s2_lo;
+    return lfo_global_std(n, S1, S2);
+}
+
+/* sigma of the LoG response r over the whole image ("global
+ * standard deviation of the LoG response") */
+double lfo_std_of_response(const int64_t *r, size_t N)
+{
+    __int128 S1 = 0;
+    unsigned __int128 S2 = 0;
+    for (size_t i = 0; i < N; ++i) {
+        S1 += r[i];
+        S2 += (unsigned __int128)((__int128)r[i] * r[i]);
+    }
+    return lfo_global_std((int64_t)N, S1, S2);
+}
+
+/* sigma of the input intensities ("global intensity standard
+ * deviation of the source band") */
+double lfo_std_of_intensity(const uint16_t *I, size_t N)
+{
+    __int128 S1 = 0;
+    unsigned __int128 S2 = 0;
+    for (size_t i = 0; i < N; ++i) {
+        S1 += I[i];
+        S2 += (unsigned __int128)I[i] * I[i];
+    }
+    return lfo_global_std((int64_t)N, S1, S2);
+}
+
+/* R21: adaptive ZC gap threshold in response units, t = ceil(k * sigma_r) */
+int64_t lfo_adaptive_zc_threshold(double k, double sigma_r) { return (int64_t)ceil(k * sigma_r); }
+
 typedef struct lfo_params {
     int32_t bit_depth;
     int32_t sigma_is_variance;
@@ -323,6 +373,9 @@ typedef struct lfo_params {
     int32_t median_window;
     int32_t out_mode;     /* 0 = extract intensities, 1 = 0/255 mask */
     int32_t median_window2; /* 0 or a second hybrid-median level (R17) */
+    int32_t adaptive;     /* bit 0: zc_threshold[j] = k_j, t_j = ceil(k_j sigma_r_j) (R21);
+                             bit 1: std thresholds = k_j * sigma_I (R22) */
+    int32_t pad_;
 } lfo_params;
 
 /* Optional intermediates (any may be NULL): r0/r1 int64[W*H], z0/z1, k0/k1
@@ -354,7 +407,8 @@ int lfo_run(const lfo_params *p, const uint16_t *I, int W, int H, uint16_t *out,
         double s = p->sigma_is_variance ? sqrt(p->sigma[j]) : p->sigma[j];
         if (lfo_mask_int(s, n, p->bit_depth, q, &F) != 0) { rc = -1; break; }
         lfo_log_response(I, W, H, q, n, r);
-        int64_t t = lfo_zc_threshold_int(p->zc_threshold[j], F, p->bit_depth);
+        int64_t t = (p->adaptive & 1) ? lfo_adaptive_zc_threshold(p->zc_threshold[j], lfo_std_of_response(r, N))
+                                      : lfo_zc_threshold_int(p->zc_threshold[j], F, p->bit_depth);
         lfo_zero_crossing(r, W, H, t, Z);
         if (j == 0 && r0o) memcpy(r0o, r, N * sizeof(int64_t));
         if (j == 1 && r1o) memcpy(r1o, r, N * sizeof(int64_t));
@@ -365,7 +419,13 @@ int lfo_run(const lfo_params *p, const uint16_t *I, int W, int H, uint16_t *out,
             for (size_t i = 0; i < N; ++i) src[i] = Z[i];
             s_img = src;
         }
-        lfo_std_gate(s_img, Z, W, H, p->std_window, p->std_threshold[j], p->std3_threshold[j], K[j]);
+        double T = p->std_threshold[j], T3 = p->std3_threshold[j];
+        if (p->adaptive & 2) {  /* R22: multiples of the global intensity sigma */
+            double sI = lfo_std_of_intensity(I, N);
+            T = T * sI;
+            if (T3 >= 0.0) T3 = T3 * sI;
+        }
+        lfo_std_gate(s_img, Z, W, H, p->std_window, T, T3, K[j]);
     }
     if (rc == 0) {
         if (k0o) memcpy(k0o, K[0], N);

@@ -504,3 +504,88 @@ def test_pipeline_rejects_out_of_range_pixels():
     I = np.full((4, 4), 300, np.uint16)
     with pytest.raises(ValueError):
         O.run(I, O.Params(bit_depth=8))
+
+
+# ------------------------------------------- adaptive thresholds (NEXT-2) ----
+def test_global_std_is_the_exact_formula():
+    """R21: sigma = sqrt(n*S2 - S1^2) / n with the integer numerator exact and
+    rounded once.  Python ints are exact and float(int) / math.sqrt round
+    correctly, so the oracle must agree bit for bit -- including numerators
+    far beyond 2^64 (the 128-bit path)."""
+    rng = np.random.default_rng(21)
+    cases = [(1, 5, 25), (4, 2, 2), (3, 6, 14), (2, 0, 2 * (2**24 - 1) ** 2)]
+    for _ in range(300):
+        n = int(rng.integers(1, 2**31))
+        v = int(rng.integers(0, 2**24))
+        s1 = int(rng.integers(-n, n)) * v // 7
+        s2 = n * v * v  # >= s1^2 / n
+        cases.append((n, s1, s2))
+    for n, s1, s2 in cases:
+        want = math.sqrt(float(n * s2 - s1 * s1)) / float(n)
+        assert O.global_std(n, s1, s2) == want, (n, s1, s2)
+
+
+def test_std_of_response_and_intensity_match_numpy():
+    rng = np.random.default_rng(22)
+    r = rng.integers(-(2**24) + 1, 2**24, (37, 53)).astype(np.int64)
+    assert math.isclose(O.std_of_response(r), float(np.std(r.astype(np.float64))), rel_tol=1e-12)
+    I = rng.integers(0, 65536, (29, 31)).astype(np.uint16)
+    assert math.isclose(O.std_of_intensity(I), float(np.std(I.astype(np.float64))), rel_tol=1e-12)
+    # closed form: half a, half b -> sigma = |a - b| / 2 exactly; constant -> 0
+    two = np.array([[100, 900] * 8] * 3, np.uint16)
+    assert O.std_of_intensity(two) == 400.0
+    assert O.std_of_intensity(np.full((5, 5), 77, np.uint16)) == 0.0
+    assert O.std_of_response(np.zeros((4, 4), np.int64)) == 0.0
+
+
+def _thr_for(t, F, b):
+    """A normalised absolute ZC threshold whose integer threshold is exactly t."""
+    return (t - 0.5) / (2.0**F * ((1 << b) - 1)) if t > 0 else 0.0
+
+
+@pytest.mark.parametrize("b,k", [(8, 0.75), (10, 0.3), (12, 1.0), (8, 0.05)])
+def test_adaptive_zc_threshold_equals_absolute_with_that_t(b, k):
+    """t_j = ceil(k * global std of r_j).  The expected t comes from
+    scipy's correlate and numpy's std; the adaptive pipeline must then equal the
+    absolute-threshold pipeline at that integer t."""
+    rng = np.random.default_rng(23 + b)
+    I = scenes.random_image(rng, 41, 47, b)
+    ts, thr = [], []
+    for j, s in enumerate((0.5, 20.0)):
+        q, F = O.mask_int(s, 5, b)
+        r = ndi.correlate(I.astype(np.int64), q.astype(np.int64), mode="nearest")
+        x = k * float(np.std(r.astype(np.float64)))
+        assert abs(x - round(x)) > 1e-6  # not on a rounding boundary
+        ts.append(math.ceil(x))
+        thr.append(_thr_for(ts[-1], F, b))
+        assert O.adaptive_zc_threshold(k, O.std_of_response(r)) == ts[-1]
+    pa = O.Params(bit_depth=b, zc_threshold=(k, k), adaptive=1, out_mode=1)
+    pb = O.Params(bit_depth=b, zc_threshold=tuple(thr), out_mode=1)
+    np.testing.assert_array_equal(O.run(I, pa), O.run(I, pb))
+
+
+def test_adaptive_std_threshold_equals_absolute_with_that_T():
+    """std thresholds = k * global intensity std (INTENSITY source)."""
+    rng = np.random.default_rng(24)
+    I = scenes.random_image(rng, 45, 39, 10)
+    v = I.astype(np.int64).ravel()
+    sI = O.global_std(v.size, int(v.sum()), int((v * v).sum()))
+    k, k3 = (0.8, 1.3), (1.5, -1.0)
+    pa = O.Params(bit_depth=10, std_source=1, std_threshold=k, std3_threshold=k3, adaptive=2, out_mode=1)
+    pb = O.Params(bit_depth=10, std_source=1, std_threshold=(k[0] * sI, k[1] * sI),
+                  std3_threshold=(k3[0] * sI, -1.0), out_mode=1)
+    np.testing.assert_array_equal(O.run(I, pa), O.run(I, pb))
+
+
+def test_adaptive_constant_image_and_invariances():
+    """Constant image: sigma = 0 -> t = 0, still empty.  The global stds are
+    invariant under the dihedral maps and I -> M - I, so the covariance pins of
+    the absolute pipeline carry over."""
+    assert not O.run(np.full((20, 20), 9, np.uint8), O.Params(bit_depth=8, adaptive=1, zc_threshold=(0.7, 0.7))).any()
+    rng = np.random.default_rng(25)
+    I = scenes.random_image(rng, 33, 28, 8)
+    p = O.Params(bit_depth=8, adaptive=1, zc_threshold=(0.6, 0.9), out_mode=1)
+    out = O.run(I, p)
+    for T in _DIHEDRAL:
+        np.testing.assert_array_equal(O.run(np.ascontiguousarray(T(I)), p), T(out))
+    np.testing.assert_array_equal(O.run((255 - I.astype(np.int64)).astype(np.uint8), p), out)

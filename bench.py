@@ -43,17 +43,22 @@ def parse():
     ap.add_argument("--tile", type=str, default="", help="TWxTH override (tuning only)")
     ap.add_argument("--median2", type=int, default=0, choices=[0, 3, 5, 7],
                     help="second hybrid-median level (the water pipeline, PAPER.md:102); 0 = the c3 metric config")
+    ap.add_argument("--adaptive", type=float, default=0.0,
+                    help="k > 0: adaptive ZC gap t = ceil(k * sigma(r)) (SPEC.md:233, NEXT-2), with its "
+                         "statistics pre-pass and all-reduce inside every step; 0 = the c3 metric config")
     return ap.parse_args()
 
 
-def workload_params(median2=0):
+def workload_params(median2=0, adaptive=0.0):
     from paper_1304_3992_b200 import lfe
     # SURVEY.md 8(c) defaults for benchmark scenes: ZC gap 0.02 (normalised),
     # std source = ZC image, 5x5 window, T = 0.3, hybrid median on, extract.
-    return lfe.Params(bit_depth=10, sigma=(0.5, 20.0), log_size=(5, 5), zc_threshold=(0.02, 0.02),
+    zc = (adaptive, adaptive) if adaptive > 0 else (0.02, 0.02)
+    return lfe.Params(bit_depth=10, sigma=(0.5, 20.0), log_size=(5, 5), zc_threshold=zc,
                       std_source=lfe.LFE_STD_ZC, std_window=5, std_threshold=(0.3, 0.3),
                       std3_threshold=(-1.0, -1.0), hybrid_median=True, median_window=5,
-                      out_mode=lfe.LFE_OUT_EXTRACT, median_window2=median2)
+                      out_mode=lfe.LFE_OUT_EXTRACT, median_window2=median2,
+                      adaptive=lfe.LFE_ADAPT_ZC if adaptive > 0 else 0)
 
 
 def oracle_params(p):
@@ -61,7 +66,8 @@ def oracle_params(p):
     return oracle.Params(bit_depth=p.bit_depth, sigma=p.sigma, log_size=p.log_size, zc_threshold=p.zc_threshold,
                          std_source=p.std_source, std_window=p.std_window, std_threshold=p.std_threshold,
                          std3_threshold=p.std3_threshold, hybrid_median=p.hybrid_median,
-                         median_window=p.median_window, out_mode=p.out_mode, median_window2=p.median_window2)
+                         median_window=p.median_window, out_mode=p.out_mode, median_window2=p.median_window2,
+                         adaptive=p.adaptive)
 
 
 def halo_rows(p):
@@ -74,16 +80,18 @@ def halo_rows(p):
 
 def config_dict(size, world, p):
     hm = "5x5 hybrid median" + (f" + {p.median_window2}x{p.median_window2} second level" if p.median_window2 else "")
+    zc = (f"ZC (adaptive gap {p.zc_threshold[0]} x global std of r, statistics pre-pass)" if p.adaptive
+          else "ZC (gap 0.02)")
     return {
         "workload": f"c3: {size}x{size} uint16 (10-bit) synthetic Cartosat-1-like PAN scene, "
-                    f"dual LoG (sigma 0.5, 20; 5x5) + ZC (gap 0.02) + 5x5 std gate (T=0.3) + OR + {hm}, extract",
+                    f"dual LoG (sigma 0.5, 20; 5x5) + {zc} + 5x5 std gate (T=0.3) + OR + {hm}, extract",
         "width": size, "height": size, "bit_depth": 10, "bands": 1,
         "parallelism": f"row strips x{world}, {halo_rows(p)}-row NCCL halo exchange" if world > 1 else "single GPU",
         "l2": "inputs larger than L2 (288 MB in + 288 MB out per step > 126 MB L2); no flush",
         "params": {"sigma": list(p.sigma), "log_size": list(p.log_size), "zc_threshold": list(p.zc_threshold),
                    "std_source": "zc", "std_window": p.std_window, "std_threshold": list(p.std_threshold),
                    "hybrid_median": bool(p.hybrid_median), "median_window": p.median_window,
-                   "median_window2": p.median_window2, "out_mode": "extract"},
+                   "median_window2": p.median_window2, "adaptive": p.adaptive, "out_mode": "extract"},
     }
 
 
@@ -197,7 +205,7 @@ def run_reference(args, world, rank):
 
     import oracle
     from paper_1304_3992_b200 import scenes
-    p = workload_params(args.median2)
+    p = workload_params(args.median2, args.adaptive)
     img = scenes.scene_c3(size=args.size)
     rows = 512
     H, W = img.shape
@@ -242,7 +250,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    p = workload_params(args.median2)
+    p = workload_params(args.median2, args.adaptive)
     size = args.size
     img = scenes.scene_c3(size=size)                      # host, numpy uint16
     H, W = img.shape
@@ -275,9 +283,19 @@ def main():
             kernel_events.append((e0, e1, n))
 
     bands = shard.bands()
+    stats = torch.zeros(9, dtype=torch.int64, device=dev) if p.adaptive else None
 
     def step(record=False):
         works = shard.exchange() if world > 1 else []
+        if p.adaptive:  # NEXT-2: whole-scene statistics first (needs the halo rows), one sync
+            for w in works:
+                w.wait()
+            works = []
+            stats.zero_()
+            lfe.lfe_stats_rows(ctx.handle, buf.data_ptr() + shard.ha * bpitch, bpitch, W, shard.rows, shard.ha,
+                               shard.hb, shard.edge_flags(), stats.data_ptr(), sptr)
+            shard.allreduce_stats(stats)
+            ctx.set_stats(stats.cpu().tolist())
         for b in bands:
             if b[5]:
                 continue

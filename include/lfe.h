@@ -11,7 +11,8 @@
  *   hybrid median ................ :76  (Sec. 3.4)
  *   urban pipeline / padding ..... :94  (Sec. 4.1, Fig. 1)
  *   water pipeline (median) ...... :102 (Sec. 4.2, Fig. 2)
- * Readings of silent or ambiguous points are R1..R20 in DESIGN.md.
+ *   adaptive thresholds .......... SPEC.md:233, :235 (NEXT-2)
+ * Readings of silent or ambiguous points are R1..R22 in DESIGN.md.
  *
  * Conventions for every call:
  *   - No C++ exception crosses this ABI; every call returns an lfe_status.
@@ -61,6 +62,8 @@ enum { LFE_TOP_IS_EDGE = 1u, LFE_BOTTOM_IS_EDGE = 2u };
 enum { LFE_OPT_KERNEL = 1, LFE_OPT_TILE_W = 2, LFE_OPT_TILE_H = 3, LFE_OPT_HOST_STRIP_ROWS = 4 };
 /* LFE_OPT_KERNEL values. */
 enum { LFE_KERNEL_AUTO = 0, LFE_KERNEL_STAGED = 1, LFE_KERNEL_FUSED = 2 };
+/* lfe_params.adaptive flags (NEXT-2, readings R21/R22). */
+enum { LFE_ADAPT_ZC = 1u, LFE_ADAPT_STD = 2u };
 
 /* The problem as the paper states it.  Index 0/1 = the two
  * LoG branches (neutral labels, reading R18).  112 bytes, natural alignment. */
@@ -70,7 +73,12 @@ typedef struct lfe_params {
     double sigma[2];            /* Eq. 1 sigma (> 0, finite)                              */
     int32_t sigma_is_variance;  /* 0: sigma used directly (R1); 1: sigma = sqrt(value)    */
     int32_t log_size[2];        /* odd mask side: 3, 5 or 7 (paper: 5)       */
-    int32_t reserved0;          /* must be 0                                             */
+    int32_t adaptive;           /* 0, or LFE_ADAPT_* flags (see lfe_stats below):         */
+                                /*  ZC:  zc_threshold[j] is k_j and the gap threshold is  */
+                                /*       t_j = ceil(k_j * sigma(r_j)) (R21)               */
+                                /*  STD: std_threshold[j] / std3_threshold[j] (if >= 0)   */
+                                /*       are multiples of sigma(I); needs the INTENSITY   */
+                                /*       std source (R22)                                 */
     double zc_threshold[2];     /* >= 0; gap threshold normalised by 2^F * (2^b - 1) (R9) */
     int32_t std_source;         /* LFE_STD_ZC (default, R10) or LFE_STD_INTENSITY         */
     int32_t std_window;         /* odd 3, 5 or 7 (paper: 5)                               */
@@ -100,6 +108,9 @@ void lfe_params_default(lfe_params *p);
 lfe_status lfe_create(const lfe_params *p, lfe_ctx **out);
 
 /* Whole-image extraction on the device (the Fig. 1 / Fig. 2 pipeline).
+ * With adaptive thresholds it first runs the statistics pass over the image,
+ * synchronises cuda_stream once to resolve the thresholds on the host (as
+ * lfe_set_stats), then enqueues the extraction.
  * d_in/d_out: device pointers to W x H pitched images; pitches must be >= the
  * row bytes and multiples of the element size; in and out must not overlap.
  * 16-byte aligned bases and pitches select the fast fused kernel; anything
@@ -111,7 +122,8 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out);
 lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
                        int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
 
-/* One row strip of a larger image (multi-GPU sharding, streaming).  d_in_row0
+/* One row strip of a larger image (multi-GPU sharding, streaming).  An
+ * adaptive ctx needs whole-image statistics first (lfe_set_stats).  d_in_row0
  * points at the first OWNED row; `halo_above` rows above it and `halo_below`
  * rows below the last owned row are readable.  If a side's edge flag is set,
  * its outermost readable row (row -halo_above, resp. rows-1+halo_below) is the
@@ -127,12 +139,48 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_
 /* End-to-end call on HOST buffers (the paper's H2D -> kernel -> D2H flow,
  * PAPER.md:150, Table 6): copies the image in row strips to device staging
  * buffers owned by the ctx, runs lfe_extract_rows per strip and copies the
- * result back, overlapping the three on separate streams.  Synchronous:
+ * result back, overlapping the three on separate streams (an adaptive ctx first
+ * streams the image once for lfe_stats_rows).  Synchronous:
  * returns when h_out is complete.  Pinned (page-locked) host buffers give
  * full PCIe bandwidth; pageable ones work but are slower.  Errors: EINVAL,
  * ENOMEM, ECUDA, ERANGE (checked at the end of the call). */
 lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch_bytes, int32_t width,
                             int32_t height, void *h_out, int64_t out_pitch_bytes);
+
+/* Exact global statistics of an image for the adaptive thresholds (NEXT-2):
+ * integer sums, additive over disjoint row ranges -- strips or ranks may be
+ * combined by summing every field (e.g. an int64 all-reduce).  r_j is branch
+ * j's integer LoG response (R3) with replicate padding at the true image edges
+ * (R5); r_j^2 is split so no 64-bit sum overflows:
+ * sum r_j^2 = r_sq_hi[j] * 2^24 + r_sq_lo[j].  72 bytes. */
+typedef struct lfe_stats {
+    int64_t n;           /* pixels                            */
+    int64_t r_sum[2];    /* sum r_j                           */
+    int64_t r_sq_hi[2];  /* sum (r_j^2 >> 24)                 */
+    int64_t r_sq_lo[2];  /* sum (r_j^2 & (2^24 - 1))          */
+    int64_t i_sum;       /* sum I                             */
+    int64_t i_sq;        /* sum I^2                           */
+} lfe_stats;
+
+/* Adds the statistics of the OWNED rows of a strip to *d_stats (DEVICE memory,
+ * 8-byte aligned, zeroed by the caller before the first strip).  Strip and
+ * halo arguments as lfe_extract_rows (only the LoG radius of the halo is
+ * read).  Enqueued on cuda_stream.  Errors: EINVAL, ECUDA. */
+lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_bytes, int32_t width,
+                          int32_t rows, int32_t halo_above, int32_t halo_below, uint32_t edge_flags,
+                          lfe_stats *d_stats, void *cuda_stream);
+
+/* Resolves the adaptive thresholds of a ctx from whole-image statistics
+ * (HOST pointer): sigma = sqrt(n*S2 - S1^2) / n with the integer numerator
+ * exact, rounded once to double (R21).  Subsequent lfe_extract_rows /
+ * lfe_extract_host calls use them; lfe_extract computes its own.  NULL clears.
+ * Errors: EINVAL (n < 1, or the ctx is not adaptive). */
+lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h_stats);
+
+/* The thresholds in force: zc_t[j] in integer response units, std_T[j] and
+ * std3_T[j] in Eq. 2 units (< 0: re-check off).  Any pointer may be NULL.
+ * Errors: EINVAL (NULL ctx; adaptive ctx without statistics). */
+lfe_status lfe_get_thresholds(const lfe_ctx *c, int64_t *zc_t, double *std_T, double *std3_T);
 
 /* Rows of real input needed above/below a strip for a bit-exact result:
  * LoG radius + 1 (ZC) + std radius + median radius (0 if off) + second-level

@@ -1142,7 +1142,7 @@ bool fused_supports(const KParams &kp, int bit_depth)
     if (kp.hm && kp.m != 5) return false;
     if (kp.m2 && !(kp.hm && kp.m == 5 && kp.m2 == 3)) return false;
     for (int j = 0; j < 2; ++j) {
-        if (kp.zc_t[j] >= (1 << 24)) return false;
+        if (kp.zc_t[j] > (1 << 24)) return false;  // t <= 2^24: every gap test is exact in fp32
         int lo, hi;
         if (!interval_of(kp.pass_lut[j], 25, &lo, &hi)) return false;
     }

@@ -50,6 +50,12 @@ struct lfe_ctx {
     cudaEvent_t ev_h2d[kHostBuffers] = {}, ev_comp[kHostBuffers] = {}, ev_d2h[kHostBuffers] = {};
     void *d_in[kHostBuffers] = {}, *d_out[kHostBuffers] = {};
     size_t in_cap = 0, out_cap = 0;
+    // resolved thresholds (absolute at create; adaptive ones after lfe_set_stats)
+    bool have_thresholds = false;
+    int64_t zc_t[2] = {0, 0};
+    double std_T[2] = {0, 0}, std3_T[2] = {-1, -1};
+    // adaptive pre-pass (NEXT-2): device accumulator + pinned host copy
+    lfe_stats *d_stats = nullptr, *h_stats = nullptr;
 };
 
 namespace {
@@ -104,7 +110,9 @@ lfe_status validate(const lfe_params *p)
     if (!p) return fail(LFE_EINVAL, "params is NULL");
     if (p->abi_size != sizeof(lfe_params))
         return fail(LFE_EINVAL, "abi_size %u != sizeof(lfe_params) %zu", p->abi_size, sizeof(lfe_params));
-    if (p->reserved0) return fail(LFE_EINVAL, "reserved fields must be 0");
+    if (p->adaptive & ~(int32_t)(LFE_ADAPT_ZC | LFE_ADAPT_STD)) return fail(LFE_EINVAL, "unknown adaptive flag");
+    if ((p->adaptive & LFE_ADAPT_STD) && p->std_source != LFE_STD_INTENSITY)
+        return fail(LFE_EINVAL, "LFE_ADAPT_STD needs std_source = LFE_STD_INTENSITY (R22)");
     if (p->bit_depth < 1 || p->bit_depth > 16) return fail(LFE_EINVAL, "bit_depth %d not in 1..16", p->bit_depth);
     if (p->sigma_is_variance != 0 && p->sigma_is_variance != 1)
         return fail(LFE_EINVAL, "sigma_is_variance must be 0 or 1");
@@ -157,6 +165,40 @@ lfe_status check_device(int *dev)
 
 size_t elem_in(const lfe_ctx *c) { return c->p.bit_depth <= 8 ? 1 : 2; }
 size_t elem_out(const lfe_ctx *c) { return c->p.out_mode == LFE_OUT_MASK ? 1 : elem_in(c); }
+
+// Population standard deviation from exact integer sums (reading R21):
+// sqrt(n*S2 - S1^2) / n, the integer numerator exact, rounded once to double.
+double global_std(int64_t n, __int128 S1, unsigned __int128 S2)
+{
+    const __int128 D = (__int128)n * (__int128)S2 - S1 * S1;
+    return std::sqrt((double)D) / (double)n;
+}
+
+// Installs resolved thresholds into the kernel parameters: ZC gap t (integer
+// units, R9/R21) and the Eq. 2 thresholds T, T3 (R11, R12, R22).
+void apply_thresholds(lfe_ctx *c, const int64_t zt[2], const double T[2], const double T3[2])
+{
+    KParams &kp = c->kp;
+    const int L = c->p.std_window * c->p.std_window;
+    for (int j = 0; j < 2; ++j) {
+        // a gap never exceeds 2^25, so any t above it acts alike
+        kp.zc_t[j] = zt[j] > (int64_t(1) << 26) ? (1 << 26) : (int32_t)zt[j];
+        // std gate (R11): s > T  <=>  L*S2 - S1^2 > L*(L-1)*T*T, compared in double
+        kp.rhs[j] = (double)(L * (L - 1)) * T[j] * T[j];
+        kp.pass_lut[j] = 0;
+        for (int k = 0; k <= L; ++k)
+            if ((double)((int64_t)L * k - (int64_t)k * k) > kp.rhs[j]) kp.pass_lut[j] |= 1ull << k;
+        kp.recheck[j] = T3[j] >= 0.0;
+        kp.rhs3[j] = (double)(9 * 8) * T3[j] * T3[j];
+        kp.pass3_lut[j] = 0;
+        for (int k = 0; k <= 9; ++k)
+            if ((double)(9 * k - k * k) > kp.rhs3[j]) kp.pass3_lut[j] |= 1u << k;
+        c->zc_t[j] = zt[j];
+        c->std_T[j] = T[j];
+        c->std3_T[j] = T3[j];
+    }
+    c->have_thresholds = true;
+}
 
 bool overlap(const void *a, size_t na, const void *b, size_t nb)
 {
@@ -269,22 +311,6 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
         }
         kp.n[j] = n;
         kp.RL = n / 2 > kp.RL ? n / 2 : kp.RL;
-        // gap threshold in integer units, t = ceil(thr * 2^F * M) (R9); a gap never exceeds 2^25
-        const double t = std::ceil(p->zc_threshold[j] * std::ldexp(1.0, c->F[j]) * (double)maxv);
-        kp.zc_t[j] = t > (double)(1 << 26) ? (1 << 26) : (int32_t)t;
-        // std gate (R11): s > T  <=>  L*S2 - S1^2 > L*(L-1)*T*T, compared in double
-        const int L = p->std_window * p->std_window;
-        const double T = p->std_threshold[j];
-        kp.rhs[j] = (double)(L * (L - 1)) * T * T;
-        kp.pass_lut[j] = 0;
-        for (int k = 0; k <= L; ++k)
-            if ((double)((int64_t)L * k - (int64_t)k * k) > kp.rhs[j]) kp.pass_lut[j] |= 1ull << k;
-        const double T3 = p->std3_threshold[j];
-        kp.recheck[j] = T3 >= 0.0;
-        kp.rhs3[j] = (double)(9 * 8) * T3 * T3;
-        kp.pass3_lut[j] = 0;
-        for (int k = 0; k <= 9; ++k)
-            if ((double)(9 * k - k * k) > kp.rhs3[j]) kp.pass3_lut[j] |= 1u << k;
         if (n == 5) {
             const int32_t *q = kp.q[j];
             // orbits (0,0) (1,0) (2,0) (1,1) (2,1) (2,2) at row-major index (2+y)*5+(2+x)
@@ -306,6 +332,13 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
     kp.Rm2 = kp.m2 / 2;
     kp.out_mode = p->out_mode;
     kp.halo = kp.RL + 1 + kp.Rs + kp.Rm + kp.Rm2;
+    kp.adaptive = p->adaptive;
+    if (!p->adaptive) {
+        int64_t zt[2];
+        for (int j = 0; j < 2; ++j)  // gap threshold in integer units, t = ceil(thr * 2^F * M) (R9)
+            zt[j] = (int64_t)std::ceil(p->zc_threshold[j] * std::ldexp(1.0, c->F[j]) * (double)maxv);
+        apply_thresholds(c, zt, p->std_threshold, p->std3_threshold);
+    }
 
     // d_err[0]: sticky ERANGE flag; d_err[1]: the fused kernel's work-queue counter
     if (cudaMalloc(&c->d_err, 2 * sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, 2 * sizeof(int)) != cudaSuccess) {
@@ -358,6 +391,105 @@ lfe_status lfe_set_option(lfe_ctx *c, int32_t key, int64_t value)
     return fail(LFE_EINVAL, "unknown option %d", key);
 }
 
+lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (!c->p.adaptive) return fail(LFE_EINVAL, "ctx has no adaptive thresholds");
+    if (!h) {
+        c->have_thresholds = false;
+        return LFE_OK;
+    }
+    if (h->n < 1) return fail(LFE_EINVAL, "statistics of %lld pixels", (long long)h->n);
+    const lfe_params &p = c->p;
+    int64_t zt[2];
+    double T[2], T3[2];
+    const unsigned __int128 Si2 = (unsigned __int128)(uint64_t)h->i_sq;
+    const double sI = global_std(h->n, (__int128)h->i_sum, Si2);
+    for (int j = 0; j < 2; ++j) {
+        if (p.adaptive & LFE_ADAPT_ZC) {  // R21: t_j = ceil(k_j * sigma(r_j))
+            const unsigned __int128 S2 =
+                ((unsigned __int128)(uint64_t)h->r_sq_hi[j] << 24) + (unsigned __int128)(uint64_t)h->r_sq_lo[j];
+            zt[j] = (int64_t)std::ceil(p.zc_threshold[j] * global_std(h->n, (__int128)h->r_sum[j], S2));
+        } else {
+            const double M = (double)((int64_t(1) << p.bit_depth) - 1);
+            zt[j] = (int64_t)std::ceil(p.zc_threshold[j] * std::ldexp(1.0, c->F[j]) * M);
+        }
+        if (p.adaptive & LFE_ADAPT_STD) {  // R22: multiples of sigma(I)
+            T[j] = p.std_threshold[j] * sI;
+            T3[j] = p.std3_threshold[j] >= 0.0 ? p.std3_threshold[j] * sI : p.std3_threshold[j];
+        } else {
+            T[j] = p.std_threshold[j];
+            T3[j] = p.std3_threshold[j];
+        }
+    }
+    apply_thresholds(c, zt, T, T3);
+    return LFE_OK;
+}
+
+lfe_status lfe_get_thresholds(const lfe_ctx *c, int64_t *zc_t, double *std_T, double *std3_T)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx without statistics (lfe_set_stats)");
+    for (int j = 0; j < 2; ++j) {
+        if (zc_t) zc_t[j] = c->zc_t[j];
+        if (std_T) std_T[j] = c->std_T[j];
+        if (std3_T) std3_T[j] = c->std3_T[j];
+    }
+    return LFE_OK;
+}
+
+static lfe_status strip_geometry(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
+                                 int32_t halo_above, int32_t halo_below, uint32_t edge_flags, int h, Geometry *g)
+{
+    if (edge_flags & ~3u) return fail(LFE_EINVAL, "unknown edge flag");
+    const bool top = edge_flags & LFE_TOP_IS_EDGE, bot = edge_flags & LFE_BOTTOM_IS_EDGE;
+    if (halo_above < 0 || halo_below < 0) return fail(LFE_EINVAL, "negative halo");
+    if (!top && halo_above < h) return fail(LFE_EINVAL, "halo_above %d < required %d", halo_above, h);
+    if (!bot && halo_below < h) return fail(LFE_EINVAL, "halo_below %d < required %d", halo_below, h);
+    // an edge side clamps at its outermost readable row; an inner side reads exactly h rows
+    const int ha = top ? halo_above : h, hb = bot ? halo_below : h;
+    const char *vin = reinterpret_cast<const char *>(d_in_row0) - (int64_t)ha * in_pitch;
+    *g = Geometry{vin, in_pitch, nullptr, 0, W, rows + ha + hb, ha, ha + rows};
+    (void)c;
+    return LFE_OK;
+}
+
+lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
+                          int32_t halo_above, int32_t halo_below, uint32_t edge_flags, lfe_stats *d_stats,
+                          void *stream)
+{
+    if (!d_stats || reinterpret_cast<uintptr_t>(d_stats) % 8) return fail(LFE_EINVAL, "d_stats NULL or misaligned");
+    lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_stats, (int64_t)W * 2, rows);
+    if (st != LFE_OK) return st;
+    Geometry g;
+    st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, c->kp.RL, &g);
+    if (st != LFE_OK) return st;
+    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
+    ++c->launches;
+    return LFE_OK;
+}
+
+static lfe_status stats_buffers(lfe_ctx *c)
+{
+    if (c->d_stats) return LFE_OK;
+    if (cudaMalloc(&c->d_stats, sizeof(lfe_stats)) != cudaSuccess ||
+        cudaMallocHost(&c->h_stats, sizeof(lfe_stats)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LFE_ENOMEM, "statistics buffers");
+    }
+    return LFE_OK;
+}
+
+// whole-image statistics -> thresholds (one stream synchronisation)
+static lfe_status resolve_from_device(lfe_ctx *c, cudaStream_t s)
+{
+    if (cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(lfe_stats), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(LFE_ECUDA, "statistics: %s", cudaGetErrorString(cudaGetLastError()));
+    return lfe_set_stats(c, c->h_stats);
+}
+
 lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
                        int64_t out_pitch, void *stream)
 {
@@ -366,6 +498,18 @@ lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W
     if (overlap(d_in, (size_t)(H - 1) * in_pitch + W * elem_in(c), d_out, (size_t)(H - 1) * out_pitch + W * elem_out(c)))
         return fail(LFE_EINVAL, "input and output overlap");
     Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H};
+    if (c->p.adaptive) {  // NEXT-2: statistics pre-pass over the whole image
+        st = stats_buffers(c);
+        if (st != LFE_OK) return st;
+        cudaStream_t s = (cudaStream_t)stream;
+        if (cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), s) != cudaSuccess)
+            return fail(LFE_ECUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
+        cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, s);
+        if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
+        ++c->launches;
+        st = resolve_from_device(c, s);
+        if (st != LFE_OK) return st;
+    }
     return run(c, g, (cudaStream_t)stream);
 }
 
@@ -375,19 +519,15 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch,
 {
     lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_out_row0, out_pitch, rows);
     if (st != LFE_OK) return st;
-    if (edge_flags & ~3u) return fail(LFE_EINVAL, "unknown edge flag");
-    const int h = c->kp.halo;
-    const bool top = edge_flags & LFE_TOP_IS_EDGE, bot = edge_flags & LFE_BOTTOM_IS_EDGE;
-    if (halo_above < 0 || halo_below < 0) return fail(LFE_EINVAL, "negative halo");
-    if (!top && halo_above < h) return fail(LFE_EINVAL, "halo_above %d < required %d", halo_above, h);
-    if (!bot && halo_below < h) return fail(LFE_EINVAL, "halo_below %d < required %d", halo_below, h);
-    // an edge side clamps at its outermost readable row; an inner side reads exactly h rows
-    const int ha = top ? halo_above : h, hb = bot ? halo_below : h;
-    const char *vin = reinterpret_cast<const char *>(d_in_row0) - (int64_t)ha * in_pitch;
-    if (overlap(vin, (size_t)(rows + ha + hb - 1) * in_pitch + W * elem_in(c), d_out_row0,
+    if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
+    Geometry g;
+    st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, c->kp.halo, &g);
+    if (st != LFE_OK) return st;
+    if (overlap(g.in, (size_t)(g.Hv - 1) * in_pitch + W * elem_in(c), d_out_row0,
                 (size_t)(rows - 1) * out_pitch + W * elem_out(c)))
         return fail(LFE_EINVAL, "input and output overlap");
-    Geometry g{vin, in_pitch, d_out_row0, out_pitch, W, rows + ha + hb, ha, ha + rows};
+    g.out = d_out_row0;
+    g.out_pitch = out_pitch;
     return run(c, g, (cudaStream_t)stream);
 }
 
@@ -449,6 +589,29 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
     if (st != LFE_OK) return st;
     cudaStream_t sh = c->st[0], sc = c->st[1], sd = c->st[2];
     const int nstrips = (H + S - 1) / S;
+    if (c->p.adaptive) {  // NEXT-2: stream the image once for the whole-image statistics
+        st = stats_buffers(c);
+        if (st != LFE_OK) return st;
+        cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), sc);
+        for (int i = 0; i < nstrips; ++i) {
+            const int b = i % kHostBuffers;
+            const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
+            const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
+            if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);
+            cudaError_t e = cudaMemcpy2DAsync(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
+                                              in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
+            if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
+            cudaEventRecord(c->ev_h2d[b], sh);
+            cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
+            const uint32_t flags = (lo == 0 ? LFE_TOP_IS_EDGE : 0u) | (hi == H ? LFE_BOTTOM_IS_EDGE : 0u);
+            const char *row0 = reinterpret_cast<const char *>(c->d_in[b]) + (size_t)(a0 - lo) * dpi;
+            st = lfe_stats_rows(c, row0, (int64_t)dpi, W, a1 - a0, a0 - lo, hi - a1, flags, c->d_stats, sc);
+            if (st != LFE_OK) return st;
+            cudaEventRecord(c->ev_comp[b], sc);
+        }
+        st = resolve_from_device(c, sc);
+        if (st != LFE_OK) return st;
+    }
     for (int i = 0; i < nstrips; ++i) {
         const int b = i % kHostBuffers;
         const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
@@ -505,6 +668,8 @@ void lfe_destroy(lfe_ctx *c)
         cudaFree(c->d_out[b]);
     }
     cudaFree(c->d_err);
+    cudaFree(c->d_stats);
+    cudaFreeHost(c->h_stats);
     delete c;
 }
 

@@ -38,6 +38,7 @@ struct KParams {
     int32_t halo;                  // RL + 1 + Rs + Rm + Rm2
     // orbit coefficients of 5x5 masks for the fused kernel: (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
     int32_t orb[2][6];
+    int32_t adaptive;              // LFE_ADAPT_* (thresholds resolved on the host before launch)
 };
 
 // A virtual image: rows [0, Hv) of `width` pixels, clamped (edge-replicated)
@@ -65,5 +66,7 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
                          int *err_flag, cudaStream_t s);
 bool fused_supports(const KParams &kp, int bit_depth);
+// adds the exact global sums of output rows [o0, o1) to *d_stats (NEXT-2)
+cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, cudaStream_t s);
 
 }  // namespace lfe

@@ -25,6 +25,7 @@ LFE_OUT_EXTRACT, LFE_OUT_MASK = 0, 1
 LFE_TOP_IS_EDGE, LFE_BOTTOM_IS_EDGE = 1, 2
 LFE_OPT_KERNEL, LFE_OPT_TILE_W, LFE_OPT_TILE_H, LFE_OPT_HOST_STRIP_ROWS = 1, 2, 3, 4
 LFE_KERNEL_AUTO, LFE_KERNEL_STAGED, LFE_KERNEL_FUSED = 0, 1, 2
+LFE_ADAPT_ZC, LFE_ADAPT_STD = 1, 2
 
 _STATUS = {0: "LFE_OK", 1: "LFE_EINVAL", 2: "LFE_EUNSUPPORTED", 3: "LFE_ENOMEM",
            4: "LFE_ENODEV", 5: "LFE_ECUDA", 6: "LFE_ERANGE"}
@@ -43,7 +44,7 @@ class lfe_params(ctypes.Structure):
         ("sigma", ctypes.c_double * 2),
         ("sigma_is_variance", ctypes.c_int32),
         ("log_size", ctypes.c_int32 * 2),
-        ("reserved0", ctypes.c_int32),
+        ("adaptive", ctypes.c_int32),
         ("zc_threshold", ctypes.c_double * 2),
         ("std_source", ctypes.c_int32),
         ("std_window", ctypes.c_int32),
@@ -58,12 +59,28 @@ class lfe_params(ctypes.Structure):
 
 assert ctypes.sizeof(lfe_params) == 112
 
+
+class lfe_stats(ctypes.Structure):
+    """Exact global sums for the adaptive thresholds (include/lfe.h; additive)."""
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("r_sum", ctypes.c_int64 * 2),
+        ("r_sq_hi", ctypes.c_int64 * 2),
+        ("r_sq_lo", ctypes.c_int64 * 2),
+        ("i_sum", ctypes.c_int64),
+        ("i_sq", ctypes.c_int64),
+    ]
+
+
+assert ctypes.sizeof(lfe_stats) == 72
+
 _lib = None
 
 # every symbol include/lfe.h declares (the CPU test checks the .so exports them)
 EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows", "lfe_extract_host",
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
-           "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version"]
+           "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
+           "lfe_set_stats", "lfe_get_thresholds"]
 TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate"]  # include/lfe_test.h
 
 
@@ -105,6 +122,12 @@ def load():
     L.lfe_last_message.restype = ctypes.c_char_p
     L.lfe_abi_version.argtypes = []
     L.lfe_abi_version.restype = I32
+    L.lfe_stats_rows.argtypes = [P, P, I64, I32, I32, I32, I32, U32, P, P]
+    L.lfe_stats_rows.restype = st
+    L.lfe_set_stats.argtypes = [P, ctypes.POINTER(lfe_stats)]
+    L.lfe_set_stats.restype = st
+    L.lfe_get_thresholds.argtypes = [P, P, P, P]
+    L.lfe_get_thresholds.restype = st
     L.lfe_test_mask.argtypes = [ctypes.c_double, I32, I32, P, P]
     L.lfe_test_mask.restype = st
     L.lfe_test_validate.argtypes = [ctypes.POINTER(lfe_params)]
@@ -144,6 +167,25 @@ def lfe_extract_rows(ctx, d_in_row0: int, in_pitch: int, width: int, rows: int, 
 
 def lfe_extract_host(ctx, h_in: int, in_pitch: int, width: int, height: int, h_out: int, out_pitch: int):
     _check(load().lfe_extract_host(ctx, h_in, in_pitch, width, height, h_out, out_pitch), "lfe_extract_host")
+
+
+def lfe_stats_rows(ctx, d_in_row0: int, in_pitch: int, width: int, rows: int, halo_above: int,
+                   halo_below: int, edge_flags: int, d_stats: int, stream: int = 0):
+    _check(load().lfe_stats_rows(ctx, d_in_row0, in_pitch, width, rows, halo_above, halo_below, edge_flags,
+                                 d_stats, stream), "lfe_stats_rows")
+
+
+def lfe_set_stats(ctx, stats: lfe_stats | None):
+    _check(load().lfe_set_stats(ctx, ctypes.byref(stats) if stats is not None else None), "lfe_set_stats")
+
+
+def lfe_get_thresholds(ctx):
+    """(zc_t[2], std_T[2], std3_T[2]) in force."""
+    z = (ctypes.c_int64 * 2)()
+    t = (ctypes.c_double * 2)()
+    t3 = (ctypes.c_double * 2)()
+    _check(load().lfe_get_thresholds(ctx, z, t, t3), "lfe_get_thresholds")
+    return tuple(z), tuple(t), tuple(t3)
 
 
 def lfe_halo(ctx) -> int:
@@ -212,6 +254,7 @@ class Params:
     median_window: int = 5
     out_mode: int = LFE_OUT_EXTRACT
     median_window2: int = 0  # second hybrid-median level (water-body pipeline)
+    adaptive: int = 0        # LFE_ADAPT_* (readings R21, R22)
 
     def to_c(self) -> lfe_params:
         p = lfe_params()
@@ -229,6 +272,7 @@ class Params:
         p.median_window = self.median_window
         p.out_mode = self.out_mode
         p.median_window2 = self.median_window2
+        p.adaptive = self.adaptive
         return p
 
 
@@ -313,6 +357,39 @@ class Context:
         lfe_extract_rows(self.handle, pi + row0 * pin, pin, W, rows, halo_above, halo_below, edge_flags,
                          po + out_row0 * pout, pout, self._stream(stream))
         return t_out
+
+    def stats_rows(self, t_in_full, row0: int, rows: int, halo_above: int, halo_below: int,
+                   edge_flags: int, t_stats, stream=None):
+        """Adds the owned rows' exact sums to t_stats (a CUDA int64 tensor of 9)."""
+        import torch
+        pi, pin = self._torch_img(t_in_full, "input")
+        if t_stats.dtype != torch.int64 or t_stats.numel() != 9 or t_stats.device.type != "cuda":
+            raise TypeError("t_stats must be a CUDA int64 tensor of 9 elements")
+        W = t_in_full.shape[1]
+        lfe_stats_rows(self.handle, pi + row0 * pin, pin, W, rows, halo_above, halo_below, edge_flags,
+                       t_stats.data_ptr(), self._stream(stream))
+        return t_stats
+
+    @staticmethod
+    def stats_from(values) -> lfe_stats:
+        """lfe_stats from 9 int64 values in field order."""
+        v = [int(x) for x in values]
+        s = lfe_stats()
+        s.n = v[0]
+        s.r_sum[0], s.r_sum[1] = v[1], v[2]
+        s.r_sq_hi[0], s.r_sq_hi[1] = v[3], v[4]
+        s.r_sq_lo[0], s.r_sq_lo[1] = v[5], v[6]
+        s.i_sum, s.i_sq = v[7], v[8]
+        return s
+
+    def set_stats(self, stats):
+        """Whole-image statistics (an lfe_stats, or 9 int64 values) -> thresholds."""
+        if stats is not None and not isinstance(stats, lfe_stats):
+            stats = self.stats_from(stats)
+        lfe_set_stats(self.handle, stats)
+
+    def thresholds(self):
+        return lfe_get_thresholds(self.handle)
 
     def last_async_error(self, stream=None) -> int:
         return lfe_last_async_error(self.handle, self._stream(stream))

@@ -78,6 +78,15 @@ class StripShard:
             ops.append(dist.P2POp(dist.irecv, self.buf[e:e + self.hb], self.rank + 1, group))
         return dist.batch_isend_irecv(ops) if ops else []
 
+    def allreduce_stats(self, t_stats, group=None):
+        """Adaptive thresholds (NEXT-2): the 9 exact int64 sums of lfe_stats are
+        additive over disjoint row ranges, so one SUM all-reduce of every rank's
+        owned-row partial gives the whole-image statistics (bit-exact)."""
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t_stats, op=dist.ReduceOp.SUM, group=group)
+        return t_stats
+
     def edge_flags(self) -> int:
         from .lfe import LFE_BOTTOM_IS_EDGE, LFE_TOP_IS_EDGE
         return (LFE_TOP_IS_EDGE if self.rank == 0 else 0) | (LFE_BOTTOM_IS_EDGE if self.rank == self.world - 1 else 0)

@@ -91,7 +91,8 @@ def _with(**kw):
     (dict(median_window=6), lfe.LFE_EINVAL),
     (dict(median_window=11), lfe.LFE_EUNSUPPORTED),
     (dict(out_mode=3), lfe.LFE_EINVAL),
-    (dict(reserved0=1), lfe.LFE_EINVAL),
+    (dict(adaptive=4), lfe.LFE_EINVAL),
+    (dict(adaptive=2), lfe.LFE_EINVAL),  # LFE_ADAPT_STD needs the intensity source
     (dict(median_window2=4), lfe.LFE_EINVAL),
     (dict(median_window2=-3), lfe.LFE_EINVAL),
     (dict(median_window2=9), lfe.LFE_EUNSUPPORTED),

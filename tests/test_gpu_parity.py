@@ -29,7 +29,7 @@ def _oparams(p: lfe.Params) -> O.Params:
                     std_source=p.std_source, std_window=p.std_window,
                     std_threshold=tuple(p.std_threshold), std3_threshold=tuple(p.std3_threshold),
                     hybrid_median=p.hybrid_median, median_window=p.median_window, out_mode=p.out_mode,
-                    median_window2=p.median_window2)
+                    median_window2=p.median_window2, adaptive=p.adaptive)
 
 
 def _pitched(shape, dtype):
@@ -367,3 +367,140 @@ def test_fused_two_level_c3_sampled():
     p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), median_window2=3)
     got = run_gpu(img, p)
     _sampled_rows(img, p, got, [(0, 30), (7001, 7033), (11970, 12000)])
+
+
+# --------------------------------------------- adaptive thresholds (NEXT-2) ----
+def _oracle_global_thresholds(img, p: lfe.Params):
+    """Whole-image adaptive thresholds from the oracle alone (R21, R22)."""
+    zt, T = [], None
+    for j in range(2):
+        s = p.sigma[j] ** 0.5 if p.sigma_is_variance else p.sigma[j]
+        q, F = O.mask_int(s, p.log_size[j], p.bit_depth)
+        r = O.log_response(img, q)
+        zt.append((O.adaptive_zc_threshold(p.zc_threshold[j], O.std_of_response(r)), F))
+        del r
+    if p.adaptive & lfe.LFE_ADAPT_STD:
+        T = O.std_of_intensity(img)
+    return zt, T
+
+
+def _absolute_oparams(img, p: lfe.Params) -> O.Params:
+    """Oracle parameters with the adaptive thresholds replaced by the absolute
+    values they resolve to on the WHOLE image (for band-sampled parity)."""
+    zt, sI = _oracle_global_thresholds(img, p)
+    op = _oparams(p)
+    op.adaptive = 0
+    if p.adaptive & lfe.LFE_ADAPT_ZC:
+        M = (1 << p.bit_depth) - 1
+        op.zc_threshold = tuple((t - 0.5) / (2.0 ** F * M) if t > 0 else 0.0 for t, F in zt)
+    if p.adaptive & lfe.LFE_ADAPT_STD:
+        op.std_threshold = tuple(k * sI for k in p.std_threshold)
+        op.std3_threshold = tuple(k * sI if k >= 0 else k for k in p.std3_threshold)
+    return op
+
+
+def _adaptive_cases():
+    yield lfe.Params(bit_depth=8, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+    yield lfe.Params(bit_depth=10, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.3, 1.2), out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=12, adaptive=lfe.LFE_ADAPT_ZC | lfe.LFE_ADAPT_STD, zc_threshold=(0.5, 0.5),
+                     std_source=lfe.LFE_STD_INTENSITY, std_threshold=(1.0, 0.6), std3_threshold=(1.5, -1.0))
+    yield lfe.Params(bit_depth=8, adaptive=lfe.LFE_ADAPT_STD, std_source=lfe.LFE_STD_INTENSITY,
+                     std_threshold=(0.4, 0.9), median_window2=3, log_size=(3, 7))
+
+
+@pytest.mark.parametrize("ci", range(4))
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_adaptive_random_images(ci, kernel):
+    """SPEC.md:233/:235 adaptive thresholds: statistics pre-pass on the device,
+    thresholds resolved on the host, extraction -- bit-exact vs the oracle."""
+    p = list(_adaptive_cases())[ci]
+    rng = np.random.default_rng(400 + ci)
+    for (H, W), kind in itertools.product(SHAPES + [(129, 463)], ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, p.bit_depth, kind)
+        assert_same(run_gpu(img, p, kernel), O.run(img, _oparams(p)), f"{H}x{W} {kind}")
+
+
+def test_adaptive_thresholds_and_sums_equal_oracle():
+    img = scenes.scene_c1(clean=False)
+    p = lfe.Params(bit_depth=8, adaptive=lfe.LFE_ADAPT_ZC | lfe.LFE_ADAPT_STD, zc_threshold=(0.75, 0.4),
+                   std_source=lfe.LFE_STD_INTENSITY, std_threshold=(1.0, 1.0), std3_threshold=(1.5, -1.0))
+    zt, sI = _oracle_global_thresholds(img, p)
+    with lfe.Context(p) as ctx:
+        with pytest.raises(lfe.LfeError):  # no statistics yet
+            ctx.thresholds()
+        d = torch.from_numpy(img).cuda()
+        ctx.extract(d)
+        z, T, T3 = ctx.thresholds()
+        assert list(z) == [t for t, _ in zt]
+        assert T == (1.0 * sI, 1.0 * sI) and T3 == (1.5 * sI, -1.0)
+        # the raw sums of lfe_stats_rows against numpy integer sums of the oracle's r
+        st = torch.zeros(9, dtype=torch.int64, device="cuda")
+        ctx.stats_rows(d, 0, img.shape[0], 0, 0, lfe.LFE_TOP_IS_EDGE | lfe.LFE_BOTTOM_IS_EDGE, st)
+        v = [int(x) for x in st.cpu()]
+    I = img.astype(np.int64)
+    want = [I.size]
+    rs, rq = [], []
+    for j in range(2):
+        q, _ = O.mask_int(p.sigma[j], 5, 8)
+        r = O.log_response(img, q)
+        rs.append(int(r.sum()))
+        rq.append(sum(int(x) * int(x) for x in r.ravel().tolist()))
+    want += rs
+    assert v[:3] == want
+    assert [v[3] * 2**24 + v[5], v[4] * 2**24 + v[6]] == rq
+    assert v[7:] == [int(I.sum()), int((I * I).sum())]
+
+
+@pytest.mark.parametrize("cuts", [[0, 50, 200, 512], [0, 7, 300, 505, 512]])
+def test_adaptive_strips_with_summed_statistics(cuts):
+    """The multi-GPU recipe: per-strip lfe_stats_rows into one accumulator (what
+    an int64 all-reduce does across ranks), lfe_set_stats, then lfe_extract_rows
+    per strip == the oracle on the whole image."""
+    img = scenes.scene_c1(clean=False)
+    p = lfe.Params(bit_depth=8, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.6, 0.8), median_window2=3)
+    want = O.run(img, _oparams(p))
+    H = img.shape[0]
+    with lfe.Context(p) as ctx:
+        h = ctx.halo
+        d = torch.from_numpy(img).cuda()
+        with pytest.raises(lfe.LfeError):  # adaptive strips need statistics first
+            ctx.extract_rows(d, 0, 10, 0, h, lfe.LFE_TOP_IS_EDGE, torch.zeros_like(d))
+        parts = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            ha, hb = min(h, a), min(h, H - b)
+            flags = (lfe.LFE_TOP_IS_EDGE if a - ha == 0 else 0) | (lfe.LFE_BOTTOM_IS_EDGE if b + hb == H else 0)
+            st = torch.zeros(9, dtype=torch.int64, device="cuda")
+            ctx.stats_rows(d[a - ha:b + hb].clone(), ha, b - a, ha, hb, flags, st)
+            parts.append(st)
+        ctx.set_stats(torch.stack(parts).sum(0).cpu().tolist())
+        out = torch.zeros_like(d)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            ha, hb = min(h, a), min(h, H - b)
+            flags = (lfe.LFE_TOP_IS_EDGE if a - ha == 0 else 0) | (lfe.LFE_BOTTOM_IS_EDGE if b + hb == H else 0)
+            ctx.extract_rows(d[a - ha:b + hb].clone(), ha, b - a, ha, hb, flags, out, out_row0=a)
+        ctx.check()
+        assert_same(out.cpu().numpy(), want, "adaptive strips")
+
+
+def test_adaptive_extract_host():
+    img = scenes.scene_c3(size=700, height=900)
+    p = lfe.Params(bit_depth=10, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+    want = O.run(img, _oparams(p))
+    with lfe.Context(p) as ctx:
+        for strip in (64, 333):
+            ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, strip)
+            assert_same(ctx.extract_host(img), want, f"host strips {strip}")
+
+
+def test_adaptive_c3_full_size_sampled():
+    """c3 at full size with SPEC's adaptive default (t = 0.75 sigma(r)); the
+    whole-image thresholds come from the oracle's own 12000^2 pass."""
+    img = scenes.scene_c3()
+    p = lfe.Params(bit_depth=10, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+    got = run_gpu(img, p)
+    op = _absolute_oparams(img, p)
+    H = img.shape[0]
+    for a, b in [(0, 24), (6000, 6030), (11976, 12000)]:
+        lo, hi = max(0, a - 8), min(H, b + 8)
+        ref = O.run(np.ascontiguousarray(img[lo:hi]), op)
+        assert_same(got[a:b], ref[a - lo:a - lo + (b - a)], f"rows {a}:{b}")

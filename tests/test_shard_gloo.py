@@ -97,3 +97,59 @@ def test_gloo_strips_reproduce_whole_image(world, H, hm):
     for _, a, out in got:
         full[a:a + out.shape[0]] = out
     np.testing.assert_array_equal(full, whole)
+
+
+def _stats_worker(rank, world, port, H, W, q_out):
+    """Each rank: partial exact sums of its OWNED rows (LoG over strip + halo,
+    clamped only at the true image edges), then the SUM all-reduce."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = scenes.random_image(np.random.default_rng(77), H, W, 10, "mixed")
+        sh = StripShard(H, W, rank, world, 2)  # LoG radius: the only halo the statistics read
+        buf = sh.alloc(torch.int64, "cpu")
+        sh.load_owned(img.astype(np.int64))
+        for w in sh.exchange():
+            w.wait()
+        B = buf.numpy().astype(np.uint16)
+        v = [sh.rows * W]
+        rs, hi, lo = [], [], []
+        for s in (0.5, 20.0):
+            q, _ = O.mask_int(s, 5, 10)
+            r = O.log_response(B, q)[sh.ha:sh.ha + sh.rows].astype(object)
+            rs.append(int(r.sum()))
+            sq = [int(x) * int(x) for x in r.ravel()]
+            hi.append(sum(x >> 24 for x in sq))
+            lo.append(sum(x & 0xFFFFFF for x in sq))
+        I = B[sh.ha:sh.ha + sh.rows].astype(np.int64)
+        v += rs + hi + lo + [int(I.sum()), int((I * I).sum())]
+        t = torch.tensor(v, dtype=torch.int64)
+        sh.allreduce_stats(t)
+        q_out.put((rank, t.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_stats_allreduce_equals_whole_image(world):
+    H, W = 61, 45
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stats_worker, args=(r, world, port, H, W, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=240) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    img = scenes.random_image(np.random.default_rng(77), H, W, 10, "mixed")
+    for _, v in got:
+        assert v[0] == H * W
+        for j, s in enumerate((0.5, 20.0)):
+            qm, _ = O.mask_int(s, 5, 10)
+            r = O.log_response(img, qm)
+            assert v[1 + j] == int(r.sum())
+            assert v[3 + j] * 2**24 + v[5 + j] == sum(int(x) ** 2 for x in r.ravel())
+            # and the threshold the library resolves from them equals the oracle's sigma
+            assert O.global_std(v[0], v[1 + j], v[3 + j] * 2**24 + v[5 + j]) == O.std_of_response(r)

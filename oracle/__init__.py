@@ -52,7 +52,7 @@ class _Params(ctypes.Structure):
         ("out_mode", ctypes.c_int32),
         ("median_window2", ctypes.c_int32),
         ("adaptive", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("mask_mode", ctypes.c_int32),
     ]
 
 
@@ -80,6 +80,13 @@ def lib():
         L.lfo_run.argtypes = [ctypes.POINTER(_Params), P, ctypes.c_int, ctypes.c_int, P,
                               P, P, P, P, P, P, P]
         L.lfo_run.restype = ctypes.c_int
+        L.lfo_mask_f32.argtypes = [ctypes.c_double, ctypes.c_int, P, P]
+        L.lfo_log_response_f.argtypes = [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, ctypes.c_double, P]
+        L.lfo_zero_crossing_f.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_double, P]
+        L.lfo_std_gate_resp_int.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_int, P]
+        L.lfo_std_gate_resp_f.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_int, P]
         L.lfo_global_std_parts.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
                                            ctypes.c_uint64]
         L.lfo_global_std_parts.restype = ctypes.c_double
@@ -190,6 +197,49 @@ def hybrid_median(E: np.ndarray, m: int = 5) -> np.ndarray:
     return out
 
 
+# ------------------------------------------------------- F32 mode (R23) ----
+def mask_f32(sigma: float, n: int):
+    """(float32 mask = (float) L_dc, c = |L_dc(0,0)|)."""
+    w = np.empty((n, n), np.float32)
+    c = ctypes.c_double()
+    if lib().lfo_mask_f32(float(sigma), int(n), _ptr(w), ctypes.byref(c)) != 0:
+        raise ValueError("bad sigma/size")
+    return w, c.value
+
+
+def log_response_f(I: np.ndarray, w: np.ndarray, scale: float) -> np.ndarray:
+    """Normalised float response r^ = (w * I) * scale, |r^| < 1e-4 snapped to 0."""
+    I = np.ascontiguousarray(I, dtype=np.uint16)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    H, W = I.shape
+    r = np.empty((H, W), np.float64)
+    lib().lfo_log_response_f(_ptr(I), W, H, _ptr(w), w.shape[0], float(scale), _ptr(r))
+    return r
+
+
+def zero_crossing_f(r: np.ndarray, t: float = 0.0) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    H, W = r.shape
+    Z = np.empty((H, W), np.uint8)
+    lib().lfo_zero_crossing_f(_ptr(r), W, H, float(t), _ptr(Z))
+    return Z
+
+
+def std_gate_response(r: np.ndarray, Z: np.ndarray, w: int, T: float, T3: float = -1.0, at_zc: bool = False):
+    """R24 (SPEC.md:236): std over the signed response window (int64 r: exact;
+    float r: double), gated to ZC pixels.  T in the response's own units."""
+    Z = np.ascontiguousarray(Z, dtype=np.uint8)
+    H, W = Z.shape
+    keep = np.empty((H, W), np.uint8)
+    if np.issubdtype(r.dtype, np.integer):
+        r = np.ascontiguousarray(r, dtype=np.int64)
+        lib().lfo_std_gate_resp_int(_ptr(r), _ptr(Z), W, H, int(w), float(T), float(T3), int(at_zc), _ptr(keep))
+    else:
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        lib().lfo_std_gate_resp_f(_ptr(r), _ptr(Z), W, H, int(w), float(T), float(T3), int(at_zc), _ptr(keep))
+    return keep
+
+
 # ------------------------------------------------- adaptive thresholds ----
 def global_std(n: int, s1: int, s2: int) -> float:
     """R21: sqrt(n*S2 - S1^2) / n from exact integer sums (Python ints)."""
@@ -232,6 +282,7 @@ class Params:
     out_mode: int = 0
     median_window2: int = 0
     adaptive: int = 0  # bit 0: ZC gap k * sigma_r (R21); bit 1: std thresholds k * sigma_I (R22)
+    mask_mode: int = 0  # 0 integer masks (R3); 1 float masks + normalised response (R23)
 
     def to_c(self) -> _Params:
         p = _Params()
@@ -249,6 +300,7 @@ class Params:
         p.out_mode = self.out_mode
         p.median_window2 = self.median_window2
         p.adaptive = self.adaptive
+        p.mask_mode = self.mask_mode
         return p
 
 
@@ -288,4 +340,6 @@ def run(I: np.ndarray, params: Params, intermediates: bool = False):
     out = out.astype(out_dtype)
     if not intermediates:
         return out
+    if params.mask_mode == 1:  # F32 mode: the response buffers hold doubles (r^)
+        r0, r1 = r0.view(np.float64), r1.view(np.float64)
     return Result(out=out, r=[r0, r1], z=[z0, z1], keep=[k0, k1], E=E)

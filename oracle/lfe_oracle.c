@@ -252,6 +252,140 @@ void lfo_std_gate(const uint16_t *src, const uint8_t *Z, int W, int H, int w, do
         }
 }
 
+/* Signed-response std sources (NEXT-3, "s_a is computed over the
+ * signed LoG response values, gated to pixels the zero-crossing mask marked";
+ * reading R24).  at_zc = 0: the window holds r (every pixel); at_zc = 1: it
+ * holds r * Z (the response at crossings, 0 elsewhere).  INT mode: r integer,
+ * sums exact in int64 (w*w*|r|^2 < 2^60), compared as in R11 against
+ * Lambda*(Lambda-1)*Tr*Tr with Tr = T * 2^F * M (T normalised like R9). */
+void lfo_std_gate_resp_int(const int64_t *r, const uint8_t *Z, int W, int H, int w, double Tr, double T3r,
+                           int at_zc, uint8_t *keep)
+{
+    int R = w / 2;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t p = (size_t)y * W + x;
+            if (!Z[p]) { keep[p] = 0; continue; }
+            int64_t S1 = 0, S2 = 0, s1 = 0, s2 = 0;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx) {
+                    size_t q = (size_t)clampi(y + dy, 0, H - 1) * W + clampi(x + dx, 0, W - 1);
+                    int64_t a = at_zc && !Z[q] ? 0 : r[q];
+                    S1 += a;
+                    S2 += a * a;
+                    if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
+                        s1 += a;
+                        s2 += a * a;
+                    }
+                }
+            int pass = std_exceeds(S1, S2, w * w, Tr);
+            if (pass && T3r >= 0.0) pass = std_exceeds(s1, s2, 9, T3r);
+            keep[p] = (uint8_t)pass;
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* F32 mode (NEXT-3; SURVEY C3/C19 -> reading R23): float masks, the     */
+/* response normalised as r^ = r / (M * c), |r^| < 1e-4 snapped to 0.    */
+/* ------------------------------------------------------------------ */
+/* w = (float) L_dc (Eq. 1, DC-corrected, R2), c = |L_dc(0,0)|.  0 or -1. */
+int lfo_mask_f32(double sigma, int n, float *w, double *c_out)
+{
+    if (n < 1 || (n % 2) == 0 || n > 15) return -1;
+    double L[15 * 15];
+    if (lfo_log_dc(sigma, n, L) != 0) return -1;
+    for (int i = 0; i < n * n; ++i) w[i] = (float)L[i];
+    *c_out = fabs(L[(n / 2) * n + n / 2]);
+    return 0;
+}
+
+/* r^(p) = (sum_d w(d) * I(clamp(p+d))) * scale, in double; scale = 1/(M c);
+ * values with |r^| < 1e-4 are exact zeros (R23) */
+void lfo_log_response_f(const uint16_t *I, int W, int H, const float *w, int n, double scale, double *rh)
+{
+    int R = n / 2;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            double acc = 0.0;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx) {
+                    int yy = clampi(y + dy, 0, H - 1), xx = clampi(x + dx, 0, W - 1);
+                    acc += (double)w[(dy + R) * n + (dx + R)] * (double)I[(size_t)yy * W + xx];
+                }
+            double v = acc * scale;
+            rh[(size_t)y * W + x] = fabs(v) < 1e-4 ? 0.0 : v;
+        }
+}
+
+static inline int sgnd(double v) { return (v > 0) - (v < 0); }
+
+/* rule R* (R6-R9) on the normalised float response, threshold t normalised */
+void lfo_zero_crossing_f(const double *r, int W, int H, double t, uint8_t *Z)
+{
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            double nb[4];
+            nb[0] = r[(size_t)clampi(y - 1, 0, H - 1) * W + x];
+            nb[1] = r[(size_t)clampi(y + 1, 0, H - 1) * W + x];
+            nb[2] = r[(size_t)y * W + clampi(x - 1, 0, W - 1)];
+            nb[3] = r[(size_t)y * W + clampi(x + 1, 0, W - 1)];
+            double rp = r[(size_t)y * W + x];
+            int z = 0;
+            if (rp != 0.0) {
+                int any = 0, smallest = 1;
+                double gap = 0.0, ap = fabs(rp);
+                for (int k = 0; k < 4; ++k)
+                    if (sgnd(nb[k]) == -sgnd(rp)) {
+                        double an = fabs(nb[k]);
+                        any = 1;
+                        if (!(ap <= an)) smallest = 0;
+                        if (ap + an > gap) gap = ap + an;
+                    }
+                z = any && smallest && gap >= t;
+            } else {
+                double mx = nb[0], mn = nb[0];
+                for (int k = 1; k < 4; ++k) {
+                    if (nb[k] > mx) mx = nb[k];
+                    if (nb[k] < mn) mn = nb[k];
+                }
+                z = mx > 0 && mn < 0 && (mx - mn) >= t;
+            }
+            Z[(size_t)y * W + x] = (uint8_t)z;
+        }
+}
+
+/* R24 on the float response: s > T  <=>  Lambda*S2 - S1^2 > Lambda*(Lambda-1)*T^2, in double */
+void lfo_std_gate_resp_f(const double *r, const uint8_t *Z, int W, int H, int w, double T, double T3, int at_zc,
+                         uint8_t *keep)
+{
+    int R = w / 2;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t p = (size_t)y * W + x;
+            if (!Z[p]) { keep[p] = 0; continue; }
+            double S1 = 0, S2 = 0, s1 = 0, s2 = 0;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx) {
+                    size_t q = (size_t)clampi(y + dy, 0, H - 1) * W + clampi(x + dx, 0, W - 1);
+                    double a = at_zc && !Z[q] ? 0.0 : r[q];
+                    S1 += a;
+                    S2 += a * a;
+                    if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
+                        s1 += a;
+                        s2 += a * a;
+                    }
+                }
+            int L = w * w;
+            int pass = (double)L * S2 - S1 * S1 > (double)(L * (L - 1)) * T * T;
+            if (pass && T3 >= 0.0) pass = 9.0 * s2 - s1 * s1 > 72.0 * T3 * T3;
+            keep[p] = (uint8_t)pass;
+        }
+}
+
 /* ------------------------------------------------------------------ */
 /* O5 merge, "combined together" (R14, R15)                 */
 /* ------------------------------------------------------------------ */
@@ -375,7 +509,7 @@ typedef struct lfo_params {
     int32_t median_window2; /* 0 or a second hybrid-median level (R17) */
     int32_t adaptive;     /* bit 0: zc_threshold[j] = k_j, t_j = ceil(k_j sigma_r_j) (R21);
                              bit 1: std thresholds = k_j * sigma_I (R22) */
-    int32_t pad_;
+    int32_t mask_mode;    /* 0 = integer masks (R3), 1 = float masks, normalised response (R23) */
 } lfo_params;
 
 /* Optional intermediates (any may be NULL): r0/r1 int64[W*H], z0/z1, k0/k1
@@ -400,32 +534,53 @@ int lfo_run(const lfo_params *p, const uint16_t *I, int W, int H, uint16_t *out,
         return -2;
     }
     int rc = 0;
+    double *rh = (double *)r;  /* F32 mode reuses the 8-byte response buffer */
     for (int j = 0; j < 2 && rc == 0; ++j) {
         int n = p->log_size[j];
         int32_t q[15 * 15];
-        int F;
+        int F = 0;
         double s = p->sigma_is_variance ? sqrt(p->sigma[j]) : p->sigma[j];
-        if (lfo_mask_int(s, n, p->bit_depth, q, &F) != 0) { rc = -1; break; }
-        lfo_log_response(I, W, H, q, n, r);
-        int64_t t = (p->adaptive & 1) ? lfo_adaptive_zc_threshold(p->zc_threshold[j], lfo_std_of_response(r, N))
-                                      : lfo_zc_threshold_int(p->zc_threshold[j], F, p->bit_depth);
-        lfo_zero_crossing(r, W, H, t, Z);
+        double M = (double)(((int64_t)1 << p->bit_depth) - 1);
+        if (p->mask_mode == 1) {  /* R23 */
+            float w[15 * 15];
+            double c;
+            if (lfo_mask_f32(s, n, w, &c) != 0) { rc = -1; break; }
+            lfo_log_response_f(I, W, H, w, n, 1.0 / (M * c), rh);
+            lfo_zero_crossing_f(rh, W, H, p->zc_threshold[j], Z);
+        } else {
+            if (lfo_mask_int(s, n, p->bit_depth, q, &F) != 0) { rc = -1; break; }
+            lfo_log_response(I, W, H, q, n, r);
+            int64_t t = (p->adaptive & 1) ? lfo_adaptive_zc_threshold(p->zc_threshold[j], lfo_std_of_response(r, N))
+                                          : lfo_zc_threshold_int(p->zc_threshold[j], F, p->bit_depth);
+            lfo_zero_crossing(r, W, H, t, Z);
+        }
         if (j == 0 && r0o) memcpy(r0o, r, N * sizeof(int64_t));
         if (j == 1 && r1o) memcpy(r1o, r, N * sizeof(int64_t));
         if (j == 0 && z0o) memcpy(z0o, Z, N);
         if (j == 1 && z1o) memcpy(z1o, Z, N);
-        const uint16_t *s_img = I;
-        if (p->std_source == 0) {
-            for (size_t i = 0; i < N; ++i) src[i] = Z[i];
-            s_img = src;
-        }
         double T = p->std_threshold[j], T3 = p->std3_threshold[j];
         if (p->adaptive & 2) {  /* R22: multiples of the global intensity sigma */
             double sI = lfo_std_of_intensity(I, N);
             T = T * sI;
             if (T3 >= 0.0) T3 = T3 * sI;
         }
-        lfo_std_gate(s_img, Z, W, H, p->std_window, T, T3, K[j]);
+        if (p->std_source >= 2) {  /* R24: the signed response (2), or the response at crossings (3) */
+            int at_zc = p->std_source == 3;
+            if (p->mask_mode == 1) {
+                lfo_std_gate_resp_f(rh, Z, W, H, p->std_window, T, T3, at_zc, K[j]);
+            } else {
+                double unit = ldexp(1.0, F) * M;  /* normalised -> integer response units (R9) */
+                lfo_std_gate_resp_int(r, Z, W, H, p->std_window, T * unit, T3 >= 0.0 ? T3 * unit : -1.0, at_zc,
+                                      K[j]);
+            }
+        } else {
+            const uint16_t *s_img = I;
+            if (p->std_source == 0) {
+                for (size_t i = 0; i < N; ++i) src[i] = Z[i];
+                s_img = src;
+            }
+            lfo_std_gate(s_img, Z, W, H, p->std_window, T, T3, K[j]);
+        }
     }
     if (rc == 0) {
         if (k0o) memcpy(k0o, K[0], N);

@@ -589,3 +589,110 @@ def test_adaptive_constant_image_and_invariances():
     for T in _DIHEDRAL:
         np.testing.assert_array_equal(O.run(np.ascontiguousarray(T(I)), p), T(out))
     np.testing.assert_array_equal(O.run((255 - I.astype(np.int64)).astype(np.uint8), p), out)
+
+
+# ------------------------------------------------ F32 mode + response std (NEXT-3) ----
+@pytest.mark.parametrize("sigma,n,b", [(0.5, 5, 8), (20.0, 5, 10), (1.4, 7, 12), (0.8, 3, 16)])
+def test_log_f32_matches_scipy_and_snaps(sigma, n, b):
+    """R23: r^ = (sum w I) / (M c) with w = (float) L_dc; |r^| < 1e-4 -> 0.
+    scipy's correlate (double) of the same float weights is the reference."""
+    w, c = O.mask_f32(sigma, n)
+    L = O.log_dc(sigma, n)
+    assert np.array_equal(w, L.astype(np.float32)) and c == abs(L[n // 2, n // 2])
+    rng = np.random.default_rng(int(sigma * 10) + n + b)
+    I = scenes.random_image(rng, 23, 29, b)
+    M = (1 << b) - 1
+    rh = O.log_response_f(I, w, 1.0 / (M * c))
+    ref = ndi.correlate(I.astype(np.float64), w.astype(np.float64), mode="nearest") * (1.0 / (M * c))
+    ref[np.abs(ref) < 1e-4] = 0.0
+    np.testing.assert_allclose(rh, ref, rtol=1e-12, atol=1e-15)
+    # a constant image: the float mask sums to ~0, so every response snaps to exactly 0
+    assert not O.log_response_f(np.full((9, 9), M, I.dtype), w, 1.0 / (M * c)).any()
+
+
+def test_zc_f32_equals_integer_rule_on_integer_values():
+    """The float rule R* evaluated on integer-valued responses is the integer
+    rule (exhaustive 5-pixel crosses, as the integer pin)."""
+    vals = [-3, -1, 0, 1, 3]
+    for t in (0, 2, 4, 5):
+        pats = np.array(list(itertools.product(vals, repeat=5)), np.float64)
+        for i, (c, u, d, l, rr) in enumerate(pats):
+            R = np.zeros((3, 3))
+            R[1, 1], R[0, 1], R[2, 1], R[1, 0], R[1, 2] = c, u, d, l, rr
+            R[0, 0], R[0, 2], R[2, 0], R[2, 2] = u, u, d, d
+            Zf = O.zero_crossing_f(R, float(t))
+            assert Zf[1, 1] == _zc_brute(int(c), [int(u), int(d), int(l), int(rr)], t)
+
+
+def _stdev_gate_brute(r, Z, w, T, T3, at_zc):
+    """Eq. 2 literally with exact rationals: keep = Z & s_w > T & (T3<0 | s_3 > T3)."""
+    from fractions import Fraction as Fr
+    H, W = Z.shape
+    keep = np.zeros_like(Z)
+    at = lambda y, x: (0 if at_zc and not Z[min(max(y, 0), H - 1), min(max(x, 0), W - 1)]
+                       else int(r[min(max(y, 0), H - 1), min(max(x, 0), W - 1)]))
+
+    def var_gt(vals, T):  # sample variance > T^2, exactly
+        n = len(vals)
+        m = Fr(sum(vals), n)
+        return sum((Fr(v) - m) ** 2 for v in vals) / (n - 1) > Fr(T) ** 2
+    for y in range(H):
+        for x in range(W):
+            if not Z[y, x]:
+                continue
+            R = w // 2
+            ok = var_gt([at(y + dy, x + dx) for dy in range(-R, R + 1) for dx in range(-R, R + 1)], T)
+            if ok and T3 >= 0:
+                ok = var_gt([at(y + dy, x + dx) for dy in (-1, 0, 1) for dx in (-1, 0, 1)], T3)
+            keep[y, x] = ok
+    return keep
+
+
+@pytest.mark.parametrize("w,at_zc", [(5, False), (5, True), (3, False), (7, True)])
+def test_std_gate_response_brute_force(w, at_zc):
+    """R24: Eq. 2 over the signed response window (or the response
+    at crossings), integer path exact against rational arithmetic."""
+    rng = np.random.default_rng(50 + w + at_zc)
+    r = rng.integers(-900, 900, (11, 13)).astype(np.int64)
+    Z = (rng.random((11, 13)) < 0.5).astype(np.uint8)
+    for T, T3 in [(300.3, -1.0), (450.7, 200.1), (0.0, -1.0), (700.2, 650.9)]:
+        got = O.std_gate_response(r, Z, w, T, T3, at_zc)
+        np.testing.assert_array_equal(got, _stdev_gate_brute(r, Z, w, T, T3, at_zc), err_msg=f"T={T} T3={T3}")
+        gf = O.std_gate_response(r.astype(np.float64), Z, w, T, T3, at_zc)  # the float variant agrees here
+        np.testing.assert_array_equal(gf, got)
+
+
+def test_pipeline_f32_agrees_with_integer_mode_away_from_ties():
+    """INT and F32 modes quantise the same Eq. 1 masks differently; their outputs
+    must agree almost everywhere (a sign error, scale error or dropped term in
+    either path would break this massively)."""
+    img = scenes.scene_c1(clean=False)
+    for src, T in [(0, (0.3, 0.3)), (2, (0.02, 0.02))]:
+        pi = O.Params(bit_depth=8, zc_threshold=(0.01, 0.01), out_mode=1, std_source=src, std_threshold=T)
+        pf = O.Params(bit_depth=8, zc_threshold=(0.01, 0.01), out_mode=1, std_source=src, std_threshold=T,
+                      mask_mode=1)
+        a, b = O.run(img, pi), O.run(img, pf)
+        assert a.any() and (a != b).mean() < 0.01, (src, (a != b).mean())
+    # the float responses are the integer ones rescaled (within the quantisation error)
+    res_i = O.run(img, pi, intermediates=True)
+    res_f = O.run(img, pf, intermediates=True)
+    for j, s in enumerate((0.5, 20.0)):
+        _, F = O.mask_int(s, 5, 8)
+        scaled = res_i.r[j] / (2.0**F * 255)
+        assert np.max(np.abs(scaled - res_f.r[j])) < 2e-3 * np.max(np.abs(scaled))
+
+
+def test_pipeline_response_std_source_matches_stagewise_composition():
+    """std_source 2/3 in the pipeline = LoG -> ZC -> std_gate_response with the
+    threshold converted to integer units T * 2^F * M (R9 normalisation)."""
+    rng = np.random.default_rng(60)
+    I = scenes.random_image(rng, 31, 37, 10)
+    for src in (2, 3):
+        p = O.Params(bit_depth=10, std_source=src, std_threshold=(0.05, 0.01), hybrid_median=False,
+                     zc_threshold=(0.002, 0.0), out_mode=1)
+        res = O.run(I, p, intermediates=True)
+        for j, s in enumerate((0.5, 20.0)):
+            _, F = O.mask_int(s, 5, 10)
+            unit = 2.0**F * 1023
+            k = O.std_gate_response(res.r[j], res.z[j], 5, p.std_threshold[j] * unit, -1.0, src == 3)
+            np.testing.assert_array_equal(k, res.keep[j])

@@ -95,6 +95,16 @@ def config_dict(size, world, p):
     }
 
 
+def ncu_issue():
+    """Executed warp-instructions per launch of the dominant kernel (committed
+    ncu summary, profiles/issue.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def measured_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -192,9 +202,28 @@ def cpu_baseline(img, p, rows=None):
     oracle.run(band, op)
     dt = time.perf_counter() - t0
     px = rows * img.shape[1]  # output rows counted (halo rows are overhead)
-    return {"value": round(px / dt / 1e6, 3), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+    # single-thread leg on a small bounded sample
+    cores = oracle.get_threads()
+    r1 = min(192, H)
+    a1 = H // 2 - r1 // 2
+    b1 = img[max(0, a1 - h):min(H, a1 + r1 + h)].copy()
+    oracle.set_threads(1)
+    t1 = time.perf_counter()
+    oracle.run(b1, op)
+    d1 = time.perf_counter() - t1
+    oracle.set_threads(cores)
+    model = "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        pass
+    return {"value": round(px / dt / 1e6, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{rows} x {img.shape[1]} rows of the c3 scene (+{h} halo rows each side), one run, "
-                      f"{dt:.2f} s, plain C oracle -O2 OpenMP over rows"}
+                      f"{dt:.2f} s, plain C oracle -O2 OpenMP over rows",
+            "single_thread": {"value": round(r1 * img.shape[1] / d1 / 1e6, 3), "unit": UNIT,
+                              "sample": f"{r1} x {img.shape[1]} rows, 1 thread, {d1:.2f} s"},
+            "cpu_model": model, "host_cpus": os.cpu_count()}
 
 
 def run_reference(args, world, rank):
@@ -390,7 +419,23 @@ def main():
             "gpu_launches": int(launches),
             "cpu_baseline": cpu,
             "clocks": clk,
+            "paper_context": {"note": "other hardware (Tesla C2075 vs Xeon E5620), context only",
+                              "paper_gpu_kernel_mpx_s": 43.0, "paper_gpu_kernel_workload": "Cartosat-1 4000x4000, "
+                              "urban (Table 6, PAPER.md:226)", "paper_speedup": "20.7x GPU vs 2-thread CPU "
+                              "(AWiFS, Table 7, PAPER.md:236)",
+                              "this_gpu_vs_oracle": round(value / cpu["value"], 1) if cpu else None},
         }
+        iss = ncu_issue()
+        if iss and not p.adaptive and not p.median_window2:
+            # the binding resource: instruction issue, 4 warp-instructions
+            # per clock per SM = 148 * 4 * 32 lane-ops per clock at the SM clock under load
+            mhz = (clk or {}).get("sm_mhz") or 1965.0
+            ach = iss["inst_per_launch"] * 32 / (k_ms * 1e-3) / 1e12
+            pk = 148 * 4 * 32 * mhz * 1e6 / 1e12
+            line["issue"] = {"bound": "alu", "achieved": round(ach, 2), "peak": round(pk, 2),
+                             "unit": "Tlane-op/s issued", "frac": round(ach / pk, 4),
+                             "inst_per_launch": iss["inst_per_launch"], "sm_mhz": mhz,
+                             "source": iss.get("source")}
         tr = ncu_traffic()
         if tr:
             line["roofline"]["traffic"] = tr.get("bytes_per_launch")

@@ -52,8 +52,11 @@ typedef enum lfe_status {
     LFE_ERANGE = 6         /* an input pixel exceeded 2^bit_depth - 1 (asynchronous)  */
 } lfe_status;
 
-/* Which image the Eq. 2 deviation is computed on (reading R10). */
-enum { LFE_STD_ZC = 0, LFE_STD_INTENSITY = 1 };
+/* Which image the Eq. 2 deviation is computed on (reading R10; the two
+ * signed-response readings of SPEC.md:236 are R24). */
+enum { LFE_STD_ZC = 0, LFE_STD_INTENSITY = 1, LFE_STD_RESPONSE = 2, LFE_STD_RESPONSE_AT_ZC = 3 };
+/* Mask arithmetic (reading R3: integer, the bit-exact contract; R23: float). */
+enum { LFE_MASK_INT = 0, LFE_MASK_F32 = 1 };
 /* What the merged image holds (reading R15). */
 enum { LFE_OUT_EXTRACT = 0, LFE_OUT_MASK = 1 };
 /* lfe_extract_rows: which strip sides are true image edges (clamped). */
@@ -66,7 +69,7 @@ enum { LFE_KERNEL_AUTO = 0, LFE_KERNEL_STAGED = 1, LFE_KERNEL_FUSED = 2 };
 enum { LFE_ADAPT_ZC = 1u, LFE_ADAPT_STD = 2u };
 
 /* The problem as the paper states it.  Index 0/1 = the two
- * LoG branches (neutral labels, reading R18).  112 bytes, natural alignment. */
+ * LoG branches (neutral labels, reading R18).  120 bytes, natural alignment. */
 typedef struct lfe_params {
     uint32_t abi_size;          /* = sizeof(lfe_params)                                  */
     int32_t bit_depth;          /* 1..16                                                 */
@@ -80,7 +83,9 @@ typedef struct lfe_params {
                                 /*       are multiples of sigma(I); needs the INTENSITY   */
                                 /*       std source (R22)                                 */
     double zc_threshold[2];     /* >= 0; gap threshold normalised by 2^F * (2^b - 1) (R9) */
-    int32_t std_source;         /* LFE_STD_ZC (default, R10) or LFE_STD_INTENSITY         */
+    int32_t std_source;         /* LFE_STD_ZC (default, R10), LFE_STD_INTENSITY, or the   */
+                                /* signed response LFE_STD_RESPONSE[_AT_ZC] (R24; T then */
+                                /* in normalised response units like zc_threshold)       */
     int32_t std_window;         /* odd 3, 5 or 7 (paper: 5)                               */
     double std_threshold[2];    /* T >= 0: keep iff s > T (Eq. 2, strict, R11)            */
     double std3_threshold[2];   /* < 0 disables the 3x3 re-check (R12); else s3 > T3 too  */
@@ -91,6 +96,11 @@ typedef struct lfe_params {
                                 /* to the first one's output -- the water-body pipeline's */
                                 /* "multiple levels of higher and lower dimensions"       */
                                 /* (reading R17); needs hybrid_median = 1   */
+    int32_t mask_mode;          /* LFE_MASK_INT (default): integer masks, bit-exact (R3); */
+                                /* LFE_MASK_F32: float masks, FP32 response normalised by */
+                                /* (2^b - 1)|L_dc(0,0)| -- equal to the oracle within the */
+                                /* tolerance contract of R23 (general kernel only)        */
+    int32_t reserved1;          /* must be 0                                             */
 } lfe_params;
 
 typedef struct lfe_ctx lfe_ctx;

@@ -21,6 +21,13 @@ lfe_status lfe_test_mask(double sigma, int32_t n, int32_t bit_depth, int32_t *q,
 /* Validation only (what lfe_create checks before touching the device). */
 lfe_status lfe_test_validate(const lfe_params *p);
 
+/* The LoG response of branch 0/1 as the general kernel computes it, for every
+ * pixel of a W x H device image: int32 r (integer masks) or float r^ (F32
+ * masks, normalised and snapped, R23) into d_r (W*H elements, row-major,
+ * 4 bytes each).  Enqueued on cuda_stream.  Errors: EINVAL, ECUDA. */
+lfe_status lfe_test_response(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
+                             int32_t height, int32_t branch, void *d_r, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,94 @@ __device__ __forceinline__ uint32_t median_n(uint32_t *v, int n)
     return v[n / 2];
 }
 
+// LoG response of branch j at (cy, cx) from the replicate-padded input region
+// (R3-R5): int32 with integer masks, or -- F32 mode, R23 -- the
+// FP32 sum in row-major tap order times 1/(M c), |r^| < 1e-4 snapped to 0,
+// returned as its bit pattern.
+__device__ __forceinline__ int32_t log_at(const KParams &kp, int j, const uint16_t *sI, const Region &RI, int cy,
+                                          int cx, int W, int Hv)
+{
+    const int n = kp.n[j], R = n / 2;
+    if (kp.f32) {
+        float acc = 0.0f;
+        for (int dy = -R; dy <= R; ++dy) {
+            const int yy = clampi(cy + dy, 0, Hv - 1);
+            for (int dx = -R; dx <= R; ++dx) {
+                const int xx = clampi(cx + dx, 0, W - 1);
+                acc = fmaf(kp.wf[j][(dy + R) * n + (dx + R)], (float)sI[RI.idx(yy, xx)], acc);
+            }
+        }
+        float v = acc * kp.fscale[j];
+        if (fabsf(v) < 1e-4f) v = 0.0f;
+        return __float_as_int(v);
+    }
+    int32_t acc = 0;
+    for (int dy = -R; dy <= R; ++dy) {
+        const int yy = clampi(cy + dy, 0, Hv - 1);
+        for (int dx = -R; dx <= R; ++dx) {
+            const int xx = clampi(cx + dx, 0, W - 1);
+            acc += kp.q[j][(dy + R) * n + (dx + R)] * (int32_t)sI[RI.idx(yy, xx)];
+        }
+    }
+    return acc;
+}
+
+// Rule R* (R6-R9) at pixel value rp with the four neighbours nb (integer units)
+__device__ __forceinline__ int zc_rule_int(int32_t rp, const int32_t (&nb)[4], int32_t t)
+{
+    if (rp != 0) {
+        const int32_t ap = rp < 0 ? -rp : rp;
+        bool any = false, smallest = true;
+        int32_t gap = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t rn = nb[k];
+            if (rp > 0 ? rn < 0 : rn > 0) {
+                const int32_t an = rn < 0 ? -rn : rn;
+                any = true;
+                smallest &= ap <= an;
+                gap = max(gap, ap + an);
+            }
+        }
+        return any && smallest && gap >= t;
+    }
+    int32_t mx = nb[0], mn = nb[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+        mx = max(mx, nb[k]);
+        mn = min(mn, nb[k]);
+    }
+    return mx > 0 && mn < 0 && (mx - mn) >= t;
+}
+
+// the same rule on the normalised float response (F32 mode, R23)
+__device__ __forceinline__ int zc_rule_f32(float rp, const float (&nb)[4], float t)
+{
+    if (rp != 0.0f) {
+        const float ap = fabsf(rp);
+        bool any = false, smallest = true;
+        float gap = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float rn = nb[k];
+            if (rp > 0.0f ? rn < 0.0f : rn > 0.0f) {
+                const float an = fabsf(rn);
+                any = true;
+                smallest &= ap <= an;
+                gap = fmaxf(gap, ap + an);
+            }
+        }
+        return any && smallest && gap >= t;
+    }
+    float mx = nb[0], mn = nb[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+        mx = fmaxf(mx, nb[k]);
+        mn = fminf(mn, nb[k]);
+    }
+    return mx > 0.0f && mn < 0.0f && (mx - mn) >= t;
+}
+
 // Hybrid median of region S at (vy, vx) with radius R (R16, R17):
 // med3(median of the '+' group, median of the 'x' group, centre), both groups
 // including the centre; neighbours at clamped coordinates (R5).
@@ -136,23 +224,12 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err_flag, 1);
 
-    // ---- stage 1: the two LoG responses (Eq. 1 masks, integer, R3)
+    // ---- stage 1: the two LoG responses (Eq. 1 masks, integer R3 or float R23)
     for (int i = threadIdx.x; i < RR.h * RR.w; i += kThreads) {
         int cy = clampi(RR.oy + i / RR.w, 0, Hv - 1);
         int cx = clampi(RR.ox + i % RR.w, 0, W - 1);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int n = kp.n[j], R = n / 2;
-            int32_t acc = 0;
-            for (int dy = -R; dy <= R; ++dy) {
-                int yy = clampi(cy + dy, 0, Hv - 1);
-                for (int dx = -R; dx <= R; ++dx) {
-                    int xx = clampi(cx + dx, 0, W - 1);
-                    acc += kp.q[j][(dy + R) * n + (dx + R)] * (int32_t)sI[RI.idx(yy, xx)];
-                }
-            }
-            sR[j * RR.h * RR.w + i] = acc;
-        }
+        for (int j = 0; j < 2; ++j) sR[j * RR.h * RR.w + i] = log_at(kp, j, sI, RI, cy, cx, W, Hv);
     }
     __syncthreads();
 
@@ -166,32 +243,14 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int32_t *r = sR + j * RR.h * RR.w;
-            int32_t rp = r[pi];
             int z;
-            if (rp != 0) {
-                int32_t ap = rp < 0 ? -rp : rp;
-                bool any = false, smallest = true;
-                int32_t gap = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    int32_t rn = r[nbi[k]];
-                    bool opp = rp > 0 ? rn < 0 : rn > 0;
-                    if (opp) {
-                        int32_t an = rn < 0 ? -rn : rn;
-                        any = true;
-                        smallest &= ap <= an;
-                        gap = max(gap, ap + an);
-                    }
-                }
-                z = any && smallest && gap >= kp.zc_t[j];
+            if (kp.f32) {
+                const float nb[4] = {__int_as_float(r[nbi[0]]), __int_as_float(r[nbi[1]]), __int_as_float(r[nbi[2]]),
+                                     __int_as_float(r[nbi[3]])};
+                z = zc_rule_f32(__int_as_float(r[pi]), nb, kp.zc_tf[j]);
             } else {
-                int32_t mx = r[nbi[0]], mn = mx;
-#pragma unroll
-                for (int k = 1; k < 4; ++k) {
-                    mx = max(mx, r[nbi[k]]);
-                    mn = min(mn, r[nbi[k]]);
-                }
-                z = mx > 0 && mn < 0 && (mx - mn) >= kp.zc_t[j];
+                const int32_t nb[4] = {r[nbi[0]], r[nbi[1]], r[nbi[2]], r[nbi[3]]};
+                z = zc_rule_int(r[pi], nb, kp.zc_t[j]);
             }
             sZ[j * RZ.h * RZ.w + i] = (uint8_t)z;
         }
@@ -223,6 +282,47 @@ __global__ void __launch_bounds__(kThreads)
                 }
                 pass = (kp.pass_lut[j] >> k) & 1ull;
                 if (pass && kp.recheck[j]) pass = (kp.pass3_lut[j] >> k3) & 1u;
+            } else if (kp.std_source >= LFE_STD_RESPONSE) {
+                // R24: Eq. 2 over the signed response window (or the
+                // response at crossings); thresholds pre-scaled to response units
+                const bool at_zc = kp.std_source == LFE_STD_RESPONSE_AT_ZC;
+                const int32_t *r = sR + j * RR.h * RR.w;
+                const int L = kp.w * kp.w;
+                if (kp.f32) {
+                    double s1 = 0, s2 = 0, t1 = 0, t2 = 0;
+                    for (int dy = -Rs; dy <= Rs; ++dy) {
+                        int yy = clampi(cy + dy, 0, Hv - 1);
+                        for (int dx = -Rs; dx <= Rs; ++dx) {
+                            int xx = clampi(cx + dx, 0, W - 1);
+                            double a = (at_zc && !Z[RZ.idx(yy, xx)]) ? 0.0 : (double)__int_as_float(r[RR.idx(yy, xx)]);
+                            s1 += a;
+                            s2 += a * a;
+                            if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
+                                t1 += a;
+                                t2 += a * a;
+                            }
+                        }
+                    }
+                    pass = (double)L * s2 - s1 * s1 > kp.rhs[j];
+                    if (pass && kp.recheck[j]) pass = 9.0 * t2 - t1 * t1 > kp.rhs3[j];
+                } else {
+                    int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
+                    for (int dy = -Rs; dy <= Rs; ++dy) {
+                        int yy = clampi(cy + dy, 0, Hv - 1);
+                        for (int dx = -Rs; dx <= Rs; ++dx) {
+                            int xx = clampi(cx + dx, 0, W - 1);
+                            int64_t a = (at_zc && !Z[RZ.idx(yy, xx)]) ? 0 : (int64_t)r[RR.idx(yy, xx)];
+                            s1 += a;
+                            s2 += a * a;
+                            if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
+                                t1 += a;
+                                t2 += a * a;
+                            }
+                        }
+                    }
+                    pass = (double)((int64_t)L * s2 - s1 * s1) > kp.rhs[j];
+                    if (pass && kp.recheck[j]) pass = (double)(9 * t2 - t1 * t1) > kp.rhs3[j];
+                }
             } else {
                 int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
                 for (int dy = -Rs; dy <= Rs; ++dy) {
@@ -281,6 +381,25 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// test entry (lfe_test_response): branch j's response at every pixel
+template <typename Tin>
+__global__ void __launch_bounds__(kThreads)
+    response_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, int j, int32_t *d_r)
+{
+    constexpr int T = 16;
+    __shared__ uint16_t sI[(T + 2 * (kMaxMask / 2)) * (T + 2 * (kMaxMask / 2))];
+    const int W = g.width, Hv = g.Hv, R = kp.RL;
+    const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
+    const Region RI{y0 - R, x0 - R, T + 2 * R, T + 2 * R};
+    for (int i = threadIdx.x; i < RI.h * RI.w; i += kThreads) {
+        const int vy = clampi(RI.oy + i / RI.w, 0, Hv - 1), vx = clampi(RI.ox + i % RI.w, 0, W - 1);
+        sI[i] = (uint16_t)reinterpret_cast<const Tin *>(reinterpret_cast<const char *>(g.in) + (int64_t)vy * g.in_pitch)[vx];
+    }
+    __syncthreads();
+    const int y = y0 + threadIdx.x / T, x = x0 + threadIdx.x % T;
+    if (y < Hv && x < W) d_r[(int64_t)y * W + x] = log_at(kp, j, sI, RI, y, x, W, Hv);
+}
+
 size_t staged_smem(const KParams &kp, int TW, int TH)
 {
     int h = kp.halo, hr = h - kp.RL, hz = hr - 1, hm2 = kp.Rm2, he = kp.Rm + hm2;
@@ -310,6 +429,16 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
         cudaFuncSetAttribute(staged_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         staged_kernel<uint8_t><<<grid, kThreads, smem, s>>>(kp, g, TW, TH, err_flag);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int branch, void *d_r, cudaStream_t s)
+{
+    dim3 grid((g.width + 15) / 16, (g.Hv + 15) / 16);
+    if (in16)
+        response_kernel<uint16_t><<<grid, kThreads, 0, s>>>(kp, g, branch, reinterpret_cast<int32_t *>(d_r));
+    else
+        response_kernel<uint8_t><<<grid, kThreads, 0, s>>>(kp, g, branch, reinterpret_cast<int32_t *>(d_r));
     return cudaGetLastError();
 }
 

@@ -129,8 +129,13 @@ lfe_status validate(const lfe_params *p)
         if (std::isnan(p->std3_threshold[j]) || std::isinf(p->std3_threshold[j]))
             return fail(LFE_EINVAL, "std3_threshold[%d] must be finite (< 0 disables)", j);
     }
-    if (p->std_source != LFE_STD_ZC && p->std_source != LFE_STD_INTENSITY)
-        return fail(LFE_EINVAL, "std_source must be LFE_STD_ZC or LFE_STD_INTENSITY");
+    if (p->std_source < LFE_STD_ZC || p->std_source > LFE_STD_RESPONSE_AT_ZC)
+        return fail(LFE_EINVAL, "std_source must be one of LFE_STD_*");
+    if (p->mask_mode != LFE_MASK_INT && p->mask_mode != LFE_MASK_F32)
+        return fail(LFE_EINVAL, "mask_mode must be LFE_MASK_INT or LFE_MASK_F32");
+    if (p->reserved1) return fail(LFE_EINVAL, "reserved fields must be 0");
+    if (p->mask_mode == LFE_MASK_F32 && (p->adaptive & LFE_ADAPT_ZC))
+        return fail(LFE_EINVAL, "LFE_ADAPT_ZC is defined on the integer response (R21): needs LFE_MASK_INT");
     if (p->std_window < 1 || !(p->std_window & 1)) return fail(LFE_EINVAL, "std_window must be odd");
     if (!odd_in(p->std_window, 3, kMaxStdWindow))
         return fail(LFE_EUNSUPPORTED, "std_window %d not in {3,5,7}", p->std_window);
@@ -183,13 +188,19 @@ void apply_thresholds(lfe_ctx *c, const int64_t zt[2], const double T[2], const 
     for (int j = 0; j < 2; ++j) {
         // a gap never exceeds 2^25, so any t above it acts alike
         kp.zc_t[j] = zt[j] > (int64_t(1) << 26) ? (1 << 26) : (int32_t)zt[j];
+        // signed-response std sources with integer masks (R24): normalised T -> integer
+        // response units, T * 2^F * M (as R9)
+        const bool to_int = c->p.std_source >= LFE_STD_RESPONSE && c->p.mask_mode == LFE_MASK_INT;
+        const double unit = to_int ? std::ldexp(1.0, c->F[j]) * (double)((int64_t(1) << c->p.bit_depth) - 1) : 1.0;
+        const double Tu = to_int ? T[j] * unit : T[j];
+        const double T3u = to_int ? (T3[j] >= 0.0 ? T3[j] * unit : -1.0) : T3[j];
         // std gate (R11): s > T  <=>  L*S2 - S1^2 > L*(L-1)*T*T, compared in double
-        kp.rhs[j] = (double)(L * (L - 1)) * T[j] * T[j];
+        kp.rhs[j] = (double)(L * (L - 1)) * Tu * Tu;
         kp.pass_lut[j] = 0;
         for (int k = 0; k <= L; ++k)
             if ((double)((int64_t)L * k - (int64_t)k * k) > kp.rhs[j]) kp.pass_lut[j] |= 1ull << k;
-        kp.recheck[j] = T3[j] >= 0.0;
-        kp.rhs3[j] = (double)(9 * 8) * T3[j] * T3[j];
+        kp.recheck[j] = T3u >= 0.0;
+        kp.rhs3[j] = (double)(9 * 8) * T3u * T3u;
         kp.pass3_lut[j] = 0;
         for (int k = 0; k <= 9; ++k)
             if ((double)(9 * k - k * k) > kp.rhs3[j]) kp.pass3_lut[j] |= 1u << k;
@@ -311,6 +322,14 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
         }
         kp.n[j] = n;
         kp.RL = n / 2 > kp.RL ? n / 2 : kp.RL;
+        if (p->mask_mode == LFE_MASK_F32) {  // R23: float masks, response normalised by M*|L_dc(0,0)|
+            double Ld[kMaxMaskCoeffs], tot = 0.0;
+            for (int i = 0; i < n * n; ++i) tot += (Ld[i] = eq1(s, i % n - n / 2, i / n - n / 2));
+            for (int i = 0; i < n * n; ++i) kp.wf[j][i] = (float)(Ld[i] - tot / (double)(n * n));
+            const double cc = std::fabs(Ld[(n / 2) * n + n / 2] - tot / (double)(n * n));
+            kp.fscale[j] = (float)(1.0 / ((double)maxv * cc));
+            kp.zc_tf[j] = (float)p->zc_threshold[j];
+        }
         if (n == 5) {
             const int32_t *q = kp.q[j];
             // orbits (0,0) (1,0) (2,0) (1,1) (2,1) (2,2) at row-major index (2+y)*5+(2+x)
@@ -333,6 +352,7 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
     kp.out_mode = p->out_mode;
     kp.halo = kp.RL + 1 + kp.Rs + kp.Rm + kp.Rm2;
     kp.adaptive = p->adaptive;
+    kp.f32 = p->mask_mode == LFE_MASK_F32;
     if (!p->adaptive) {
         int64_t zt[2];
         for (int j = 0; j < 2; ++j)  // gap threshold in integer units, t = ceil(thr * 2^F * M) (R9)
@@ -650,6 +670,18 @@ lfe_status lfe_test_mask(double sigma, int32_t n, int32_t bit_depth, int32_t *q,
 }
 
 lfe_status lfe_test_validate(const lfe_params *p) { return validate(p); }
+
+lfe_status lfe_test_response(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, int32_t branch,
+                             void *d_r, void *stream)
+{
+    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_r, (int64_t)W * 4, H);
+    if (st != LFE_OK) return st;
+    if (branch != 0 && branch != 1) return fail(LFE_EINVAL, "branch must be 0 or 1");
+    Geometry g{d_in, in_pitch, nullptr, 0, W, H, 0, H};
+    cudaError_t e = launch_response(c->kp, g, c->p.bit_depth > 8, branch, d_r, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "response launch: %s", cudaGetErrorString(e));
+    return LFE_OK;
+}
 
 void lfe_destroy(lfe_ctx *c)
 {

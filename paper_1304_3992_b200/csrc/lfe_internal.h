@@ -39,6 +39,11 @@ struct KParams {
     // orbit coefficients of 5x5 masks for the fused kernel: (0,0) (1,0) (2,0) (1,1) (2,1) (2,2)
     int32_t orb[2][6];
     int32_t adaptive;              // LFE_ADAPT_* (thresholds resolved on the host before launch)
+    // F32 mode (R23): float masks, response scale 1/(M c), ZC threshold (normalised)
+    int32_t f32;
+    float wf[2][kMaxMaskCoeffs];
+    float fscale[2];
+    float zc_tf[2];
 };
 
 // A virtual image: rows [0, Hv) of `width` pixels, clamped (edge-replicated)
@@ -66,6 +71,8 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
                          int *err_flag, cudaStream_t s);
 bool fused_supports(const KParams &kp, int bit_depth);
+// test entry: branch j's response for every pixel of a whole image (int32 or float bits)
+cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int branch, void *d_r, cudaStream_t s);
 // adds the exact global sums of output rows [o0, o1) to *d_stats (NEXT-2)
 cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, cudaStream_t s);
 

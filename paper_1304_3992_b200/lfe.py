@@ -20,7 +20,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LFE_LIB") or os.path.join(_PKG, "liblfe.so")  # LFE_LIB: A/B experiments only
 
 LFE_OK, LFE_EINVAL, LFE_EUNSUPPORTED, LFE_ENOMEM, LFE_ENODEV, LFE_ECUDA, LFE_ERANGE = range(7)
-LFE_STD_ZC, LFE_STD_INTENSITY = 0, 1
+LFE_STD_ZC, LFE_STD_INTENSITY, LFE_STD_RESPONSE, LFE_STD_RESPONSE_AT_ZC = 0, 1, 2, 3
+LFE_MASK_INT, LFE_MASK_F32 = 0, 1
 LFE_OUT_EXTRACT, LFE_OUT_MASK = 0, 1
 LFE_TOP_IS_EDGE, LFE_BOTTOM_IS_EDGE = 1, 2
 LFE_OPT_KERNEL, LFE_OPT_TILE_W, LFE_OPT_TILE_H, LFE_OPT_HOST_STRIP_ROWS = 1, 2, 3, 4
@@ -54,10 +55,12 @@ class lfe_params(ctypes.Structure):
         ("median_window", ctypes.c_int32),
         ("out_mode", ctypes.c_int32),
         ("median_window2", ctypes.c_int32),
+        ("mask_mode", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
     ]
 
 
-assert ctypes.sizeof(lfe_params) == 112
+assert ctypes.sizeof(lfe_params) == 120
 
 
 class lfe_stats(ctypes.Structure):
@@ -81,7 +84,7 @@ EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows"
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
            "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
            "lfe_set_stats", "lfe_get_thresholds"]
-TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate"]  # include/lfe_test.h
+TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response"]  # include/lfe_test.h
 
 
 def load():
@@ -132,6 +135,8 @@ def load():
     L.lfe_test_mask.restype = st
     L.lfe_test_validate.argtypes = [ctypes.POINTER(lfe_params)]
     L.lfe_test_validate.restype = st
+    L.lfe_test_response.argtypes = [P, P, I64, I32, I32, I32, P, P]
+    L.lfe_test_response.restype = st
     _lib = L
     return L
 
@@ -255,6 +260,7 @@ class Params:
     out_mode: int = LFE_OUT_EXTRACT
     median_window2: int = 0  # second hybrid-median level (water-body pipeline)
     adaptive: int = 0        # LFE_ADAPT_* (readings R21, R22)
+    mask_mode: int = LFE_MASK_INT  # LFE_MASK_F32: float masks, tolerance contract (R23)
 
     def to_c(self) -> lfe_params:
         p = lfe_params()
@@ -273,6 +279,7 @@ class Params:
         p.out_mode = self.out_mode
         p.median_window2 = self.median_window2
         p.adaptive = self.adaptive
+        p.mask_mode = self.mask_mode
         return p
 
 
@@ -390,6 +397,18 @@ class Context:
 
     def thresholds(self):
         return lfe_get_thresholds(self.handle)
+
+    def test_response(self, t_in, branch: int, stream=None):
+        """lfe_test_response: branch's LoG response of a whole device image as the
+        general kernel computes it (int32, or float32 in F32 mode)."""
+        import torch
+        pi, pin = self._torch_img(t_in, "input")
+        H, W = t_in.shape
+        dt = torch.float32 if self.params.mask_mode == LFE_MASK_F32 else torch.int32
+        out = torch.empty((H, W), dtype=dt, device=t_in.device)
+        _check(load().lfe_test_response(self.handle, pi, pin, W, H, branch, out.data_ptr(), self._stream(stream)),
+               "lfe_test_response")
+        return out
 
     def last_async_error(self, stream=None) -> int:
         return lfe_last_async_error(self.handle, self._stream(stream))

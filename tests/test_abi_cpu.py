@@ -49,7 +49,7 @@ def test_no_torch_types_in_signatures():
 def test_abi_version_and_params_default():
     assert lfe.lfe_abi_version() == 1
     p = lfe.lfe_params_default()
-    assert p.abi_size == ctypes.sizeof(lfe.lfe_params) == 112
+    assert p.abi_size == ctypes.sizeof(lfe.lfe_params) == 120
     assert (p.bit_depth, p.sigma[0], p.sigma[1], p.log_size[0], p.log_size[1]) == (8, 0.5, 20.0, 5, 5)
     assert (p.std_source, p.std_window, p.std_threshold[0], p.std3_threshold[0]) == (0, 5, 0.3, -1.0)
     assert (p.hybrid_median, p.median_window, p.out_mode, p.median_window2) == (1, 5, 0, 0)
@@ -82,7 +82,6 @@ def _with(**kw):
     (dict(log_size=(5, 9)), lfe.LFE_EUNSUPPORTED),
     (dict(log_size=(1, 5)), lfe.LFE_EUNSUPPORTED),
     (dict(zc_threshold=(-0.1, 0.0)), lfe.LFE_EINVAL),
-    (dict(std_source=2), lfe.LFE_EINVAL),
     (dict(std_window=4), lfe.LFE_EINVAL),
     (dict(std_window=9), lfe.LFE_EUNSUPPORTED),
     (dict(std_threshold=(-1.0, 0.3)), lfe.LFE_EINVAL),
@@ -92,6 +91,10 @@ def _with(**kw):
     (dict(median_window=11), lfe.LFE_EUNSUPPORTED),
     (dict(out_mode=3), lfe.LFE_EINVAL),
     (dict(adaptive=4), lfe.LFE_EINVAL),
+    (dict(mask_mode=2), lfe.LFE_EINVAL),
+    (dict(reserved1=1), lfe.LFE_EINVAL),
+    (dict(std_source=4), lfe.LFE_EINVAL),
+    (dict(mask_mode=1, adaptive=1), lfe.LFE_EINVAL),  # adaptive ZC is defined on integer responses
     (dict(adaptive=2), lfe.LFE_EINVAL),  # LFE_ADAPT_STD needs the intensity source
     (dict(median_window2=4), lfe.LFE_EINVAL),
     (dict(median_window2=-3), lfe.LFE_EINVAL),

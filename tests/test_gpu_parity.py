@@ -7,6 +7,7 @@ import itertools
 
 import numpy as np
 import pytest
+import scipy.ndimage as ndi
 
 import oracle as O
 from paper_1304_3992_b200 import lfe, scenes
@@ -29,7 +30,7 @@ def _oparams(p: lfe.Params) -> O.Params:
                     std_source=p.std_source, std_window=p.std_window,
                     std_threshold=tuple(p.std_threshold), std3_threshold=tuple(p.std3_threshold),
                     hybrid_median=p.hybrid_median, median_window=p.median_window, out_mode=p.out_mode,
-                    median_window2=p.median_window2, adaptive=p.adaptive)
+                    median_window2=p.median_window2, adaptive=p.adaptive, mask_mode=p.mask_mode)
 
 
 def _pitched(shape, dtype):
@@ -504,3 +505,152 @@ def test_adaptive_c3_full_size_sampled():
         lo, hi = max(0, a - 8), min(H, b + 8)
         ref = O.run(np.ascontiguousarray(img[lo:hi]), op)
         assert_same(got[a:b], ref[a - lo:a - lo + (b - a)], f"rows {a}:{b}")
+
+
+# ------------------------------ F32 masks (tolerance contract) and response std (NEXT-3) ----
+def _f32_exempt(img, p: lfe.Params, res):
+    """R23 / SURVEY C19: the near-tie set of the ORACLE's double responses, box-
+    dilated by the radius of everything downstream (std + median levels)."""
+    near = np.zeros(img.shape, bool)
+    L = p.std_window * p.std_window
+    for j in range(2):
+        r, t = res.r[j], p.zc_threshold[j]
+        near |= np.abs(np.abs(r) - 1e-4) < 1e-5
+        P = np.pad(r, 1, mode="edge")
+        nbs = [P[:-2, 1:-1], P[2:, 1:-1], P[1:-1, :-2], P[1:-1, 2:]]
+        for nb in nbs:
+            opp = np.sign(r) * np.sign(nb) < 0
+            tie = opp & ((np.abs(np.abs(r) - np.abs(nb)) < 1e-5) | (np.abs(np.abs(r) + np.abs(nb) - t) < 1e-5))
+            near |= tie
+        mx, mn = np.maximum.reduce(nbs), np.minimum.reduce(nbs)
+        near |= (r == 0) & (mx > 0) & (mn < 0) & (np.abs(mx - mn - t) < 1e-5)
+        if p.std_source >= lfe.LFE_STD_RESPONSE:  # std margin |s - T| < 1e-4 T at crossings
+            a = r * res.z[j] if p.std_source == lfe.LFE_STD_RESPONSE_AT_ZC else r
+            k = p.std_window
+            s1 = ndi.uniform_filter(a, k, mode="nearest") * L
+            s2 = ndi.uniform_filter(a * a, k, mode="nearest") * L
+            s = np.sqrt(np.maximum(L * s2 - s1 * s1, 0) / (L * (L - 1)))
+            near |= (res.z[j] > 0) & (np.abs(s - p.std_threshold[j]) < 1e-4 * max(p.std_threshold[j], 1e-12) + 1e-9)
+    rad = p.std_window // 2 + (p.median_window // 2 + p.median_window2 // 2 if p.hybrid_median else 0)
+    return ndi.maximum_filter(near, size=2 * rad + 3, mode="nearest")  # +1: both ends of each pair
+
+
+def _f32_cases():
+    yield lfe.Params(bit_depth=8, mask_mode=lfe.LFE_MASK_F32, zc_threshold=(0.01, 0.01))
+    yield lfe.Params(bit_depth=10, mask_mode=lfe.LFE_MASK_F32, zc_threshold=(0.02, 0.005), out_mode=lfe.LFE_OUT_MASK,
+                     log_size=(3, 7))
+    yield lfe.Params(bit_depth=12, mask_mode=lfe.LFE_MASK_F32, std_source=lfe.LFE_STD_RESPONSE,
+                     std_threshold=(0.02, 0.01), zc_threshold=(0.01, 0.01))
+    yield lfe.Params(bit_depth=8, mask_mode=lfe.LFE_MASK_F32, std_source=lfe.LFE_STD_RESPONSE_AT_ZC,
+                     std_threshold=(0.01, 0.01), std3_threshold=(0.005, -1.0), median_window2=3)
+
+
+@pytest.mark.parametrize("ci", range(4))
+def test_f32_tolerance_contract(ci):
+    """F32 masks: the GPU's FP32 response agrees with the oracle's double one
+    within 1e-5 (scale sum|w|/c), and the output is exact outside the exemption
+    set (near ties, dilated).  Piecewise-constant test images are full of exact
+    ties (symmetric steps), so the exempt and mismatch fractions are bounded on
+    the noisy scenes only, where they are small."""
+    p = list(_f32_cases())[ci]
+    rng = np.random.default_rng(500 + ci)
+    scene = scenes.scene_c1(clean=False)[:256, :320] if p.bit_depth == 8 else scenes.scene_c3(size=320)[:256]
+    if p.bit_depth == 12:
+        scene = scene * 4
+    cases = [("scene", np.ascontiguousarray(scene).astype(np.uint8 if p.bit_depth <= 8 else np.uint16), True)]
+    cases += [(f"{H}x{W} {k}", scenes.random_image(rng, H, W, p.bit_depth, k), False) for (H, W), k in
+              [((37, 53), "mixed"), ((130, 257), "blocks"), ((64, 64), "mixed")]]
+    for name, img, natural in cases:
+        op = _oparams(p)
+        res = O.run(img, op, intermediates=True)
+        with lfe.Context(p) as ctx:
+            d = torch.from_numpy(img).cuda()
+            for j in range(2):
+                w, c = O.mask_f32(p.sigma[j], p.log_size[j])
+                rg = ctx.test_response(d, j).cpu().numpy().astype(np.float64)
+                bound = 1e-5 * np.abs(w).sum() / c
+                diff = np.abs(rg - res.r[j])
+                snap = np.abs(np.abs(res.r[j]) - 1e-4) < 1e-5
+                assert np.all((diff <= bound) | snap), (name, j, float(diff[~snap].max()), bound)
+        got = run_gpu(img, p)
+        ex = _f32_exempt(img, p, res)
+        mism = got != res.out
+        bad = mism & ~ex
+        assert not bad.any(), f"{name}: {int(bad.sum())} non-exempt mismatches, first at {np.argwhere(bad)[0]}"
+        print(f"F32 case {ci} {name}: exempt {ex.mean():.4f}, mismatching {mism.mean():.5f}")
+        if natural:
+            # the exemption set is conservative (every near tie, dilated by the 9x9-11x11
+            # dependency box); what actually differs is tiny
+            assert mism.mean() < 0.002 and ex.mean() < 0.75, (name, mism.mean(), ex.mean())
+
+
+def test_int_response_is_exact():
+    """The general kernel's integer LoG (lfe_test_response) equals the oracle's."""
+    rng = np.random.default_rng(510)
+    for b, ls in [(8, (5, 5)), (10, (3, 7)), (16, (7, 3))]:
+        img = scenes.random_image(rng, 45, 67, b)
+        p = lfe.Params(bit_depth=b, log_size=ls)
+        with lfe.Context(p) as ctx:
+            d = torch.from_numpy(img).cuda()
+            for j in range(2):
+                q, _ = O.mask_int(p.sigma[j], ls[j], b)
+                assert np.array_equal(ctx.test_response(d, j).cpu().numpy(), O.log_response(img, q))
+
+
+def _resp_cases():
+    yield lfe.Params(bit_depth=8, std_source=lfe.LFE_STD_RESPONSE, std_threshold=(0.05, 0.02), zc_threshold=(0.01, 0.0))
+    yield lfe.Params(bit_depth=10, std_source=lfe.LFE_STD_RESPONSE_AT_ZC, std_threshold=(0.01, 0.004),
+                     std3_threshold=(0.02, -1.0), out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=12, std_source=lfe.LFE_STD_RESPONSE, std_threshold=(0.01, 0.01), std_window=7,
+                     log_size=(7, 5), median_window2=5)
+
+
+@pytest.mark.parametrize("ci", range(3))
+def test_response_std_sources_exact(ci):
+    """SPEC.md:236's signed-response std gate (R24), integer masks: bit-exact."""
+    p = list(_resp_cases())[ci]
+    rng = np.random.default_rng(520 + ci)
+    for (H, W), kind in itertools.product(SHAPES, ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, p.bit_depth, kind)
+        assert_same(run_gpu(img, p), O.run(img, _oparams(p)), f"{H}x{W} {kind}")
+    img = scenes.scene_c1(clean=False) if p.bit_depth == 8 else scenes.scene_c3(size=300)
+    if img.dtype == np.uint8 or p.bit_depth >= 10:
+        assert_same(run_gpu(img, p), O.run(img, _oparams(p)), "scene")
+
+
+# -------------------------------------------------------- launch mechanics ----
+def test_extract_is_cuda_graph_capturable():
+    """lfe_extract enqueues only kernel launches after its first call, so it can
+    be captured into a CUDA graph (c1/c2-size scenes are launch-bound)."""
+    img = scenes.scene_c1(clean=False)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.01, 0.01))
+    want = O.run(img, _oparams(p))
+    with lfe.Context(p) as ctx:
+        d = torch.from_numpy(img).cuda()
+        out = torch.empty_like(d)
+        ctx.extract(d, out)  # first call: one-time attribute / occupancy queries
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ctx.extract(d, out)
+        out.zero_()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        ctx.check()
+        assert_same(out.cpu().numpy(), want, "graph replay")
+
+
+def test_c5_full_size_streamed_sampled():
+    """c5: the 48000 x 48000 u16 mosaic (4.6 GB) streamed from host memory through
+    lfe_extract_host; the oracle checks row bands at the image edges and across
+    the mosaic's tile seams."""
+    T = 12000
+    img = np.empty((4 * T, 4 * T), np.uint16)
+    for i in range(16):
+        img[(i // 4) * T:(i // 4 + 1) * T, (i % 4) * T:(i % 4 + 1) * T] = scenes.scene_c5_tile(i, T)
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, 2048)
+        got = ctx.extract_host(img)
+    _sampled_rows(img, p, got, [(0, 12), (11994, 12006), (23990, 24010), (47988, 48000)])

@@ -157,6 +157,8 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b)
 }
 
 // median of three packed pairs: min3 / max3, then the remaining element by XOR
+// (measured: the IADD3 form a + b + c - lo - hi, which moves the two LOP3 to the
+// FMA-lite pipe, is 0.5% slower on c3)
 __device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c)
 {
     uint32_t lo = vmin2(vmin2(a, b), c), hi = vmax2(vmax2(a, b), c);
@@ -1138,6 +1140,7 @@ bool fused_supports(const KParams &kp, int bit_depth)
     (void)bit_depth;
     if (kp.n[0] != 5 || kp.n[1] != 5) return false;
     if (kp.std_source != LFE_STD_ZC || kp.w != 5) return false;
+    if (kp.f32) return false;  // float masks (R23): general kernel only
     if (kp.recheck[0] || kp.recheck[1]) return false;
     if (kp.hm && kp.m != 5) return false;
     if (kp.m2 && !(kp.hm && kp.m == 5 && kp.m2 == 3)) return false;

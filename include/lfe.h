@@ -75,7 +75,7 @@ typedef struct lfe_params {
     int32_t bit_depth;          /* 1..16                                                 */
     double sigma[2];            /* Eq. 1 sigma (> 0, finite)                              */
     int32_t sigma_is_variance;  /* 0: sigma used directly (R1); 1: sigma = sqrt(value)    */
-    int32_t log_size[2];        /* odd mask side: 3, 5 or 7 (paper: 5)       */
+    int32_t log_size[2];        /* odd mask side: 3, 5, 7 or 9 (paper: 5)    */
     int32_t adaptive;           /* 0, or LFE_ADAPT_* flags (see lfe_stats below):         */
                                 /*  ZC:  zc_threshold[j] is k_j and the gap threshold is  */
                                 /*       t_j = ceil(k_j * sigma(r_j)) (R21)               */
@@ -131,6 +131,19 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out);
  * lfe_last_async_error); the output is then unspecified. */
 lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
                        int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
+
+/* Several independent bands of one scene in ONE launch (band-sequential
+ * planes, e.g. a multispectral scene run "on a single band" each, PAPER.md:28,
+ * :82; NEXT-4).  Band b's input is the W x H image at d_in + b *
+ * in_band_stride_bytes, its output at d_out + b * out_band_stride_bytes; every
+ * band is processed exactly as lfe_extract would (each pads at its own
+ * borders).  bands in 1..65535; band strides >= one band's span; 16-byte
+ * aligned strides keep the fused kernel eligible.  Adaptive contexts:
+ * EUNSUPPORTED (their statistics are per image).  Errors as lfe_extract. */
+lfe_status lfe_extract_bands(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes,
+                             int64_t in_band_stride_bytes, int32_t width, int32_t height, int32_t bands,
+                             void *d_out, int64_t out_pitch_bytes, int64_t out_band_stride_bytes,
+                             void *cuda_stream);
 
 /* One row strip of a larger image (multi-GPU sharding, streaming).  An
  * adaptive ctx needs whole-image statistics first (lfe_set_stats).  d_in_row0
@@ -198,7 +211,7 @@ lfe_status lfe_get_thresholds(const lfe_ctx *c, int64_t *zc_t, double *std_T, do
 int32_t lfe_halo(const lfe_ctx *c);
 
 /* The integer mask of branch 0/1 (R3): coeffs[n*n] row-major (caller buffer
- * of >= 49 int32), *n the side, *shift_F the quantisation shift and
+ * of >= 81 int32), *n the side, *shift_F the quantisation shift and
  * *zc_t the gap threshold in integer response units.  Any out pointer may be
  * NULL.  Errors: EINVAL. */
 lfe_status lfe_get_mask(const lfe_ctx *c, int32_t branch, int32_t *coeffs, int32_t *n,

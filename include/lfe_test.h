@@ -14,7 +14,7 @@ extern "C" {
 
 /* The library's own integer-mask synthesis (reading R3 of DESIGN.md: Eq. 1,
  * PAPER.md:50, DC-corrected and quantised) without a device: q[n*n]
- * row-major, *shift_F.  Errors: EINVAL (sigma <= 0, n not odd 1..7, bit depth
+ * row-major, *shift_F.  Errors: EINVAL (sigma <= 0, n not odd 1..9, bit depth
  * not 1..16). */
 lfe_status lfe_test_mask(double sigma, int32_t n, int32_t bit_depth, int32_t *q, int32_t *shift_F);
 

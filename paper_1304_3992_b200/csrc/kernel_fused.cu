@@ -77,6 +77,8 @@ struct FusedArgs {
     int W, H;               // virtual image
     int o0, o1;             // output rows
     int col_groups;
+    int nbands;             // independent bands (NEXT-4): units are (band, column group, row)
+    long long out_band_stride;
     int cap;                // max rows per piece (0 = whole contiguous range; tuning/tests)
     int nb;                 // > 0: CTA b owns units [bounds[b], bounds[b+1]) (cost-weighted partition)
     int bounds[kMaxGrid + 1];
@@ -126,12 +128,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar)
+// (x, row, band) box of the 3-D tensor map [bands][rows][row elements]
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
 {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
             smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -282,7 +285,7 @@ __device__ __forceinline__ void fix_pairs(const Fix &f, uint32_t &p0, uint32_t &
 // `cap` rows when the tuning option sets one.  Every CTA gets the same number
 // of rows +-1 and pays the pipeline warm-up once per piece.
 struct Item {
-    int ys, ye, plo, phi, xo, nst;
+    int ys, ye, plo, phi, xo, nst, band;
 };
 
 struct Pieces {
@@ -294,7 +297,7 @@ struct Pieces {
             u1 = a.bounds[blockIdx.x + 1];
             return;
         }
-        const long long U = (long long)a.col_groups * (a.o1 - a.o0);
+        const long long U = (long long)a.nbands * a.col_groups * (a.o1 - a.o0);
         u = U * blockIdx.x / gridDim.x;
         u1 = U * (blockIdx.x + 1) / gridDim.x;
     }
@@ -303,7 +306,8 @@ struct Pieces {
     {
         if (u >= u1) return false;
         const int R = a.o1 - a.o0;
-        const int cg = (int)(u / R), r0 = (int)(u - (long long)cg * R);
+        const int bg = (int)(u / R), r0 = (int)(u - (long long)bg * R);
+        const int band = bg / a.col_groups, cg = bg - band * a.col_groups;
         int n = (int)min((long long)(R - r0), u1 - u);
         if (a.cap > 0) n = min(n, a.cap);
         // keep the rows within kEdge of the virtual top/bottom in pieces of their
@@ -315,6 +319,7 @@ struct Pieces {
         it.ys = a.o0 + r0;
         it.ye = it.ys + n;
         it.xo = cg * kCtaOut;
+        it.band = band;
         it.plo = max(0, it.ys - kHalo);
         it.phi = min(a.H, it.ye + kHalo);
         it.nst = (it.phi - it.plo + kR - 1) / kR;
@@ -356,9 +361,10 @@ struct Producer {
 #pragma unroll
             for (int b = 0; b < kNBox; ++b) {
                 if constexpr (IN16)
-                    tma_load_2d(dst + b * kBoxBytes, map, it.xo - kHaloX + b * kBoxCols, y, &full[slot]);
+                    tma_load_3d(dst + b * kBoxBytes, map, it.xo - kHaloX + b * kBoxCols, y, it.band, &full[slot]);
                 else
-                    tma_load_2d(dst + b * kBoxBytes, map, (it.xo - 2 * kHaloX + b * kBoxCols) / 2, y, &full[slot]);
+                    tma_load_3d(dst + b * kBoxBytes, map, (it.xo - 2 * kHaloX + b * kBoxCols) / 2, y, it.band,
+                                &full[slot]);
             }
             ++g;
             if (++k == it.nst) have = false;
@@ -464,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     auto store = [&](int row, uint32_t o0, uint32_t o1) {
         if (lane < 2 || lane >= 30) return;
-        char *orow = reinterpret_cast<char *>(a.out) + (long long)(row - a.o0) * a.out_pitch;
+        char *orow = reinterpret_cast<char *>(a.out) + it.band * a.out_band_stride + (long long)(row - a.o0) * a.out_pitch;
         if (IN16 && !MASKOUT) {
             if (x0 + 3 < W) {
                 *reinterpret_cast<uint2 *>(orow + 2LL * x0) = make_uint2(o0, o1);
@@ -1029,7 +1035,7 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo)
     double c = 0.0;
     long long u = u0;
     while (u < u1) {
-        const int g = (int)(u / R), r0 = (int)(u - (long long)g * R);
+        const int bg = (int)(u / R), r0 = (int)(u - (long long)bg * R), g = bg % G;
         const int n = (int)std::min<long long>(R - r0, u1 - u);
         const double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kEdgeCol) : 1.0;
         int ys = fa.o0 + r0;
@@ -1050,7 +1056,7 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo)
 // CTAs needed when no CTA may exceed cost `cap` (filling bounds when given)
 int fill(const FusedArgs &fa, double cap, int halo, int grid, int *bounds)
 {
-    const long long U = (long long)fa.col_groups * (fa.o1 - fa.o0);
+    const long long U = (long long)fa.nbands * fa.col_groups * (fa.o1 - fa.o0);
     long long u = 0;
     int b = 0;
     if (bounds) bounds[0] = 0;
@@ -1073,7 +1079,7 @@ int fill(const FusedArgs &fa, double cap, int halo, int grid, int *bounds)
 
 void weighted_partition(FusedArgs &fa, int grid, int halo)
 {
-    const long long U = (long long)fa.col_groups * (fa.o1 - fa.o0);
+    const long long U = (long long)fa.nbands * fa.col_groups * (fa.o1 - fa.o0);
     fa.nb = 0;
     if (grid > kMaxGrid || grid < 2 || fa.cap > 0 || U >= (1LL << 31) || U < 4LL * grid) return;
     double lo = part::cost(fa, 0, U, halo) / grid, hi = part::cost(fa, 0, U, halo);
@@ -1105,7 +1111,7 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads, smem);
         grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     }
-    const long long units = (long long)fa.col_groups * (fa.o1 - fa.o0);
+    const long long units = (long long)fa.nbands * fa.col_groups * (fa.o1 - fa.o0);
     const int grid = units < grid_cap ? (int)units : grid_cap;
     cudaError_t e = cudaSuccess;
     FusedArgs fw = fa;
@@ -1176,6 +1182,8 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     fa.o0 = g.o0;
     fa.o1 = g.o1;
     fa.col_groups = (g.width + kCtaOut - 1) / kCtaOut;
+    fa.nbands = g.bands;
+    fa.out_band_stride = g.out_band_stride;
     fa.cap = tile_h > 0 ? tile_h : 0;
     fa.out = g.out;
     fa.out_pitch = g.out_pitch;
@@ -1186,11 +1194,13 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     CUtensorMap map;
     // u8 rows are fetched as u16 pairs (the row pitch is a multiple of 16 bytes,
     // so the pair holding an odd last pixel stays inside the row)
-    const cuuint64_t dims[2] = {(cuuint64_t)(in16 ? g.width : (g.width + 1) / 2), (cuuint64_t)g.Hv};
-    const cuuint64_t strides[1] = {(cuuint64_t)g.in_pitch};
-    const cuuint32_t box[2] = {(cuuint32_t)(in16 ? 232 : 240), (cuuint32_t)kR};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void *>(g.in), dims, strides, box,
+    const cuuint64_t dims[3] = {(cuuint64_t)(in16 ? g.width : (g.width + 1) / 2), (cuuint64_t)g.Hv,
+                                (cuuint64_t)g.bands};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.in_pitch,
+                                   (cuuint64_t)(g.bands > 1 ? g.in_band_stride : g.in_pitch * (int64_t)g.Hv)};
+    const cuuint32_t box[3] = {(cuuint32_t)(in16 ? 232 : 240), (cuuint32_t)kR, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(g.in), dims, strides, box,
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;

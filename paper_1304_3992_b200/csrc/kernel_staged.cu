@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(kThreads)
     const int W = g.width, Hv = g.Hv;
     const int x0 = blockIdx.x * TW;
     const int y0 = g.o0 + blockIdx.y * TH;
+    // band blockIdx.z of a band-sequential scene (NEXT-4); bands = 1 otherwise
+    const char *g_in = reinterpret_cast<const char *>(g.in) + (int64_t)blockIdx.z * g.in_band_stride;
+    char *g_out = reinterpret_cast<char *>(g.out) + (int64_t)blockIdx.z * g.out_band_stride;
     const int h = kp.halo;
     const int hr = h - kp.RL;      // LoG-response halo
     const int hz = hr - 1;         // ZC halo (= Rs + Rm)
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int i = threadIdx.x; i < RI.h * RI.w; i += kThreads) {
         int vy = clampi(RI.oy + i / RI.w, 0, Hv - 1);
         int vx = clampi(RI.ox + i % RI.w, 0, W - 1);
-        const Tin *row = reinterpret_cast<const Tin *>(reinterpret_cast<const char *>(g.in) + (int64_t)vy * g.in_pitch);
+        const Tin *row = reinterpret_cast<const Tin *>(g_in + (int64_t)vy * g.in_pitch);
         uint32_t v = row[vx];
         bad |= v > (uint32_t)kp.maxv;
         sI[i] = (uint16_t)v;
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(kThreads)
         } else {
             o = sE[RE.idx(vy, vx)];
         }
-        char *orow = reinterpret_cast<char *>(g.out) + (int64_t)(vy - g.o0) * g.out_pitch;
+        char *orow = g_out + (int64_t)(vy - g.o0) * g.out_pitch;
         if (kp.out_mode == LFE_OUT_MASK)
             reinterpret_cast<uint8_t *>(orow)[vx] = (uint8_t)o;
         else
@@ -420,8 +423,8 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
     int TH = tile_h > 0 ? tile_h : 32;
     size_t smem = staged_smem(kp, TW, TH);
     if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;  // tile too large for this halo
-    dim3 grid((g.width + TW - 1) / TW, (g.o1 - g.o0 + TH - 1) / TH);
-    if (grid.y == 0 || grid.x == 0) return cudaSuccess;
+    dim3 grid((g.width + TW - 1) / TW, (g.o1 - g.o0 + TH - 1) / TH, g.bands);
+    if (grid.y == 0 || grid.x == 0 || grid.z == 0) return cudaSuccess;
     if (in16) {
         cudaFuncSetAttribute(staged_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         staged_kernel<uint16_t><<<grid, kThreads, smem, s>>>(kp, g, TW, TH, err_flag);

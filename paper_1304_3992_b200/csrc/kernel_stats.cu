@@ -4,9 +4,10 @@
 // readings R21, R22 in DESIGN.md).
 //
 // One persistent grid walks the output rows [o0, o1) of a virtual image in
-// 16 x 128 tiles.  Each tile plus the LoG radius is staged in shared memory
+// 32 x 128 tiles.  Each tile plus the LoG radius is staged in shared memory
 // with clamped (edge-replicated, R5) coordinates, both integer LoG responses
-// r_j are evaluated exactly (int32, |r| < 2^24 by R3), and every thread keeps
+// r_j are evaluated exactly (int32, |r| < 2^24 by R3) by per-column streaming
+// over the rows (symmetric pair sums, per-offset row partials), and every thread keeps
 // exact integer sums: n, sum r_j, sum r_j^2 split as (r^2 >> 24, r^2 & 2^24-1)
 // so that no 64-bit sum can overflow, sum I and sum I^2.  The block reduces them
 // and adds them to the caller's lfe_stats with 64-bit atomics -- integer sums,
@@ -19,9 +20,9 @@
 namespace lfe {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;  // one image column per thread
 constexpr int kTileW = 128;
-constexpr int kTileH = 16;
+constexpr int kTileH = 32;
 constexpr int kMaxR = kMaxMask / 2;
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -33,59 +34,95 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v)
     return v;
 }
 
-template <typename Tin>
+// R = the larger mask radius.  Each thread walks one column of a 32-row tile
+// down its rows: per input row it forms the symmetric pair sums
+// h_b = I(x-b) + I(x+b) (h_0 = I(x)), the per-offset row partials
+// p_a = sum_b q(a, b) h_b of each 8-fold symmetric mask (the smaller mask is
+// padded with zero coefficients), and streams them into the 2R+1 pending
+// output rows.  Every value is an exact int32 (|r| < 2^24, R3).
+template <typename Tin, int R>
 __global__ void __launch_bounds__(kThreads)
     stats_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, lfe_stats *out)
 {
     __shared__ uint16_t sI[(kTileH + 2 * kMaxR) * (kTileW + 2 * kMaxR)];
     __shared__ unsigned long long red[kThreads / 32][9];
-    const int W = g.width, Hv = g.Hv, RL = kp.RL;
-    const int TWh = kTileW + 2 * RL, THh = kTileH + 2 * RL;
+    constexpr int TWh = kTileW + 2 * R, THh = kTileH + 2 * R;
+    const int W = g.width, Hv = g.Hv;
     const int tiles_x = (W + kTileW - 1) / kTileW;
     const int rows = g.o1 - g.o0;
     const long long ntiles = (long long)tiles_x * ((rows + kTileH - 1) / kTileH);
 
+    // q(a, b) of both masks, a, b in 0..R (0 outside a smaller mask)
+    int32_t q[2][R + 1][R + 1];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int nj = kp.n[j], Rj = nj / 2;
+#pragma unroll
+        for (int a = 0; a <= R; ++a)
+#pragma unroll
+            for (int b = 0; b <= R; ++b) q[j][a][b] = (a <= Rj && b <= Rj) ? kp.q[j][(Rj + a) * nj + (Rj + b)] : 0;
+    }
+
     long long n = 0, rs0 = 0, rs1 = 0, is = 0;
     unsigned long long hi0 = 0, lo0 = 0, hi1 = 0, lo1 = 0, iq = 0;
+    const int lx = threadIdx.x;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int tx = (int)(t % tiles_x), ty = (int)(t / tiles_x);
         const int x0 = tx * kTileW, y0 = g.o0 + ty * kTileH;
         __syncthreads();  // previous tile's readers are done
         for (int i = threadIdx.x; i < THh * TWh; i += kThreads) {
-            const int vy = clampi(y0 - RL + i / TWh, 0, Hv - 1);
-            const int vx = clampi(x0 - RL + i % TWh, 0, W - 1);
+            const int vy = clampi(y0 - R + i / TWh, 0, Hv - 1);
+            const int vx = clampi(x0 - R + i % TWh, 0, W - 1);
             const Tin *row = reinterpret_cast<const Tin *>(reinterpret_cast<const char *>(g.in) + (int64_t)vy * g.in_pitch);
             sI[i] = (uint16_t)row[vx];
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kTileH * kTileW; i += kThreads) {
-            const int ly = i / kTileW, lx = i % kTileW;
-            const int vy = y0 + ly, vx = x0 + lx;
-            if (vy >= g.o1 || vx >= W) continue;
-            int32_t r[2];
+        const bool col_ok = x0 + lx < W;
+        int32_t acc[2][2 * R + 1];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k <= 2 * R; ++k) acc[j][k] = 0;
+        for (int i = 0; i < THh; ++i) {  // input row y0 - R + i
+            const uint16_t *sr = sI + i * TWh + lx + R;  // tile entries hold clamped values (R5)
+            int32_t h[R + 1];
+            h[0] = sr[0];
+#pragma unroll
+            for (int b = 1; b <= R; ++b) h[b] = (int32_t)sr[-b] + (int32_t)sr[b];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const int nj = kp.n[j], R = nj / 2;
-                int32_t acc = 0;
-                // tile entries hold the values at clamped coordinates, so the entry at
-                // the unclamped offset is the replicate-padded neighbour (R5)
-                for (int dy = -R; dy <= R; ++dy)
-                    for (int dx = -R; dx <= R; ++dx)
-                        acc += kp.q[j][(dy + R) * nj + (dx + R)] * (int32_t)sI[(ly + RL + dy) * TWh + lx + RL + dx];
-                r[j] = acc;
+#pragma unroll
+                for (int k = 0; k <= 2 * R; ++k) {  // pending output row y0 - 2R + i + k
+                    const int a = k < R ? R - k : k - R;
+                    int32_t pa = 0;
+#pragma unroll
+                    for (int b = 0; b <= R; ++b) pa += q[j][a][b] * h[b];
+                    acc[j][k] += pa;
+                }
             }
-            const uint32_t v = sI[(ly + RL) * TWh + lx + RL];
-            ++n;
-            rs0 += r[0];
-            rs1 += r[1];
-            const unsigned long long q0 = (unsigned long long)((long long)r[0] * r[0]);
-            const unsigned long long q1 = (unsigned long long)((long long)r[1] * r[1]);
-            hi0 += q0 >> 24;
-            lo0 += q0 & 0xFFFFFFull;
-            hi1 += q1 >> 24;
-            lo1 += q1 & 0xFFFFFFull;
-            is += v;
-            iq += (unsigned long long)v * v;
+            // acc[.][0] is complete: output row y0 - 2R + i
+            const int y = y0 - 2 * R + i;
+            if (i >= 2 * R && col_ok && y < g.o1) {
+                const int32_t r0 = acc[0][0], r1 = acc[1][0];
+                const uint32_t v = sI[(i - R) * TWh + lx + R];
+                ++n;
+                rs0 += r0;
+                rs1 += r1;
+                const unsigned long long s0 = (unsigned long long)((long long)r0 * r0);
+                const unsigned long long s1 = (unsigned long long)((long long)r1 * r1);
+                hi0 += s0 >> 24;
+                lo0 += s0 & 0xFFFFFFull;
+                hi1 += s1 >> 24;
+                lo1 += s1 & 0xFFFFFFull;
+                is += v;
+                iq += (unsigned long long)v * v;
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+#pragma unroll
+                for (int k = 0; k < 2 * R; ++k) acc[j][k] = acc[j][k + 1];
+                acc[j][2 * R] = 0;
+            }
         }
     }
     unsigned long long s[9] = {(unsigned long long)n,  (unsigned long long)rs0, (unsigned long long)rs1,
@@ -106,6 +143,18 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+template <typename Tin>
+cudaError_t launch_stats_t(const KParams &kp, const Geometry &g, lfe_stats *d_stats, int grid, cudaStream_t s)
+{
+    switch (kp.RL) {
+    case 1: stats_kernel<Tin, 1><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
+    case 2: stats_kernel<Tin, 2><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
+    case 3: stats_kernel<Tin, 3><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
+    default: stats_kernel<Tin, 4><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, cudaStream_t s)
@@ -120,12 +169,8 @@ cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_st
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
     }
-    const int grid = (int)(ntiles < 8LL * sms ? ntiles : 8LL * sms);
-    if (in16)
-        stats_kernel<uint16_t><<<grid, kThreads, 0, s>>>(kp, g, d_stats);
-    else
-        stats_kernel<uint8_t><<<grid, kThreads, 0, s>>>(kp, g, d_stats);
-    return cudaGetLastError();
+    const int grid = (int)(ntiles < 16LL * sms ? ntiles : 16LL * sms);
+    return in16 ? launch_stats_t<uint16_t>(kp, g, d_stats, grid, s) : launch_stats_t<uint8_t>(kp, g, d_stats, grid, s);
 }
 
 }  // namespace lfe

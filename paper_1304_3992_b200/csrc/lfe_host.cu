@@ -121,7 +121,7 @@ lfe_status validate(const lfe_params *p)
             return fail(LFE_EINVAL, "sigma[%d] must be finite and > 0", j);
         if (p->log_size[j] < 1 || !(p->log_size[j] & 1)) return fail(LFE_EINVAL, "log_size[%d] must be odd", j);
         if (!odd_in(p->log_size[j], 3, kMaxMask))
-            return fail(LFE_EUNSUPPORTED, "log_size[%d] = %d not in {3,5,7}", j, p->log_size[j]);
+            return fail(LFE_EUNSUPPORTED, "log_size[%d] = %d not in {3,5,7,9}", j, p->log_size[j]);
         if (!std::isfinite(p->zc_threshold[j]) || p->zc_threshold[j] < 0.0)
             return fail(LFE_EINVAL, "zc_threshold[%d] must be finite and >= 0", j);
         if (!std::isfinite(p->std_threshold[j]) || p->std_threshold[j] < 0.0)
@@ -222,7 +222,8 @@ lfe_status run(lfe_ctx *c, const Geometry &g, cudaStream_t s)
     const bool in16 = c->p.bit_depth > 8;
     int k = c->cfg.kernel;
     const bool aligned = ((reinterpret_cast<uintptr_t>(g.in) | reinterpret_cast<uintptr_t>(g.out) |
-                           (uintptr_t)g.in_pitch | (uintptr_t)g.out_pitch) & 15u) == 0;
+                           (uintptr_t)g.in_pitch | (uintptr_t)g.out_pitch | (uintptr_t)g.in_band_stride |
+                           (uintptr_t)g.out_band_stride) & 15u) == 0;
     const bool fused_ok = aligned && fused_supports(c->kp, c->p.bit_depth);
     if (k == LFE_KERNEL_AUTO) k = fused_ok ? LFE_KERNEL_FUSED : LFE_KERNEL_STAGED;
     if (k == LFE_KERNEL_FUSED && !fused_ok)
@@ -533,6 +534,28 @@ lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W
     return run(c, g, (cudaStream_t)stream);
 }
 
+lfe_status lfe_extract_bands(lfe_ctx *c, const void *d_in, int64_t in_pitch, int64_t in_band_stride, int32_t W,
+                             int32_t H, int32_t bands, void *d_out, int64_t out_pitch, int64_t out_band_stride,
+                             void *stream)
+{
+    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
+    if (st != LFE_OK) return st;
+    if (bands < 1 || bands > 65535) return fail(LFE_EINVAL, "bands %d not in 1..65535", bands);
+    if (c->p.adaptive) return fail(LFE_EUNSUPPORTED, "adaptive thresholds are per image: call lfe_extract per band");
+    const int64_t in_span = (int64_t)(H - 1) * in_pitch + (int64_t)W * (int64_t)elem_in(c);
+    const int64_t out_span = (int64_t)(H - 1) * out_pitch + (int64_t)W * (int64_t)elem_out(c);
+    if (bands > 1 && (in_band_stride < in_span || out_band_stride < out_span))
+        return fail(LFE_EINVAL, "band strides smaller than one band");
+    if (in_band_stride % (int64_t)elem_in(c) || out_band_stride % (int64_t)elem_out(c))
+        return fail(LFE_EINVAL, "band stride not a multiple of the element size");
+    if (overlap(d_in, (size_t)((bands - 1) * in_band_stride + in_span), d_out,
+                (size_t)((bands - 1) * out_band_stride + out_span)))
+        return fail(LFE_EINVAL, "input and output overlap");
+    Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H, bands, bands > 1 ? in_band_stride : 0,
+               bands > 1 ? out_band_stride : 0};
+    return run(c, g, (cudaStream_t)stream);
+}
+
 lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
                             int32_t halo_above, int32_t halo_below, uint32_t edge_flags, void *d_out_row0,
                             int64_t out_pitch, void *stream)
@@ -661,7 +684,7 @@ lfe_status lfe_test_mask(double sigma, int32_t n, int32_t bit_depth, int32_t *q,
 {
     if (!q || !shift_F) return fail(LFE_EINVAL, "NULL output");
     if (!std::isfinite(sigma) || !(sigma > 0.0)) return fail(LFE_EINVAL, "sigma must be > 0");
-    if (!odd_in(n, 1, kMaxMask)) return fail(LFE_EINVAL, "n must be odd 1..7");
+    if (!odd_in(n, 1, kMaxMask)) return fail(LFE_EINVAL, "n must be odd 1..9");
     if (bit_depth < 1 || bit_depth > 16) return fail(LFE_EINVAL, "bit depth");
     int F = 0;
     if (!make_mask(sigma, n, bit_depth, q, &F)) return fail(LFE_EINVAL, "no quantisation");

@@ -9,7 +9,7 @@
 
 namespace lfe {
 
-constexpr int kMaxMask = 7;                 // largest compiled LoG side
+constexpr int kMaxMask = 9;                 // largest compiled LoG side (NEXT-4: 9x9)
 constexpr int kMaxMaskCoeffs = kMaxMask * kMaxMask;
 constexpr int kMaxStdWindow = 7;
 constexpr int kMaxMedianWindow = 7;
@@ -56,6 +56,11 @@ struct Geometry {
     int32_t width;
     int32_t Hv;
     int32_t o0, o1;
+    // independent bands of one scene (NEXT-4, band-sequential planes): band b's
+    // input / output start at in + b * in_band_stride / out + b * out_band_stride
+    int32_t bands = 1;
+    int64_t in_band_stride = 0;
+    int64_t out_band_stride = 0;
 };
 
 struct LaunchCfg {

@@ -83,7 +83,7 @@ _lib = None
 EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows", "lfe_extract_host",
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
            "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
-           "lfe_set_stats", "lfe_get_thresholds"]
+           "lfe_set_stats", "lfe_get_thresholds", "lfe_extract_bands"]
 TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response"]  # include/lfe_test.h
 
 
@@ -125,6 +125,8 @@ def load():
     L.lfe_last_message.restype = ctypes.c_char_p
     L.lfe_abi_version.argtypes = []
     L.lfe_abi_version.restype = I32
+    L.lfe_extract_bands.argtypes = [P, P, I64, I64, I32, I32, I32, P, I64, I64, P]
+    L.lfe_extract_bands.restype = st
     L.lfe_stats_rows.argtypes = [P, P, I64, I32, I32, I32, I32, U32, P, P]
     L.lfe_stats_rows.restype = st
     L.lfe_set_stats.argtypes = [P, ctypes.POINTER(lfe_stats)]
@@ -174,6 +176,12 @@ def lfe_extract_host(ctx, h_in: int, in_pitch: int, width: int, height: int, h_o
     _check(load().lfe_extract_host(ctx, h_in, in_pitch, width, height, h_out, out_pitch), "lfe_extract_host")
 
 
+def lfe_extract_bands(ctx, d_in: int, in_pitch: int, in_band_stride: int, width: int, height: int, bands: int,
+                      d_out: int, out_pitch: int, out_band_stride: int, stream: int = 0):
+    _check(load().lfe_extract_bands(ctx, d_in, in_pitch, in_band_stride, width, height, bands, d_out, out_pitch,
+                                    out_band_stride, stream), "lfe_extract_bands")
+
+
 def lfe_stats_rows(ctx, d_in_row0: int, in_pitch: int, width: int, rows: int, halo_above: int,
                    halo_below: int, edge_flags: int, d_stats: int, stream: int = 0):
     _check(load().lfe_stats_rows(ctx, d_in_row0, in_pitch, width, rows, halo_above, halo_below, edge_flags,
@@ -198,7 +206,7 @@ def lfe_halo(ctx) -> int:
 
 
 def lfe_get_mask(ctx, branch: int):
-    coeffs = (ctypes.c_int32 * 49)()
+    coeffs = (ctypes.c_int32 * 81)()
     n, F, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
     _check(load().lfe_get_mask(ctx, branch, coeffs, ctypes.byref(n), ctypes.byref(F), ctypes.byref(t)),
            "lfe_get_mask")
@@ -352,6 +360,21 @@ class Context:
         po, pout = self._torch_img(t_out, "output")
         H, W = t_in.shape
         lfe_extract(self.handle, pi, pin, W, H, po, pout, self._stream(stream))
+        return t_out
+
+    def extract_bands(self, t_in, t_out=None, stream=None):
+        """All bands of a [B, H, W] CUDA tensor in one launch (lfe_extract_bands)."""
+        import torch
+        if t_in.dim() != 3 or t_in.stride(2) != 1:
+            raise ValueError("input must be [bands, H, W] with unit column stride")
+        if t_out is None:
+            tout = torch.uint8 if self.params.out_mode == LFE_OUT_MASK else t_in.dtype
+            t_out = torch.empty(t_in.shape, dtype=tout, device=t_in.device)
+        self._check_dtype(t_in, t_out)
+        B, H, W = t_in.shape
+        e_in, e_out = t_in.element_size(), t_out.element_size()
+        lfe_extract_bands(self.handle, t_in.data_ptr(), t_in.stride(1) * e_in, t_in.stride(0) * e_in, W, H, B,
+                          t_out.data_ptr(), t_out.stride(1) * e_out, t_out.stride(0) * e_out, self._stream(stream))
         return t_out
 
     def extract_rows(self, t_in_full, row0: int, rows: int, halo_above: int, halo_below: int,

@@ -79,7 +79,7 @@ def _with(**kw):
     (dict(sigma=(float("nan"), 1.0)), lfe.LFE_EINVAL),
     (dict(sigma=(float("inf"), 1.0)), lfe.LFE_EINVAL),
     (dict(log_size=(4, 5)), lfe.LFE_EINVAL),
-    (dict(log_size=(5, 9)), lfe.LFE_EUNSUPPORTED),
+    (dict(log_size=(5, 11)), lfe.LFE_EUNSUPPORTED),
     (dict(log_size=(1, 5)), lfe.LFE_EUNSUPPORTED),
     (dict(zc_threshold=(-0.1, 0.0)), lfe.LFE_EINVAL),
     (dict(std_window=4), lfe.LFE_EINVAL),
@@ -126,7 +126,7 @@ def test_strerror():
 
 
 @pytest.mark.parametrize("sigma", [0.5, 0.7, math.sqrt(0.5), 1.0, 1.7, 4.0, math.sqrt(20), 20.0, 55.0])
-@pytest.mark.parametrize("n", [3, 5, 7])
+@pytest.mark.parametrize("n", [3, 5, 7, 9])
 @pytest.mark.parametrize("b", [1, 4, 8, 10, 12, 14, 16])
 def test_library_masks_equal_oracle_masks(sigma, n, b):
     """Two independent implementations of reading R3 agree exactly."""

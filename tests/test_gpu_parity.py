@@ -107,12 +107,15 @@ def _param_cases():
                      out_mode=lfe.LFE_OUT_MASK)
     yield lfe.Params(bit_depth=12, median_window=3, median_window2=5, std_source=lfe.LFE_STD_INTENSITY,
                      std_threshold=(40.0, 90.0))
+    # NEXT-4: 9x9 LoG with the largest std / median windows (halo 4 + 1 + 3 + 3 + 3 = 14)
+    yield lfe.Params(bit_depth=10, log_size=(9, 5), sigma=(1.5, 20.0), std_window=7, median_window=7,
+                     median_window2=7, zc_threshold=(0.01, 0.01))
 
 
 SHAPES = [(1, 1), (1, 17), (23, 1), (2, 2), (5, 7), (37, 53), (64, 64), (65, 129), (130, 257), (300, 200)]
 
 
-@pytest.mark.parametrize("ci", range(15))
+@pytest.mark.parametrize("ci", range(16))
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_random_images_param_sweep(ci, kernel):
     p = list(_param_cases())[ci]
@@ -141,7 +144,7 @@ def _sampled_rows(img, p, got, bands):
     """Compare rows [a, b) of a full-size GPU result with the oracle run on the
     band plus a halo of real rows (clamped only at the true image edge)."""
     H = img.shape[0]
-    halo = 3 + 1 + 3 + 3 + 3 + 1  # >= any configuration's halo (second median level included)
+    halo = 4 + 1 + 3 + 3 + 3 + 1  # >= any configuration's halo (9x9 LoG, second median level)
     for a, b in bands:
         lo, hi = max(0, a - halo), min(H, b + halo)
         ref = O.run(np.ascontiguousarray(img[lo:hi]), _oparams(p))
@@ -654,3 +657,42 @@ def test_c5_full_size_streamed_sampled():
         ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, 2048)
         got = ctx.extract_host(img)
     _sampled_rows(img, p, got, [(0, 12), (11994, 12006), (23990, 24010), (47988, 48000)])
+
+
+# ------------------------------------------------ multi-band scenes (NEXT-4) ----
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("bd,shape", [(8, (3, 37, 150)), (12, (4, 65, 1400)), (10, (2, 200, 2700))])
+def test_extract_bands_one_launch(kernel, bd, shape):
+    """lfe_extract_bands: every band of a [B, H, W] scene in one launch equals
+    the oracle on that band alone (each band pads at its own borders)."""
+    rng = np.random.default_rng(600 + bd)
+    B, H, W = shape
+    img = np.stack([scenes.random_image(rng, H, W, bd, "mixed" if b % 2 else "blocks") for b in range(B)])
+    p = lfe.Params(bit_depth=bd, zc_threshold=(0.01, 0.01), median_window2=3 if bd == 12 else 0)
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_KERNEL, kernel)
+        tin = torch.uint8 if bd <= 8 else torch.uint16
+        Wp = ((W * (1 if bd <= 8 else 2) + 15) // 16) * 16 // (1 if bd <= 8 else 2)
+        d = torch.zeros((B, H, Wp), dtype=tin, device="cuda")[:, :, :W]
+        d.copy_(torch.from_numpy(img))
+        out = torch.zeros((B, H, Wp), dtype=tin, device="cuda")[:, :, :W]
+        n0 = ctx.launches
+        ctx.extract_bands(d, out)
+        ctx.check()
+        assert ctx.launches == n0 + 1
+        got = out.cpu().numpy()
+    for b in range(B):
+        assert_same(got[b], O.run(img[b], _oparams(p)), f"band {b}")
+
+
+def test_c4_all_bands_one_launch_full_size_sampled():
+    """c4 at full size: 4 x 8192 x 8192 u16 (12-bit) bands in one lfe_extract_bands
+    call (fused kernel, 3-D tensor map), sampled rows of every band."""
+    img = scenes.scene_c4(size=8192)
+    p = lfe.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
+    with lfe.Context(p) as ctx:
+        d = torch.from_numpy(img).cuda()
+        got = ctx.extract_bands(d).cpu().numpy()
+        ctx.check()
+    for b in range(4):
+        _sampled_rows(img[b], p, got[b], [(0, 12), (4090 + b, 4106 + b), (8180, 8192)])

@@ -21,7 +21,7 @@ def timeit(p, n=20):
         e1.record()
         torch.cuda.synchronize()
         z = ctx.thresholds()[0]
-        return e0.elapsed_time(e1) / n, z, float((out > 0).float().mean())
+        return e0.elapsed_time(e1) / n, z, float((out.to(torch.int32) > 0).float().mean())
 
 
 pa = lfe.Params(bit_depth=10, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))

@@ -32,7 +32,7 @@ lfe_status fail(lfe_status s, const char *fmt, ...)
     return s;
 }
 
-constexpr int kHostBuffers = 2;
+constexpr int kHostBuffers = 3;
 
 }  // namespace
 
@@ -587,6 +587,14 @@ lfe_status lfe_last_async_error(lfe_ctx *c, void *stream)
     return LFE_OK;
 }
 
+// pitched copy; one contiguous copy when the rows are back to back on both sides
+static cudaError_t copy_rows(void *dst, size_t dpitch, const void *src, size_t spitch, size_t row_bytes, int rows,
+                             cudaMemcpyKind kind, cudaStream_t s)
+{
+    if (dpitch == spitch && spitch == row_bytes) return cudaMemcpyAsync(dst, src, row_bytes * (size_t)rows, kind, s);
+    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, kind, s);
+}
+
 static lfe_status host_prepare(lfe_ctx *c, size_t in_bytes, size_t out_bytes)
 {
     if (!c->st[0]) {
@@ -626,8 +634,10 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
     const int h = c->kp.halo;
     const int S = c->host_strip_rows < H ? c->host_strip_rows : H;
     const size_t ei = elem_in(c), eo = elem_out(c);
-    const size_t dpi = ((size_t)W * ei + 127) & ~(size_t)127;  // device pitches, 128-B aligned rows
-    const size_t dpo = ((size_t)W * eo + 127) & ~(size_t)127;
+    // device pitches: the host pitch when it is 16-byte aligned (each strip is then one
+    // contiguous copy), else the row bytes rounded up to 128
+    const size_t dpi = in_pitch % 16 == 0 ? (size_t)in_pitch : ((size_t)W * ei + 127) & ~(size_t)127;
+    const size_t dpo = out_pitch % 16 == 0 ? (size_t)out_pitch : ((size_t)W * eo + 127) & ~(size_t)127;
     st = host_prepare(c, dpi * (size_t)(S + 2 * h), dpo * (size_t)S);
     if (st != LFE_OK) return st;
     cudaStream_t sh = c->st[0], sc = c->st[1], sd = c->st[2];
@@ -641,8 +651,8 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
             const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
             const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
             if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);
-            cudaError_t e = cudaMemcpy2DAsync(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
-                                              in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
+            cudaError_t e = copy_rows(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
+                                      in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
             if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
             cudaEventRecord(c->ev_h2d[b], sh);
             cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
@@ -660,8 +670,8 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
         const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
         const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
         if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);  // input buffer free
-        cudaError_t e = cudaMemcpy2DAsync(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
-                                          in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
+        cudaError_t e = copy_rows(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
+                                  in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
         if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
         cudaEventRecord(c->ev_h2d[b], sh);
         cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
@@ -672,8 +682,8 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
         if (st != LFE_OK) return st;
         cudaEventRecord(c->ev_comp[b], sc);
         cudaStreamWaitEvent(sd, c->ev_comp[b], 0);
-        e = cudaMemcpy2DAsync(reinterpret_cast<char *>(h_out) + (int64_t)a0 * out_pitch, out_pitch, c->d_out[b], dpo,
-                              (size_t)W * eo, a1 - a0, cudaMemcpyDeviceToHost, sd);
+        e = copy_rows(reinterpret_cast<char *>(h_out) + (int64_t)a0 * out_pitch, out_pitch, c->d_out[b], dpo,
+                      (size_t)W * eo, a1 - a0, cudaMemcpyDeviceToHost, sd);
         if (e != cudaSuccess) return fail(LFE_ECUDA, "D2H: %s", cudaGetErrorString(e));
         cudaEventRecord(c->ev_d2h[b], sd);
     }

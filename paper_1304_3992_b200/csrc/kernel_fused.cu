@@ -80,7 +80,8 @@ struct FusedArgs {
     int nbands;             // independent bands (NEXT-4): units are (band, column group, row)
     long long out_band_stride;
     int cap;                // max rows per piece (0 = whole contiguous range; tuning/tests)
-    int nb;                 // > 0: CTA b owns units [bounds[b], bounds[b+1]) (cost-weighted partition)
+    int nb;                 // > 0: cost-weighted partition: CTA b owns units [bounds[b], bounds[b+1]),
+    int paired;             //      or (paired) CTAs 2k, 2k+1 share [bounds[k], bounds[k+1]) half by half
     int bounds[kMaxGrid + 1];
     void *out;
     long long out_pitch;
@@ -289,9 +290,24 @@ struct Item {
 };
 
 struct Pieces {
-    long long u, u1;
+    long long u, u1;    // unit cursor / end of this CTA's range (or of its CTA pair's range)
+    long long pu, pu1;  // this CTA's part of the current segment
+    int half;           // -1: a range of its own; 0/1: its half of every segment of a pair range
     __device__ __forceinline__ void init(const FusedArgs &a)
     {
+        pu = pu1 = 0;
+        half = -1;
+        if (a.nb > 0 && a.paired) {
+            // CTAs 2k and 2k+1 land on the two SMs of one TPC, which share the
+            // instruction cache: both take half of every segment of one range, so
+            // they run the same code path (interior / column edge / edge rows) at
+            // the same time instead of thrashing each other's hot loop.
+            const int pair = blockIdx.x >> 1;
+            u = a.bounds[pair];
+            u1 = a.bounds[pair + 1];
+            half = blockIdx.x & 1;
+            return;
+        }
         if (a.nb > 0) {
             u = a.bounds[blockIdx.x];
             u1 = a.bounds[blockIdx.x + 1];
@@ -304,18 +320,31 @@ struct Pieces {
     template <int kHalo>
     __device__ __forceinline__ bool next(const FusedArgs &a, Item &it)
     {
-        if (u >= u1) return false;
         const int R = a.o1 - a.o0;
-        const int bg = (int)(u / R), r0 = (int)(u - (long long)bg * R);
+        while (pu >= pu1) {  // next segment: one (band, column group), split at the edge rows
+            if (u >= u1) return false;
+            const int r0 = (int)(u - (u / R) * R);
+            int n = (int)min((long long)(R - r0), u1 - u);
+            // keep the rows within kEdge of the virtual top/bottom in segments of their
+            // own, so that only those short pieces take the row-clamping path
+            const int ys = a.o0 + r0;
+            if (ys < kEdge && ys + n > kEdge) n = kEdge - ys;
+            if (ys < a.H - kEdge && ys + n > a.H - kEdge) n = a.H - kEdge - ys;
+            if (half < 0) {
+                pu = u;
+                pu1 = u + n;
+            } else {
+                const long long mid = u + n / 2;
+                pu = half ? mid : u;
+                pu1 = half ? u + n : mid;
+            }
+            u += n;
+        }
+        const int bg = (int)(pu / R), r0 = (int)(pu - (long long)bg * R);
         const int band = bg / a.col_groups, cg = bg - band * a.col_groups;
-        int n = (int)min((long long)(R - r0), u1 - u);
+        int n = (int)(pu1 - pu);
         if (a.cap > 0) n = min(n, a.cap);
-        // keep the rows within kEdge of the virtual top/bottom in pieces of their
-        // own, so that only those short pieces take the row-clamping path
-        const int ys = a.o0 + r0;
-        if (ys < kEdge && ys + n > kEdge) n = kEdge - ys;
-        if (ys < a.H - kEdge && ys + n > a.H - kEdge) n = a.H - kEdge - ys;
-        u += n;
+        pu += n;
         it.ys = a.o0 + r0;
         it.ye = it.ys + n;
         it.xo = cg * kCtaOut;
@@ -1024,12 +1053,14 @@ bool interval_of(uint64_t lut, int L, int *lo, int *hi)
 // search on the per-CTA cost cap balances the CTAs.  Constants fitted to a
 // per-CTA globaltimer trace (LFE_DEBUG_TIMING, scripts/partition_fit.py).
 namespace part {
-constexpr double kPiece = 35.0;      // row-equivalents per piece (pipeline warm-up)
-constexpr double kEdgePiece = 17.0;  // extra for an edge-row piece (general path)
+constexpr double kPiece = 20.0;      // row-equivalents per piece (pipeline warm-up)
+constexpr double kEdgePiece = 0.0;   // extra for an edge-row piece (general path; ~0 once paired)
 constexpr double kEdgeCol = 1.066;   // column-edge group, cheap path (W % 4 == 0)
 constexpr double kEdgeColGen = 1.40; // column-edge group, general path
 
-double cost(const FusedArgs &fa, long long u0, long long u1, int halo)
+// per-CTA cost of units [u0, u1); `paired`: the cost of one CTA of a pair
+// sharing the range (half of every segment, every piece)
+double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool paired)
 {
     const int G = fa.col_groups, R = fa.o1 - fa.o0;
     double c = 0.0;
@@ -1045,7 +1076,8 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo)
             if (ys < kEdge && ye > kEdge) ye = kEdge;
             if (ys < fa.H - kEdge && ye > fa.H - kEdge) ye = fa.H - kEdge;
             const bool edge = ys - halo < 0 || ye + halo > fa.H;
-            c += f * ((ye - ys) + kPiece + (edge ? kEdgePiece : 0.0));
+            const int rows = paired ? (ye - ys + 1) / 2 : ye - ys;
+            c += f * (rows + kPiece + (edge ? kEdgePiece : 0.0));
             ys = ye;
         }
         u += n;
@@ -1054,7 +1086,7 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo)
 }
 
 // CTAs needed when no CTA may exceed cost `cap` (filling bounds when given)
-int fill(const FusedArgs &fa, double cap, int halo, int grid, int *bounds)
+int fill(const FusedArgs &fa, double cap, int halo, int grid, int *bounds, bool paired)
 {
     const long long U = (long long)fa.nbands * fa.col_groups * (fa.o1 - fa.o0);
     long long u = 0;
@@ -1065,7 +1097,7 @@ int fill(const FusedArgs &fa, double cap, int halo, int grid, int *bounds)
         long long lo = u + 1, hi = U;  // largest u1 with cost(u, u1) <= cap (at least one unit)
         while (lo < hi) {
             const long long mid = (lo + hi + 1) / 2;
-            if (cost(fa, u, mid, halo) <= cap) lo = mid; else hi = mid - 1;
+            if (cost(fa, u, mid, halo, paired) <= cap) lo = mid; else hi = mid - 1;
         }
         u = lo;
         ++b;
@@ -1081,13 +1113,19 @@ void weighted_partition(FusedArgs &fa, int grid, int halo)
 {
     const long long U = (long long)fa.nbands * fa.col_groups * (fa.o1 - fa.o0);
     fa.nb = 0;
+    fa.paired = 0;
     if (grid > kMaxGrid || grid < 2 || fa.cap > 0 || U >= (1LL << 31) || U < 4LL * grid) return;
-    double lo = part::cost(fa, 0, U, halo) / grid, hi = part::cost(fa, 0, U, halo);
+    const bool paired = (grid & 1) == 0;
+    const int bins = paired ? grid / 2 : grid;
+    double lo = part::cost(fa, 0, U, halo, paired) / bins, hi = part::cost(fa, 0, U, halo, paired);
     for (int it = 0; it < 40 && hi - lo > 0.5; ++it) {
         const double mid = 0.5 * (lo + hi);
-        if (part::fill(fa, mid, halo, grid, nullptr) <= grid) hi = mid; else lo = mid;
+        if (part::fill(fa, mid, halo, bins, nullptr, paired) <= bins) hi = mid; else lo = mid;
     }
-    if (part::fill(fa, hi, halo, grid, fa.bounds) <= grid) fa.nb = grid;
+    if (part::fill(fa, hi, halo, bins, fa.bounds, paired) <= bins) {
+        fa.nb = grid;
+        fa.paired = paired;
+    }
 }
 
 // The cost-weighted partition is a host-side binary search (~0.1-0.4 ms of CPU
@@ -1107,7 +1145,7 @@ void cached_partition(FusedArgs &fa, int grid, int halo)
 {
     struct Entry {
         PartKey key;
-        int nb;
+        int nb, paired;
         int bounds[kMaxGrid + 1];
     };
     constexpr int kEntries = 8;
@@ -1117,6 +1155,7 @@ void cached_partition(FusedArgs &fa, int grid, int halo)
     for (int i = 0; i < used; ++i)
         if (table[i].key == key) {
             fa.nb = table[i].nb;
+            fa.paired = table[i].paired;
             if (fa.nb > 0) std::copy(table[i].bounds, table[i].bounds + grid + 1, fa.bounds);
             return;
         }
@@ -1126,6 +1165,7 @@ void cached_partition(FusedArgs &fa, int grid, int halo)
     if (used < kEntries) ++used;
     e.key = key;
     e.nb = fa.nb;
+    e.paired = fa.paired;
     if (fa.nb > 0) std::copy(fa.bounds, fa.bounds + grid + 1, e.bounds);
 }
 

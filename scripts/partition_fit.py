@@ -1,8 +1,9 @@
 """Fit the partition cost model from a LFE_DEBUG_TIMING trace (per-CTA unit ranges included)."""
 import sys
 import numpy as np
-blocks = open(sys.argv[1]).read().strip().split('---')
-rows = [l.split() for l in blocks[0].strip().splitlines()]
+blocks = [b for b in open(sys.argv[1]).read().strip().split('---') if b.strip()]
+paired = '--paired' in sys.argv  # the trace's u0/u1 are CTA-pair ranges; each CTA does half of each segment
+rows = [l.split() for l in blocks[-1].strip().splitlines()]
 a = np.array([[int(v) for v in r] for r in rows], dtype=np.float64)
 dur = (a[:, 2] - a[:, 1]) / 1e3
 G, R, H = 9, 12000, 12000
@@ -17,8 +18,9 @@ for i in range(len(a)):
             ye = ye_all
             if ys < 16 and ye > 16: ye = 16
             if ys < H - 16 and ye > H - 16: ye = H - 16
-            if g in (0, G - 1): ecol += ye - ys
-            else: plain += ye - ys
+            nr = ((ye - ys) // 2 + (ye - ys) % 2 * (int(a[i, 0]) & 1)) if paired else ye - ys
+            if g in (0, G - 1): ecol += nr
+            else: plain += nr
             pieces += 1; edges += (ys - 7 < 0 or ye + 7 > H); ys = ye
         u += n
     X.append([plain, ecol, pieces, edges])

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "lfe.h"
@@ -665,27 +666,52 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
         st = resolve_from_device(c, sc);
         if (st != LFE_OK) return st;
     }
+    // LFE_DEBUG_HOST=<file>: per-strip event timeline of the three streams (debug only)
+    static const char *dbg_path = getenv("LFE_DEBUG_HOST");
+    cudaEvent_t dev[6 * 64 + 1];
+    const int ndbg = dbg_path && nstrips <= 64 ? nstrips : 0;
+    for (int k = 0; k < (ndbg ? 6 * ndbg + 1 : 0); ++k) cudaEventCreate(&dev[k]);
+    if (ndbg) cudaEventRecord(dev[6 * ndbg], sh);
     for (int i = 0; i < nstrips; ++i) {
         const int b = i % kHostBuffers;
         const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
         const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
         if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);  // input buffer free
+        if (ndbg) cudaEventRecord(dev[6 * i + 0], sh);
         cudaError_t e = copy_rows(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
                                   in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
         if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
+        if (ndbg) cudaEventRecord(dev[6 * i + 1], sh);
         cudaEventRecord(c->ev_h2d[b], sh);
         cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
         if (i >= kHostBuffers) cudaStreamWaitEvent(sc, c->ev_d2h[b], 0);   // output buffer free
+        if (ndbg) cudaEventRecord(dev[6 * i + 2], sc);
         const uint32_t flags = (lo == 0 ? LFE_TOP_IS_EDGE : 0u) | (hi == H ? LFE_BOTTOM_IS_EDGE : 0u);
         const char *row0 = reinterpret_cast<const char *>(c->d_in[b]) + (size_t)(a0 - lo) * dpi;
         st = lfe_extract_rows(c, row0, (int64_t)dpi, W, a1 - a0, a0 - lo, hi - a1, flags, c->d_out[b], (int64_t)dpo, sc);
         if (st != LFE_OK) return st;
+        if (ndbg) cudaEventRecord(dev[6 * i + 3], sc);
         cudaEventRecord(c->ev_comp[b], sc);
         cudaStreamWaitEvent(sd, c->ev_comp[b], 0);
+        if (ndbg) cudaEventRecord(dev[6 * i + 4], sd);
         e = copy_rows(reinterpret_cast<char *>(h_out) + (int64_t)a0 * out_pitch, out_pitch, c->d_out[b], dpo,
                       (size_t)W * eo, a1 - a0, cudaMemcpyDeviceToHost, sd);
         if (e != cudaSuccess) return fail(LFE_ECUDA, "D2H: %s", cudaGetErrorString(e));
+        if (ndbg) cudaEventRecord(dev[6 * i + 5], sd);
         cudaEventRecord(c->ev_d2h[b], sd);
+    }
+    if (ndbg) {
+        cudaDeviceSynchronize();
+        if (FILE *f = fopen(dbg_path, "a")) {
+            for (int i = 0; i < ndbg; ++i) {
+                float t[6];
+                for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&t[k], dev[6 * ndbg], dev[6 * i + k]);
+                fprintf(f, "%d h2d %.3f %.3f comp %.3f %.3f d2h %.3f %.3f\n", i, t[0], t[1], t[2], t[3], t[4], t[5]);
+            }
+            fprintf(f, "---\n");
+            fclose(f);
+        }
+        for (int k = 0; k < 6 * ndbg + 1; ++k) cudaEventDestroy(dev[k]);
     }
     return lfe_last_async_error(c, sd);
 }

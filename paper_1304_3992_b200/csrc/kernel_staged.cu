@@ -15,9 +15,11 @@
 //
 // Border semantics (reading R5): each stage pads ITS OWN input by replication.
 // Every shared-memory region entry (i, j) holds the stage value at the CLAMPED
-// virtual coordinate, and each stage reads its input at clamp(c + d); a halo
-// entry outside the image therefore equals the stage value at the image edge,
-// exactly as if that stage's input had been padded.
+// virtual coordinate.  A stage evaluates its element at the clamped centre c and
+// reads its input window at c + d WITHOUT clamping: the input region's entry at
+// an outside coordinate already holds the value at the image edge, exactly as
+// if that stage's input had been padded (each region extends its consumer's
+// by the consumer's radius, so c + d stays inside it).
 //
 // This kernel handles every supported parameter set (mask 3/5/7, std window
 // 3/5/7, median 3/5/7, both std sources, any bit depth).  kernel_fused.cu is
@@ -47,19 +49,16 @@ __device__ __forceinline__ void cswap(uint32_t &a, uint32_t &b)
     b = hi;
 }
 
-// median of n (odd, <= 13) values by an insertion sort (general path only)
-__device__ __forceinline__ uint32_t median_n(uint32_t *v, int n)
+// median of N (odd, compile-time) values: (N+1)/2 bubble passes move the
+// largest (N+1)/2 values to the top, all indices static (registers only)
+template <int N>
+__device__ __forceinline__ uint32_t median_static(uint32_t (&v)[N])
 {
-    for (int i = 1; i < n; ++i) {
-        uint32_t x = v[i];
-        int j = i - 1;
-        while (j >= 0 && v[j] > x) {
-            v[j + 1] = v[j];
-            --j;
-        }
-        v[j + 1] = x;
-    }
-    return v[n / 2];
+#pragma unroll
+    for (int p = 0; p <= N / 2; ++p)
+#pragma unroll
+        for (int i = 0; i < N - 1 - p; ++i) cswap(v[i], v[i + 1]);
+    return v[N / 2];
 }
 
 // LoG response of branch j at (cy, cx) from the replicate-padded input region
@@ -73,9 +72,9 @@ __device__ __forceinline__ int32_t log_at(const KParams &kp, int j, const uint16
     if (kp.f32) {
         float acc = 0.0f;
         for (int dy = -R; dy <= R; ++dy) {
-            const int yy = clampi(cy + dy, 0, Hv - 1);
+            const int yy = cy + dy;
             for (int dx = -R; dx <= R; ++dx) {
-                const int xx = clampi(cx + dx, 0, W - 1);
+                const int xx = cx + dx;
                 acc = fmaf(kp.wf[j][(dy + R) * n + (dx + R)], (float)sI[RI.idx(yy, xx)], acc);
             }
         }
@@ -85,9 +84,9 @@ __device__ __forceinline__ int32_t log_at(const KParams &kp, int j, const uint16
     }
     int32_t acc = 0;
     for (int dy = -R; dy <= R; ++dy) {
-        const int yy = clampi(cy + dy, 0, Hv - 1);
+        const int yy = cy + dy;
         for (int dx = -R; dx <= R; ++dx) {
-            const int xx = clampi(cx + dx, 0, W - 1);
+            const int xx = cx + dx;
             acc += kp.q[j][(dy + R) * n + (dx + R)] * (int32_t)sI[RI.idx(yy, xx)];
         }
     }
@@ -152,33 +151,39 @@ __device__ __forceinline__ int zc_rule_f32(float rp, const float (&nb)[4], float
 
 // Hybrid median of region S at (vy, vx) with radius R (R16, R17):
 // med3(median of the '+' group, median of the 'x' group, centre), both groups
-// including the centre; neighbours at clamped coordinates (R5).
-__device__ __forceinline__ uint32_t hybrid_median_at(const uint16_t *S, const Region &RS, int vy, int vx, int R,
-                                                     int W, int Hv)
+// including the centre.  The region's entries at outside coordinates hold the
+// edge values, so the neighbours are read unclamped (R5).
+template <int R>
+__device__ __forceinline__ uint32_t hybrid_median_r(const uint16_t *S, const Region &RS, int vy, int vx)
 {
-    uint32_t P[13], X[13];
-    int np = 0;
+    constexpr int N = 4 * R + 1;
+    uint32_t P[N], X[N];
     const uint32_t c = S[RS.idx(vy, vx)];
-    P[np] = c;
-    X[np] = c;
-    ++np;
+    P[0] = c;
+    X[0] = c;
+#pragma unroll
     for (int d = 1; d <= R; ++d) {
-        int ym = clampi(vy - d, 0, Hv - 1), yp = clampi(vy + d, 0, Hv - 1);
-        int xm = clampi(vx - d, 0, W - 1), xp = clampi(vx + d, 0, W - 1);
-        P[np] = S[RS.idx(vy, xm)];
-        X[np++] = S[RS.idx(ym, xm)];
-        P[np] = S[RS.idx(vy, xp)];
-        X[np++] = S[RS.idx(ym, xp)];
-        P[np] = S[RS.idx(ym, vx)];
-        X[np++] = S[RS.idx(yp, xm)];
-        P[np] = S[RS.idx(yp, vx)];
-        X[np++] = S[RS.idx(yp, xp)];
+        const int k = 4 * d - 3;
+        P[k] = S[RS.idx(vy, vx - d)];
+        P[k + 1] = S[RS.idx(vy, vx + d)];
+        P[k + 2] = S[RS.idx(vy - d, vx)];
+        P[k + 3] = S[RS.idx(vy + d, vx)];
+        X[k] = S[RS.idx(vy - d, vx - d)];
+        X[k + 1] = S[RS.idx(vy - d, vx + d)];
+        X[k + 2] = S[RS.idx(vy + d, vx - d)];
+        X[k + 3] = S[RS.idx(vy + d, vx + d)];
     }
-    uint32_t a = median_n(P, np), b = median_n(X, np), cc = c;
+    uint32_t a = median_static(P), b = median_static(X), cc = c;
     cswap(a, b);
     cswap(b, cc);
     cswap(a, b);
     return b;  // median of three
+}
+
+__device__ __forceinline__ uint32_t hybrid_median_at(const uint16_t *S, const Region &RS, int vy, int vx, int R)
+{
+    return R == 1 ? hybrid_median_r<1>(S, RS, vy, vx)
+                  : (R == 2 ? hybrid_median_r<2>(S, RS, vy, vx) : hybrid_median_r<3>(S, RS, vy, vx));
 }
 
 template <typename Tin>
@@ -240,8 +245,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int i = threadIdx.x; i < RZ.h * RZ.w; i += kThreads) {
         int cy = clampi(RZ.oy + i / RZ.w, 0, Hv - 1);
         int cx = clampi(RZ.ox + i % RZ.w, 0, W - 1);
-        int nbi[4] = {RR.idx(clampi(cy - 1, 0, Hv - 1), cx), RR.idx(clampi(cy + 1, 0, Hv - 1), cx),
-                      RR.idx(cy, clampi(cx - 1, 0, W - 1)), RR.idx(cy, clampi(cx + 1, 0, W - 1))};
+        int nbi[4] = {RR.idx(cy - 1, cx), RR.idx(cy + 1, cx), RR.idx(cy, cx - 1), RR.idx(cy, cx + 1)};
         int pi = RR.idx(cy, cx);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -275,9 +279,9 @@ __global__ void __launch_bounds__(kThreads)
             if (kp.std_source == LFE_STD_ZC) {
                 int k = 0, k3 = 0;
                 for (int dy = -Rs; dy <= Rs; ++dy) {
-                    int yy = clampi(cy + dy, 0, Hv - 1);
+                    int yy = cy + dy;
                     for (int dx = -Rs; dx <= Rs; ++dx) {
-                        int xx = clampi(cx + dx, 0, W - 1);
+                        int xx = cx + dx;
                         int zv = Z[RZ.idx(yy, xx)];
                         k += zv;
                         if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) k3 += zv;
@@ -294,9 +298,9 @@ __global__ void __launch_bounds__(kThreads)
                 if (kp.f32) {
                     double s1 = 0, s2 = 0, t1 = 0, t2 = 0;
                     for (int dy = -Rs; dy <= Rs; ++dy) {
-                        int yy = clampi(cy + dy, 0, Hv - 1);
+                        int yy = cy + dy;
                         for (int dx = -Rs; dx <= Rs; ++dx) {
-                            int xx = clampi(cx + dx, 0, W - 1);
+                            int xx = cx + dx;
                             double a = (at_zc && !Z[RZ.idx(yy, xx)]) ? 0.0 : (double)__int_as_float(r[RR.idx(yy, xx)]);
                             s1 += a;
                             s2 += a * a;
@@ -311,9 +315,9 @@ __global__ void __launch_bounds__(kThreads)
                 } else {
                     int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
                     for (int dy = -Rs; dy <= Rs; ++dy) {
-                        int yy = clampi(cy + dy, 0, Hv - 1);
+                        int yy = cy + dy;
                         for (int dx = -Rs; dx <= Rs; ++dx) {
-                            int xx = clampi(cx + dx, 0, W - 1);
+                            int xx = cx + dx;
                             int64_t a = (at_zc && !Z[RZ.idx(yy, xx)]) ? 0 : (int64_t)r[RR.idx(yy, xx)];
                             s1 += a;
                             s2 += a * a;
@@ -329,9 +333,9 @@ __global__ void __launch_bounds__(kThreads)
             } else {
                 int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
                 for (int dy = -Rs; dy <= Rs; ++dy) {
-                    int yy = clampi(cy + dy, 0, Hv - 1);
+                    int yy = cy + dy;
                     for (int dx = -Rs; dx <= Rs; ++dx) {
-                        int xx = clampi(cx + dx, 0, W - 1);
+                        int xx = cx + dx;
                         int64_t a = sI[RI.idx(yy, xx)];
                         s1 += a;
                         s2 += a * a;
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(kThreads)
         for (int i = threadIdx.x; i < RM.h * RM.w; i += kThreads) {
             int cy = clampi(RM.oy + i / RM.w, 0, Hv - 1);
             int cx = clampi(RM.ox + i % RM.w, 0, W - 1);
-            sM[i] = (uint16_t)hybrid_median_at(sE, RE, cy, cx, kp.Rm, W, Hv);
+            sM[i] = (uint16_t)hybrid_median_at(sE, RE, cy, cx, kp.Rm);
         }
         __syncthreads();
     }
@@ -370,9 +374,9 @@ __global__ void __launch_bounds__(kThreads)
         if (vy >= g.o1 || vx >= W) continue;
         uint32_t o;
         if (kp.m2) {
-            o = hybrid_median_at(sM, RM, vy, vx, kp.Rm2, W, Hv);
+            o = hybrid_median_at(sM, RM, vy, vx, kp.Rm2);
         } else if (kp.hm) {
-            o = hybrid_median_at(sE, RE, vy, vx, kp.Rm, W, Hv);
+            o = hybrid_median_at(sE, RE, vy, vx, kp.Rm);
         } else {
             o = sE[RE.idx(vy, vx)];
         }

@@ -61,36 +61,111 @@ __device__ __forceinline__ uint32_t median_static(uint32_t (&v)[N])
     return v[N / 2];
 }
 
-// LoG response of branch j at (cy, cx) from the replicate-padded input region
-// (R3-R5): int32 with integer masks, or -- F32 mode, R23 -- the
-// FP32 sum in row-major tap order times 1/(M c), |r^| < 1e-4 snapped to 0,
-// returned as its bit pattern.
-__device__ __forceinline__ int32_t log_at(const KParams &kp, int j, const uint16_t *sI, const Region &RI, int cy,
-                                          int cx, int W, int Hv)
+__device__ __forceinline__ uint32_t med3u(uint32_t a, uint32_t b, uint32_t c)
 {
-    const int n = kp.n[j], R = n / 2;
+    return max(min(a, b), min(max(a, b), c));
+}
+
+// N = 5: med3(max(min(a,b), min(c,d)), min(max(a,b), max(c,d)), e)
+template <>
+__device__ __forceinline__ uint32_t median_static<5>(uint32_t (&v)[5])
+{
+    return med3u(max(min(v[0], v[1]), min(v[2], v[3])), min(max(v[0], v[1]), max(v[2], v[3])), v[4]);
+}
+
+// N = 9: med3(max of the triples' minima, median of their medians, min of their maxima)
+template <>
+__device__ __forceinline__ uint32_t median_static<9>(uint32_t (&v)[9])
+{
+    uint32_t lo[3], md[3], hi[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const uint32_t a = v[3 * t], b = v[3 * t + 1], c = v[3 * t + 2];
+        lo[t] = min(min(a, b), c);
+        hi[t] = max(max(a, b), c);
+        md[t] = med3u(a, b, c);
+    }
+    return med3u(max(max(lo[0], lo[1]), lo[2]), med3u(md[0], md[1], md[2]), min(min(hi[0], hi[1]), hi[2]));
+}
+
+// LoG response of branch J (mask side N) at the region entry `base` (row width
+// w) from the replicate-padded input region (R3-R5): int32 with
+// integer masks, or -- F32 mode, R23 -- the FP32 sum in row-major tap order
+// times 1/(M c), |r^| < 1e-4 snapped to 0, returned as its bit pattern.  N and
+// J are compile-time so the taps unroll with immediate offsets.
+template <int N, int J>
+__device__ __forceinline__ int32_t log_n(const KParams &kp, const uint16_t *sI, int base, int w)
+{
+    constexpr int R = N / 2;
     if (kp.f32) {
         float acc = 0.0f;
+#pragma unroll
         for (int dy = -R; dy <= R; ++dy) {
-            const int yy = cy + dy;
-            for (int dx = -R; dx <= R; ++dx) {
-                const int xx = cx + dx;
-                acc = fmaf(kp.wf[j][(dy + R) * n + (dx + R)], (float)sI[RI.idx(yy, xx)], acc);
-            }
+            const uint16_t *row = sI + base + dy * w;
+#pragma unroll
+            for (int dx = -R; dx <= R; ++dx) acc = fmaf(kp.wf[J][(dy + R) * N + (dx + R)], (float)row[dx], acc);
         }
-        float v = acc * kp.fscale[j];
+        float v = acc * kp.fscale[J];
         if (fabsf(v) < 1e-4f) v = 0.0f;
         return __float_as_int(v);
     }
     int32_t acc = 0;
+#pragma unroll
     for (int dy = -R; dy <= R; ++dy) {
-        const int yy = cy + dy;
-        for (int dx = -R; dx <= R; ++dx) {
-            const int xx = cx + dx;
-            acc += kp.q[j][(dy + R) * n + (dx + R)] * (int32_t)sI[RI.idx(yy, xx)];
-        }
+        const uint16_t *row = sI + base + dy * w;
+#pragma unroll
+        for (int dx = -R; dx <= R; ++dx) acc += kp.q[J][(dy + R) * N + (dx + R)] * (int32_t)row[dx];
     }
     return acc;
+}
+
+template <int J>
+__device__ __forceinline__ int32_t log_j(const KParams &kp, const uint16_t *sI, int base, int w)
+{
+    switch (kp.n[J]) {
+    case 3: return log_n<3, J>(kp, sI, base, w);
+    case 5: return log_n<5, J>(kp, sI, base, w);
+    case 7: return log_n<7, J>(kp, sI, base, w);
+    default: return log_n<9, J>(kp, sI, base, w);
+    }
+}
+
+__device__ __forceinline__ int32_t log_at(const KParams &kp, int j, const uint16_t *sI, const Region &RI, int cy,
+                                          int cx)
+{
+    const int base = RI.idx(cy, cx);
+    return j == 0 ? log_j<0>(kp, sI, base, RI.w) : log_j<1>(kp, sI, base, RI.w);
+}
+
+// Eq. 2 window sums of the std gate over a (2RS+1)^2 window and its 3x3 core;
+// val(dy, dx) returns the window value at that offset.  Compile-time RS unrolls
+// the taps (immediate shared-memory offsets).
+template <int RS, typename T, typename F>
+__device__ __forceinline__ void window_sums(F val, T &s1, T &s2, T &t1, T &t2)
+{
+#pragma unroll
+    for (int dy = -RS; dy <= RS; ++dy)
+#pragma unroll
+        for (int dx = -RS; dx <= RS; ++dx) {
+            const T a = val(dy, dx);
+            s1 += a;
+            s2 += a * a;
+            if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
+                t1 += a;
+                t2 += a * a;
+            }
+        }
+}
+
+template <typename T, typename F>
+__device__ __forceinline__ void window_sums_rs(int RS, F val, T &s1, T &s2, T &t1, T &t2)
+{
+    if (RS == 1)
+        window_sums<1>(val, s1, s2, t1, t2);
+    else if (RS == 2)
+        window_sums<2>(val, s1, s2, t1, t2);
+    else
+        window_sums<3>(val, s1, s2, t1, t2);
 }
 
 // Rule R* (R6-R9) at pixel value rp with the four neighbours nb (integer units)
@@ -237,7 +312,7 @@ __global__ void __launch_bounds__(kThreads)
         int cy = clampi(RR.oy + i / RR.w, 0, Hv - 1);
         int cx = clampi(RR.ox + i % RR.w, 0, W - 1);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) sR[j * RR.h * RR.w + i] = log_at(kp, j, sI, RI, cy, cx, W, Hv);
+        for (int j = 0; j < 2; ++j) sR[j * RR.h * RR.w + i] = log_at(kp, j, sI, RI, cy, cx);
     }
     __syncthreads();
 
@@ -277,16 +352,8 @@ __global__ void __launch_bounds__(kThreads)
             const int Rs = kp.Rs;
             bool pass;
             if (kp.std_source == LFE_STD_ZC) {
-                int k = 0, k3 = 0;
-                for (int dy = -Rs; dy <= Rs; ++dy) {
-                    int yy = cy + dy;
-                    for (int dx = -Rs; dx <= Rs; ++dx) {
-                        int xx = cx + dx;
-                        int zv = Z[RZ.idx(yy, xx)];
-                        k += zv;
-                        if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) k3 += zv;
-                    }
-                }
+                int k = 0, k2 = 0, k3 = 0, k32 = 0;  // binary window: S2 = S1 = k (R11)
+                window_sums_rs(Rs, [&](int dy, int dx) { return (int)Z[zi + dy * RZ.w + dx]; }, k, k2, k3, k32);
                 pass = (kp.pass_lut[j] >> k) & 1ull;
                 if (pass && kp.recheck[j]) pass = (kp.pass3_lut[j] >> k3) & 1u;
             } else if (kp.std_source >= LFE_STD_RESPONSE) {
@@ -295,56 +362,33 @@ __global__ void __launch_bounds__(kThreads)
                 const bool at_zc = kp.std_source == LFE_STD_RESPONSE_AT_ZC;
                 const int32_t *r = sR + j * RR.h * RR.w;
                 const int L = kp.w * kp.w;
+                const int rb = RR.idx(cy, cx);
                 if (kp.f32) {
                     double s1 = 0, s2 = 0, t1 = 0, t2 = 0;
-                    for (int dy = -Rs; dy <= Rs; ++dy) {
-                        int yy = cy + dy;
-                        for (int dx = -Rs; dx <= Rs; ++dx) {
-                            int xx = cx + dx;
-                            double a = (at_zc && !Z[RZ.idx(yy, xx)]) ? 0.0 : (double)__int_as_float(r[RR.idx(yy, xx)]);
-                            s1 += a;
-                            s2 += a * a;
-                            if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
-                                t1 += a;
-                                t2 += a * a;
-                            }
-                        }
-                    }
+                    window_sums_rs(
+                        Rs,
+                        [&](int dy, int dx) {
+                            return (at_zc && !Z[zi + dy * RZ.w + dx]) ? 0.0
+                                                                      : (double)__int_as_float(r[rb + dy * RR.w + dx]);
+                        },
+                        s1, s2, t1, t2);
                     pass = (double)L * s2 - s1 * s1 > kp.rhs[j];
                     if (pass && kp.recheck[j]) pass = 9.0 * t2 - t1 * t1 > kp.rhs3[j];
                 } else {
                     int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
-                    for (int dy = -Rs; dy <= Rs; ++dy) {
-                        int yy = cy + dy;
-                        for (int dx = -Rs; dx <= Rs; ++dx) {
-                            int xx = cx + dx;
-                            int64_t a = (at_zc && !Z[RZ.idx(yy, xx)]) ? 0 : (int64_t)r[RR.idx(yy, xx)];
-                            s1 += a;
-                            s2 += a * a;
-                            if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
-                                t1 += a;
-                                t2 += a * a;
-                            }
-                        }
-                    }
+                    window_sums_rs(
+                        Rs,
+                        [&](int dy, int dx) {
+                            return (at_zc && !Z[zi + dy * RZ.w + dx]) ? (int64_t)0 : (int64_t)r[rb + dy * RR.w + dx];
+                        },
+                        s1, s2, t1, t2);
                     pass = (double)((int64_t)L * s2 - s1 * s1) > kp.rhs[j];
                     if (pass && kp.recheck[j]) pass = (double)(9 * t2 - t1 * t1) > kp.rhs3[j];
                 }
             } else {
                 int64_t s1 = 0, s2 = 0, t1 = 0, t2 = 0;
-                for (int dy = -Rs; dy <= Rs; ++dy) {
-                    int yy = cy + dy;
-                    for (int dx = -Rs; dx <= Rs; ++dx) {
-                        int xx = cx + dx;
-                        int64_t a = sI[RI.idx(yy, xx)];
-                        s1 += a;
-                        s2 += a * a;
-                        if (dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1) {
-                            t1 += a;
-                            t2 += a * a;
-                        }
-                    }
-                }
+                const int ib = RI.idx(cy, cx);
+                window_sums_rs(Rs, [&](int dy, int dx) { return (int64_t)sI[ib + dy * RI.w + dx]; }, s1, s2, t1, t2);
                 const int L = kp.w * kp.w;
                 pass = (double)((int64_t)L * s2 - s1 * s1) > kp.rhs[j];
                 if (pass && kp.recheck[j]) pass = (double)(9 * t2 - t1 * t1) > kp.rhs3[j];
@@ -404,7 +448,7 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
     const int y = y0 + threadIdx.x / T, x = x0 + threadIdx.x % T;
-    if (y < Hv && x < W) d_r[(int64_t)y * W + x] = log_at(kp, j, sI, RI, y, x, W, Hv);
+    if (y < Hv && x < W) d_r[(int64_t)y * W + x] = log_at(kp, j, sI, RI, y, x);
 }
 
 size_t staged_smem(const KParams &kp, int TW, int TH)

@@ -119,6 +119,86 @@ __device__ __forceinline__ int32_t log_n(const KParams &kp, const uint16_t *sI, 
     return acc;
 }
 
+// Integer masks are exactly 8-fold symmetric (R3: Eq. 1 depends on x^2 + y^2),
+// so r = sum over orbits {(+-a, +-b), (+-b, +-a)} of q(a, b) * (orbit pixel sum):
+// the (R+1)(R+2)/2 orbit sums are plain integer adds, shared by both branches
+// when their masks have the same side, then one IMAD per orbit and branch.
+__host__ __device__ constexpr int orbit_of(int dy, int dx, int R)
+{
+    const int y = dy < 0 ? -dy : dy, x = dx < 0 ? -dx : dx;
+    const int a = y < x ? y : x, b = y < x ? x : y;
+    return a * (2 * R + 3 - a) / 2 + (b - a);
+}
+
+template <int N>
+__device__ __forceinline__ void orbit_sums(const uint16_t *sI, int base, int w, int32_t (&o)[(N / 2 + 1) * (N / 2 + 2) / 2])
+{
+    constexpr int R = N / 2, K = (R + 1) * (R + 2) / 2;
+#pragma unroll
+    for (int k = 0; k < K; ++k) o[k] = 0;
+#pragma unroll
+    for (int dy = -R; dy <= R; ++dy) {
+        const uint16_t *row = sI + base + dy * w;
+#pragma unroll
+        for (int dx = -R; dx <= R; ++dx) o[orbit_of(dy, dx, R)] += (int32_t)row[dx];
+    }
+}
+
+template <int N, int J>
+__device__ __forceinline__ int32_t orbit_dot(const KParams &kp, const int32_t (&o)[(N / 2 + 1) * (N / 2 + 2) / 2])
+{
+    constexpr int R = N / 2;
+    int32_t acc = 0;
+#pragma unroll
+    for (int a = 0; a <= R; ++a)
+#pragma unroll
+        for (int b = a; b <= R; ++b) acc += kp.q[J][(R + a) * N + (R + b)] * o[orbit_of(a, b, R)];
+    return acc;
+}
+
+template <int N, int J>
+__device__ __forceinline__ int32_t log_int_orbits(const KParams &kp, const uint16_t *sI, int base, int w)
+{
+    int32_t o[(N / 2 + 1) * (N / 2 + 2) / 2];
+    orbit_sums<N>(sI, base, w, o);
+    return orbit_dot<N, J>(kp, o);
+}
+
+// both branches' integer responses at one entry
+__device__ __forceinline__ void log_pair_int(const KParams &kp, const uint16_t *sI, int base, int w, int32_t &r0,
+                                             int32_t &r1)
+{
+#define LFE_SAME(N)                                 \
+    case N: {                                       \
+        int32_t o[(N / 2 + 1) * (N / 2 + 2) / 2];   \
+        orbit_sums<N>(sI, base, w, o);              \
+        r0 = orbit_dot<N, 0>(kp, o);                \
+        r1 = orbit_dot<N, 1>(kp, o);                \
+        return;                                     \
+    }
+    if (kp.n[0] == kp.n[1]) {
+        switch (kp.n[0]) {
+            LFE_SAME(3)
+            LFE_SAME(5)
+            LFE_SAME(7)
+            LFE_SAME(9)
+        }
+    }
+#undef LFE_SAME
+    switch (kp.n[0]) {
+    case 3: r0 = log_int_orbits<3, 0>(kp, sI, base, w); break;
+    case 5: r0 = log_int_orbits<5, 0>(kp, sI, base, w); break;
+    case 7: r0 = log_int_orbits<7, 0>(kp, sI, base, w); break;
+    default: r0 = log_int_orbits<9, 0>(kp, sI, base, w); break;
+    }
+    switch (kp.n[1]) {
+    case 3: r1 = log_int_orbits<3, 1>(kp, sI, base, w); break;
+    case 5: r1 = log_int_orbits<5, 1>(kp, sI, base, w); break;
+    case 7: r1 = log_int_orbits<7, 1>(kp, sI, base, w); break;
+    default: r1 = log_int_orbits<9, 1>(kp, sI, base, w); break;
+    }
+}
+
 template <int J>
 __device__ __forceinline__ int32_t log_j(const KParams &kp, const uint16_t *sI, int base, int w)
 {
@@ -311,8 +391,15 @@ __global__ void __launch_bounds__(kThreads)
     for (int i = threadIdx.x; i < RR.h * RR.w; i += kThreads) {
         int cy = clampi(RR.oy + i / RR.w, 0, Hv - 1);
         int cx = clampi(RR.ox + i % RR.w, 0, W - 1);
+        if (kp.f32) {  // R23: fp32 in row-major tap order
 #pragma unroll
-        for (int j = 0; j < 2; ++j) sR[j * RR.h * RR.w + i] = log_at(kp, j, sI, RI, cy, cx);
+            for (int j = 0; j < 2; ++j) sR[j * RR.h * RR.w + i] = log_at(kp, j, sI, RI, cy, cx);
+        } else {  // integer: exact in any order -- orbit sums shared by the branches
+            int32_t r0, r1;
+            log_pair_int(kp, sI, RI.idx(cy, cx), RI.w, r0, r1);
+            sR[i] = r0;
+            sR[RR.h * RR.w + i] = r1;
+        }
     }
     __syncthreads();
 
@@ -468,7 +555,7 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
                           int *err_flag, cudaStream_t s)
 {
     int TW = tile_w > 0 ? tile_w : 64;
-    int TH = tile_h > 0 ? tile_h : 32;
+    int TH = tile_h > 0 ? tile_h : 64;  // 64x64: measured best on c3 (scripts/staged_tiles.sh)
     size_t smem = staged_smem(kp, TW, TH);
     if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;  // tile too large for this halo
     dim3 grid((g.width + TW - 1) / TW, (g.o1 - g.o0 + TH - 1) / TH, g.bands);

@@ -182,7 +182,11 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        if args.impl == "lfe":
+            import torch
+            torch.cuda.set_device(local)  # before the first NCCL call (P2P needs the device set)
         dist.init_process_group("nccl" if args.impl == "lfe" else "gloo")
+        dist.barrier()  # a full-group collective first: batch_isend_irecv's first call must not be partial
     return world, rank, local
 
 
@@ -373,31 +377,40 @@ def main():
     achieved = bytes_launch / (k_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
 
-    # end-to-end through the public API with host buffers (pinned), rank-local strip
+    # end-to-end through the public API with host buffers (pinned): each rank streams its
+    # strip plus the halo rows of its neighbours (so its owned rows are exact) and keeps
+    # the owned output rows
     e2e = None
     if not args.no_e2e:
-        h_in = torch.from_numpy(np.ascontiguousarray(img[shard.a:shard.b])).pin_memory()
-        h_out = torch.empty((shard.rows, W), dtype=torch.uint16).pin_memory()
+        ea, eb = shard.a - shard.ha, shard.b + shard.hb
+        erows = eb - ea
+        h_in = torch.from_numpy(np.ascontiguousarray(img[ea:eb])).pin_memory()
+        h_out = torch.empty((erows, W), dtype=torch.uint16).pin_memory()
         K = max(1, min(args.steps, 10))
         strip_rows = 1024
         ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, strip_rows)
-        ctx.extract_host_ptr(h_in.data_ptr(), W * 2, W, shard.rows, h_out.data_ptr(), W * 2)  # warm-up
+        ctx.extract_host_ptr(h_in.data_ptr(), W * 2, W, erows, h_out.data_ptr(), W * 2)  # warm-up
         if world > 1:
             dist.barrier()
         tw0 = time.perf_counter()
         for _ in range(K):
-            ctx.extract_host_ptr(h_in.data_ptr(), W * 2, W, shard.rows, h_out.data_ptr(), W * 2)
+            ctx.extract_host_ptr(h_in.data_ptr(), W * 2, W, erows, h_out.data_ptr(), W * 2)
         e2e_s = time.perf_counter() - tw0
         if world > 1:
             tt = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt.item())
-        nst = (shard.rows + strip_rows - 1) // strip_rows
-        h2d_rows = sum(min(shard.rows, (i + 1) * strip_rows + halo) - max(0, i * strip_rows - halo) for i in range(nst))
+        nst = (erows + strip_rows - 1) // strip_rows
+        h2d_rows = sum(min(erows, (i + 1) * strip_rows + halo) - max(0, i * strip_rows - halo) for i in range(nst))
+        h2d_tot = torch.tensor([h2d_rows * W * 2, erows * W * 2], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(h2d_tot)
+        h2d_b, d2h_b = (int(v) for v in h2d_tot.tolist())
         e2e = {"value": round(H * W * K / e2e_s / 1e6, 3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d_rows * W * 2 * world), "d2h_bytes_per_step": int(H * W * 2),
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                "how": "lfe_extract_host on pinned host buffers: strip-pipelined H2D -> kernel -> D2H on 3 streams, "
-                      f"{strip_rows}-row strips, wall clock of {K} synchronous calls (max over ranks)"}
+                      f"{strip_rows}-row strips, wall clock of {K} synchronous calls (max over ranks); each rank "
+                      "streams its strip plus its neighbours' halo rows"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -67,15 +67,19 @@ class StripShard:
     def exchange(self, group=None):
         """Post the halo exchange (isend/irecv with both neighbours); returns the
         works to wait on.  Owned rows are not modified."""
+        import torch
         import torch.distributed as dist
         h, ops = self.halo, []
+        # rows travel as bytes: NCCL has no uint16 type, and a byte view of whole
+        # contiguous rows is the same memory
+        B = self.buf if self.buf.dtype == torch.uint8 else self.buf.view(torch.uint8)
         if self.rank > 0:
-            ops.append(dist.P2POp(dist.isend, self.buf[self.ha:self.ha + h], self.rank - 1, group))
-            ops.append(dist.P2POp(dist.irecv, self.buf[0:self.ha], self.rank - 1, group))
+            ops.append(dist.P2POp(dist.isend, B[self.ha:self.ha + h], self.rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, B[0:self.ha], self.rank - 1, group))
         if self.rank < self.world - 1:
             e = self.ha + self.rows
-            ops.append(dist.P2POp(dist.isend, self.buf[e - h:e], self.rank + 1, group))
-            ops.append(dist.P2POp(dist.irecv, self.buf[e:e + self.hb], self.rank + 1, group))
+            ops.append(dist.P2POp(dist.isend, B[e - h:e], self.rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, B[e:e + self.hb], self.rank + 1, group))
         return dist.batch_isend_irecv(ops) if ops else []
 
     def allreduce_stats(self, t_stats, group=None):

@@ -72,6 +72,8 @@ struct FusedArgs {
     float tg[2];            // ZC gap threshold (exact integer in fp32)
     uint32_t add_lo[2];     // byte-replicated 0x80 - lo
     uint32_t add_hi[2];     // byte-replicated 0x7F - hi
+    uint32_t add_lo3[2];    // the same for the 3x3 re-check interval (R12; 0..9 = always)
+    uint32_t add_hi3[2];
     uint32_t ung_top;       // "no gap" flags of an edge between equal values
     uint32_t range_mask;    // input bits that must be zero (ERANGE); 0 = no check
     int W, H;               // virtual image
@@ -407,7 +409,7 @@ __host__ __device__ constexpr int warp_bytes(int hml) { return kEBytes + kZBytes
 
 // HML: hybrid-median levels -- 0 none, 1 the 5x5 filter, 2 the 5x5 filter followed
 // by a 3x3 one on its output (the water pipeline's second level, R17)
-template <bool IN16, int HML, bool MASKOUT, bool GAP>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ FusedArgs a, int *err_flag)
 {
@@ -559,8 +561,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (XQ) Rw = isR ? prmt(V0, V1, 0x7733) : Rw;
         const uint32_t K0 = V0 + prmt(V0, Lw, 0x2105) + prmt(V0, Lw, 0x1054) + prmt(V0, Rw, 0x4321) + prmt(V0, Rw, 0x5432);
         const uint32_t K1 = V1 + prmt(V1, Lw, 0x2107) + prmt(V1, Lw, 0x1076) + prmt(V1, Rw, 0x6321) + prmt(V1, Rw, 0x7632);
-        const uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
-        const uint32_t pass1 = (K1 + a.add_lo[1]) & ~(K1 + a.add_hi[1]) & 0x80808080u;
+        uint32_t pass0 = (K0 + a.add_lo[0]) & ~(K0 + a.add_hi[0]) & 0x80808080u;
+        uint32_t pass1 = (K1 + a.add_lo[1]) & ~(K1 + a.add_hi[1]) & 0x80808080u;
+        if constexpr (RC) {
+            // "re-calculated ... with a localized 3x3 neighborhood" (R12): 3-row
+            // count of Z rows rho-7 .. rho-5, then the same byte-wise horizontal sum over +-1
+            uint32_t W3;
+            if constexpr (!YF) {
+                W3 = zRing[((row_e - 1) & 7) * 32 + lane] + Zc + zRing[((row_e + 1) & 7) * 32 + lane];
+            } else {
+                W3 = 0;
+                if (row_e >= 0) {
+#pragma unroll
+                    for (int k = -1; k <= 1; ++k) W3 += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
+                }
+            }
+            const uint32_t W30 = W3 & 0x0F0F0F0Fu, W31 = (W3 >> 4) & 0x0F0F0F0Fu;
+            uint32_t L3 = __shfl_up_sync(0xffffffffu, prmt(W30, W31, 0x7632), 1);
+            uint32_t R3 = __shfl_down_sync(0xffffffffu, prmt(W30, W31, 0x5410), 1);
+            if constexpr (XQ) L3 = isL ? prmt(W30, W31, 0x4400) : L3;
+            if constexpr (XQ) R3 = isR ? prmt(W30, W31, 0x7733) : R3;
+            const uint32_t K30 = W30 + prmt(W30, L3, 0x2105) + prmt(W30, R3, 0x4321);
+            const uint32_t K31 = W31 + prmt(W31, L3, 0x2107) + prmt(W31, R3, 0x6321);
+            pass0 &= (K30 + a.add_lo3[0]) & ~(K30 + a.add_hi3[0]);
+            pass1 &= (K31 + a.add_lo3[1]) & ~(K31 + a.add_hi3[1]);
+        }
         const uint32_t M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
         uint32_t e0, e1;                                              // E pairs of row rho-6
         {
@@ -1176,10 +1201,10 @@ constexpr size_t fused_smem()
     return kHdr + (size_t)kS * nbox * (IN16 ? 232 * 2 : 480) * kR + (size_t)kWarps * warp_bytes(HML);
 }
 
-template <bool IN16, int HML, bool MASKOUT, bool GAP>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC>
 cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP>;
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC>;
     constexpr size_t smem = fused_smem<IN16, HML>();
     static int grid_cap = 0;
     if (!grid_cap) {
@@ -1226,9 +1251,9 @@ bool fused_supports(const KParams &kp, int bit_depth)
     if (kp.n[0] != 5 || kp.n[1] != 5) return false;
     if (kp.std_source != LFE_STD_ZC || kp.w != 5) return false;
     if (kp.f32) return false;  // float masks (R23): general kernel only
-    if (kp.recheck[0] || kp.recheck[1]) return false;
     if (kp.hm && kp.m != 5) return false;
     if (kp.m2 && !(kp.hm && kp.m == 5 && kp.m2 == 3)) return false;
+    if ((kp.recheck[0] || kp.recheck[1]) && kp.m2) return false;  // no such variant compiled
     for (int j = 0; j < 2; ++j) {
         if (kp.zc_t[j] > (1 << 24)) return false;  // t <= 2^24: every gap test is exact in fp32
         int lo, hi;
@@ -1249,6 +1274,10 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
         interval_of(kp.pass_lut[j], 25, &lo, &hi);
         fa.add_lo[j] = (uint32_t)(0x80 - lo) * 0x01010101u;
         fa.add_hi[j] = (uint32_t)(0x7F - hi) * 0x01010101u;
+        int lo3 = 0, hi3 = 9;  // no re-check: every 3x3 count passes
+        if (kp.recheck[j]) interval_of(kp.pass3_lut[j], 9, &lo3, &hi3);
+        fa.add_lo3[j] = (uint32_t)(0x80 - lo3) * 0x01010101u;
+        fa.add_hi3[j] = (uint32_t)(0x7F - hi3) * 0x01010101u;
     }
     fa.ung_top = (kp.zc_t[0] > 0 ? 0x08080808u : 0u) | (kp.zc_t[1] > 0 ? 0x80808080u : 0u);
     const uint32_t maxv = (uint32_t)kp.maxv;
@@ -1286,30 +1315,41 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
 
     const int hml = kp.m2 ? 2 : kp.hm ? 1 : 0;
     const bool mask = kp.out_mode == LFE_OUT_MASK;
-    // the GAP variant is exact for t = 0 as well; the two-level filter only has that one
-    const bool gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || hml == 2;
-#define LFE_DISPATCH(A, B, C, D) \
-    if (in16 == A && hml == B && mask == C && gap == D) return launch_t<A, B, C, D>(fa, map, err_flag, s);
-    LFE_DISPATCH(true, 1, false, true)
-    LFE_DISPATCH(true, 1, false, false)
-    LFE_DISPATCH(true, 1, true, true)
-    LFE_DISPATCH(true, 1, true, false)
-    LFE_DISPATCH(true, 0, false, true)
-    LFE_DISPATCH(true, 0, false, false)
-    LFE_DISPATCH(true, 0, true, true)
-    LFE_DISPATCH(true, 0, true, false)
-    LFE_DISPATCH(false, 1, false, true)
-    LFE_DISPATCH(false, 1, false, false)
-    LFE_DISPATCH(false, 1, true, true)
-    LFE_DISPATCH(false, 1, true, false)
-    LFE_DISPATCH(false, 0, false, true)
-    LFE_DISPATCH(false, 0, false, false)
-    LFE_DISPATCH(false, 0, true, true)
-    LFE_DISPATCH(false, 0, true, false)
-    LFE_DISPATCH(true, 2, false, true)
-    LFE_DISPATCH(true, 2, true, true)
-    LFE_DISPATCH(false, 2, false, true)
-    LFE_DISPATCH(false, 2, true, true)
+    const bool rc = kp.recheck[0] || kp.recheck[1];
+    // the GAP variant is exact for t = 0 as well; the two-level filter and the 3x3
+    // re-check only have that one
+    const bool gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || hml == 2 || rc;
+#define LFE_DISPATCH(A, B, C, D, E) \
+    if (in16 == A && hml == B && mask == C && gap == D && rc == E) return launch_t<A, B, C, D, E>(fa, map, err_flag, s);
+    LFE_DISPATCH(true, 1, false, true, false)
+    LFE_DISPATCH(true, 1, false, false, false)
+    LFE_DISPATCH(true, 1, true, true, false)
+    LFE_DISPATCH(true, 1, true, false, false)
+    LFE_DISPATCH(true, 0, false, true, false)
+    LFE_DISPATCH(true, 0, false, false, false)
+    LFE_DISPATCH(true, 0, true, true, false)
+    LFE_DISPATCH(true, 0, true, false, false)
+    LFE_DISPATCH(false, 1, false, true, false)
+    LFE_DISPATCH(false, 1, false, false, false)
+    LFE_DISPATCH(false, 1, true, true, false)
+    LFE_DISPATCH(false, 1, true, false, false)
+    LFE_DISPATCH(false, 0, false, true, false)
+    LFE_DISPATCH(false, 0, false, false, false)
+    LFE_DISPATCH(false, 0, true, true, false)
+    LFE_DISPATCH(false, 0, true, false, false)
+    LFE_DISPATCH(true, 2, false, true, false)
+    LFE_DISPATCH(true, 2, true, true, false)
+    LFE_DISPATCH(false, 2, false, true, false)
+    LFE_DISPATCH(false, 2, true, true, false)
+    // the paper's 5x5 -> 3x3 re-check (R12), one or no median level
+    LFE_DISPATCH(true, 1, false, true, true)
+    LFE_DISPATCH(true, 1, true, true, true)
+    LFE_DISPATCH(true, 0, false, true, true)
+    LFE_DISPATCH(true, 0, true, true, true)
+    LFE_DISPATCH(false, 1, false, true, true)
+    LFE_DISPATCH(false, 1, true, true, true)
+    LFE_DISPATCH(false, 0, false, true, true)
+    LFE_DISPATCH(false, 0, true, true, true)
 #undef LFE_DISPATCH
     return cudaErrorNotSupported;
 }

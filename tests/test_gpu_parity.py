@@ -60,8 +60,9 @@ def run_gpu(img: np.ndarray, p: lfe.Params, kernel=lfe.LFE_KERNEL_AUTO, tile=Non
 
 def fused_ok(p: lfe.Params) -> bool:
     return (tuple(p.log_size) == (5, 5) and p.std_source == lfe.LFE_STD_ZC and p.std_window == 5
-            and max(p.std3_threshold) < 0 and (not p.hybrid_median or p.median_window == 5)
-            and (p.median_window2 == 0 or (p.hybrid_median and p.median_window == 5 and p.median_window2 == 3)))
+            and p.mask_mode == lfe.LFE_MASK_INT and (not p.hybrid_median or p.median_window == 5)
+            and (p.median_window2 == 0 or (p.hybrid_median and p.median_window == 5 and p.median_window2 == 3))
+            and not (max(p.std3_threshold) >= 0 and p.median_window2))
 
 
 def assert_same(got, want, what=""):
@@ -696,3 +697,31 @@ def test_c4_all_bands_one_launch_full_size_sampled():
         ctx.check()
     for b in range(4):
         _sampled_rows(img[b], p, got[b], [(0, 12), (4090 + b, 4106 + b), (8180, 8192)])
+
+
+# ------------------------------ the paper's 5x5 -> 3x3 re-check on the fused path ----
+@pytest.mark.parametrize("bd,mode,hm", [(8, lfe.LFE_OUT_EXTRACT, True), (10, lfe.LFE_OUT_MASK, True),
+                                        (12, lfe.LFE_OUT_EXTRACT, False), (8, lfe.LFE_OUT_MASK, False)])
+def test_fused_recheck(bd, mode, hm):
+    """a pixel whose 5x5 deviation passes is re-checked on its 3x3
+    neighbourhood (R12).  Fused kernel, every shape, both column-edge paths."""
+    p = lfe.Params(bit_depth=bd, std_threshold=(0.25, 0.35), std3_threshold=(0.4, 0.2), zc_threshold=(0.01, 0.0),
+                   out_mode=mode, hybrid_median=hm)
+    assert fused_ok(p)
+    rng = np.random.default_rng(700 + bd + mode + hm)
+    for (H, W), kind in itertools.product(SHAPES + [(33, 452), (129, 463), (40, 1348), (20, 1344)],
+                                          ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, bd, kind)
+        assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), f"{H}x{W} {kind}")
+    # one branch re-checked, the other not; an empty 3x3 interval (T3 above the maximum)
+    for t3 in [(0.3, -1.0), (-1.0, 0.45), (0.6, 0.6)]:
+        p2 = lfe.Params(bit_depth=bd, std3_threshold=t3, out_mode=mode, hybrid_median=hm)
+        img = scenes.random_image(rng, 70, 300, bd, "mixed")
+        assert_same(run_gpu(img, p2, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p2)), f"t3 {t3}")
+
+
+def test_fused_recheck_c3_sampled():
+    img = scenes.scene_c3()
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), std3_threshold=(0.4, 0.4))
+    got = run_gpu(img, p)
+    _sampled_rows(img, p, got, [(0, 20), (5000, 5024), (11980, 12000)])

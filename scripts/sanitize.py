@@ -43,3 +43,8 @@ with lfe.Context(lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))) as ctx:
     ctx.extract_bands(b)
     ctx.check()
     print('ok bands')
+# the 3x3 re-check variant of the fused kernel
+with lfe.Context(lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), std3_threshold=(0.4, 0.4))) as ctx:
+    ctx.extract(torch.from_numpy(img).cuda())
+    ctx.check()
+    print('ok recheck')

@@ -725,3 +725,23 @@ def test_fused_recheck_c3_sampled():
     p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), std3_threshold=(0.4, 0.4))
     got = run_gpu(img, p)
     _sampled_rows(img, p, got, [(0, 20), (5000, 5024), (11980, 12000)])
+
+
+def test_extract_bands_validation():
+    with lfe.Context(lfe.Params()) as ctx:
+        d = torch.zeros((3, 40, 64), dtype=torch.uint8, device="cuda")
+        o = torch.zeros_like(d)
+        pin, pout = d.stride(1), o.stride(1)
+        for args in [(pin, 40 * 64, 64, 40, 0), (pin, 40 * 64, 64, 40, 70000),   # band count
+                     (pin, 10 * 64, 64, 40, 3)]:                                   # band stride < one band
+            with pytest.raises(lfe.LfeError):
+                lfe.lfe_extract_bands(ctx.handle, d.data_ptr(), args[0], args[1], args[2], args[3], args[4],
+                                      o.data_ptr(), pout, 40 * 64, 0)
+        with pytest.raises(lfe.LfeError):  # input and output overlap
+            lfe.lfe_extract_bands(ctx.handle, d.data_ptr(), pin, 40 * 64, 64, 40, 3, d.data_ptr(), pin, 40 * 64, 0)
+    pa = lfe.Params(adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.5, 0.5))
+    with lfe.Context(pa) as ctx:
+        d = torch.zeros((2, 40, 64), dtype=torch.uint8, device="cuda")
+        with pytest.raises(lfe.LfeError) as ei:
+            ctx.extract_bands(d)
+        assert ei.value.status == lfe.LFE_EUNSUPPORTED

@@ -26,7 +26,8 @@
  *     flag and (for lfe_extract_host) its staging buffers.
  *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
  *   - A ctx is used by one host thread at a time; distinct ctxs are
- *     independent.  A ctx is bound to the CUDA device current at create.
+ *     independent.  A ctx is bound to the CUDA device current at create;
+ *     compute calls with another device current return LFE_EINVAL.
  *   - There is no CPU fallback: without an sm_100 device every compute entry
  *     point returns LFE_ENODEV.
  */

@@ -1206,11 +1206,16 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
 {
     auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC>;
     constexpr size_t smem = fused_smem<IN16, HML>();
-    static int grid_cap = 0;
+    // the shared-memory attribute is per device: one-time setup for each device this
+    // process launches on (a ctx binds one device; several ctxs may span devices)
+    constexpr int kMaxDevices = 64;
+    static int grid_caps[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &grid_cap = grid_caps[dev < kMaxDevices ? dev : kMaxDevices - 1];
     if (!grid_cap) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kThreads, smem);
         grid_cap = sms * (per_sm > 0 ? per_sm : 1);

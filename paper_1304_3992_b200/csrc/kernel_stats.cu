@@ -162,13 +162,10 @@ cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_st
     const int rows = g.o1 - g.o0;
     if (rows <= 0 || g.width <= 0) return cudaSuccess;
     const long long ntiles = (long long)((g.width + kTileW - 1) / kTileW) * ((rows + kTileH - 1) / kTileH);
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
     const int grid = (int)(ntiles < 16LL * sms ? ntiles : 16LL * sms);
     return in16 ? launch_stats_t<uint16_t>(kp, g, d_stats, grid, s) : launch_stats_t<uint8_t>(kp, g, d_stats, grid, s);
 }

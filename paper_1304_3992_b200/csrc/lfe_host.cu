@@ -218,8 +218,19 @@ bool overlap(const void *a, size_t na, const void *b, size_t nb)
     return x < y + nb && y < x + na;
 }
 
+// a ctx is bound to the device current at lfe_create; launching from another is an error
+lfe_status check_bound_device(const lfe_ctx *c)
+{
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(LFE_ECUDA, "cudaGetDevice failed");
+    if (dev != c->device) return fail(LFE_EINVAL, "ctx is bound to device %d but device %d is current", c->device, dev);
+    return LFE_OK;
+}
+
 lfe_status run(lfe_ctx *c, const Geometry &g, cudaStream_t s)
 {
+    lfe_status bound = check_bound_device(c);
+    if (bound != LFE_OK) return bound;
     const bool in16 = c->p.bit_depth > 8;
     int k = c->cfg.kernel;
     const bool aligned = ((reinterpret_cast<uintptr_t>(g.in) | reinterpret_cast<uintptr_t>(g.out) |
@@ -485,6 +496,8 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, i
     if (st != LFE_OK) return st;
     Geometry g;
     st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, c->kp.RL, &g);
+    if (st != LFE_OK) return st;
+    st = check_bound_device(c);
     if (st != LFE_OK) return st;
     cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));

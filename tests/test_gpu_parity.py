@@ -745,3 +745,37 @@ def test_extract_bands_validation():
         with pytest.raises(lfe.LfeError) as ei:
             ctx.extract_bands(d)
         assert ei.value.status == lfe.LFE_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("pi", range(5))
+def test_strips_equal_oracle_every_variant(kernel, pi):
+    """Row strips (lfe_extract_rows, halos of exactly lfe_halo rows) for every
+    fused variant family and a general-kernel configuration, against the oracle
+    on the whole image: no median, one level, two levels, the 3x3 re-check,
+    a 9x9 mask with 7x7 windows (halo 14)."""
+    p = [lfe.Params(bit_depth=8, hybrid_median=False, zc_threshold=(0.01, 0.0)),
+         lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), out_mode=lfe.LFE_OUT_MASK),
+         lfe.Params(bit_depth=8, median_window2=3, zc_threshold=(0.0, 0.01)),
+         lfe.Params(bit_depth=10, std3_threshold=(0.4, 0.3), zc_threshold=(0.01, 0.01)),
+         lfe.Params(bit_depth=10, log_size=(9, 5), sigma=(1.5, 20.0), std_window=7, median_window=7)][pi]
+    if kernel == lfe.LFE_KERNEL_AUTO and not fused_ok(p):
+        pytest.skip("general kernel only (covered by the STAGED run)")
+    rng = np.random.default_rng(800 + pi)
+    img = scenes.random_image(rng, 150, 452, p.bit_depth, "mixed")
+    want = O.run(img, _oparams(p))
+    H = img.shape[0]
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_KERNEL, kernel)
+        h = ctx.halo
+        d = _pitched(img.shape, torch.uint8 if p.bit_depth <= 8 else torch.uint16)
+        d.copy_(torch.from_numpy(img))
+        out = _pitched(img.shape, torch.uint8 if p.bit_depth <= 8 or p.out_mode == lfe.LFE_OUT_MASK else torch.uint16)
+        for cuts in ([0, 75, 150], [0, 3, 20, 130, 147, 150], [0, 16, 17, 134, 150]):
+            out.zero_()
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                ha, hb = min(h, a), min(h, H - b)
+                flags = (lfe.LFE_TOP_IS_EDGE if a - ha == 0 else 0) | (lfe.LFE_BOTTOM_IS_EDGE if b + hb == H else 0)
+                ctx.extract_rows(d, a, b - a, ha, hb, flags, out, out_row0=a)
+            ctx.check()
+            assert_same(out.cpu().numpy(), want, f"cuts {cuts} halo {h}")

@@ -129,3 +129,37 @@ class StripShard:
         if hi < R:
             out.append(self.band(hi, R - hi))
         return out
+
+
+def plan_bands(bands: int, H: int, world: int, halo: int):
+    """Work of each rank for a multispectral scene (c4).  Bands
+    are independent images; the band-major row line (bands x H rows) is cut
+    into `world` contiguous, equal pieces, each cut snapped to a band boundary
+    when it would leave fewer than `halo` rows of a band on one side (so one
+    neighbour exchange still suffices).  When world divides bands this deals
+    out whole bands and needs no collective at all.  Returns, per rank, a list
+    of (band, a, b) owned row ranges."""
+    if bands < 1 or world < 1 or H < 1:
+        raise ValueError("bad bands/H/world")
+    T = bands * H
+    cuts = [0]
+    for k in range(1, world):
+        c = round(k * T / world)
+        b0 = (c // H) * H
+        if 0 < c - b0 < halo:
+            c = b0
+        elif 0 < b0 + H - c < halo:
+            c = b0 + H
+        cuts.append(max(c, cuts[-1]))
+    cuts.append(T)
+    work = []
+    for k in range(world):
+        lo, hi, items = cuts[k], cuts[k + 1], []
+        u = lo
+        while u < hi:
+            b = u // H
+            e = min(hi, (b + 1) * H)
+            items.append((b, u - b * H, e - b * H))
+            u = e
+        work.append(items)
+    return work

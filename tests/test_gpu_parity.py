@@ -779,3 +779,27 @@ def test_strips_equal_oracle_every_variant(kernel, pi):
                 ctx.extract_rows(d, a, b - a, ha, hb, flags, out, out_row0=a)
             ctx.check()
             assert_same(out.cpu().numpy(), want, f"cuts {cuts} halo {h}")
+
+
+@pytest.mark.parametrize("world", [1, 3, 6, 8])
+def test_c4_bands_dealt_to_ranks(world):
+    """c4's multi-GPU plan (shard.plan_bands): each simulated rank runs its
+    (band, rows) items through lfe_extract_rows with halos from its band; the
+    assembled scene equals the oracle band by band."""
+    from paper_1304_3992_b200.shard import plan_bands
+    img = scenes.scene_c4(size=512)
+    B, H, W = img.shape
+    p = lfe.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
+    with lfe.Context(p) as ctx:
+        h = ctx.halo
+        d = torch.from_numpy(img).cuda()
+        out = torch.zeros_like(d)
+        for items in plan_bands(B, H, world, h):
+            for b, a, e in items:
+                ha, hb = min(h, a), min(h, H - e)
+                flags = (lfe.LFE_TOP_IS_EDGE if a - ha == 0 else 0) | (lfe.LFE_BOTTOM_IS_EDGE if e + hb == H else 0)
+                ctx.extract_rows(d[b], a, e - a, ha, hb, flags, out[b], out_row0=a)
+        ctx.check()
+        got = out.cpu().numpy()
+    for b in range(B):
+        assert_same(got[b], O.run(img[b], _oparams(p)), f"band {b}")

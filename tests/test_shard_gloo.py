@@ -153,3 +153,26 @@ def test_gloo_stats_allreduce_equals_whole_image(world):
             assert v[3 + j] * 2**24 + v[5 + j] == sum(int(x) ** 2 for x in r.ravel())
             # and the threshold the library resolves from them equals the oracle's sigma
             assert O.global_std(v[0], v[1 + j], v[3 + j] * 2**24 + v[5 + j]) == O.std_of_response(r)
+
+
+@pytest.mark.parametrize("bands,world", [(4, 1), (4, 2), (4, 3), (4, 4), (4, 8), (3, 8), (4, 6), (1, 5)])
+def test_plan_bands_covers_every_band_row_once(bands, world):
+    from paper_1304_3992_b200.shard import plan_bands
+    H = 8192
+    work = plan_bands(bands, H, world, 7)
+    assert len(work) == world
+    cover = {b: [] for b in range(bands)}
+    for items in work:
+        for b, a, e in items:
+            cover[b].append((a, e))
+    for b, rs in cover.items():
+        rs.sort()
+        assert rs[0][0] == 0 and rs[-1][1] == H
+        assert all(x[1] == y[0] for x, y in zip(rs, rs[1:]))
+    rows = [sum(e - a for _, a, e in items) for items in work]
+    assert min(rows) > 0 and max(rows) <= 1.01 * (bands * H / world) + 7
+    for items in work:  # every partial band keeps >= halo rows (one exchange suffices)
+        for b, a, e in items:
+            assert e - a >= 7 or (a, e) == (0, H)
+    if bands % world == 0:  # whole bands, no exchange
+        assert all(a == 0 and e == H for items in work for _, a, e in items)

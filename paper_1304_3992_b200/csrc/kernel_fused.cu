@@ -59,8 +59,12 @@ constexpr int kProdThread = kThreads - 32;  // producer: lane 0 of the highest (
 constexpr int kR = 8;                       // rows per TMA stage (= rows per chunk)
 constexpr int kS = 4;                       // ring stages
 constexpr int kERow = 264;                  // bytes per E ring row: 128 px + 2 px pad each side
-constexpr int kEBytes = 8 * kERow;          // 8-row E ring per warp
-constexpr int kZBytes = 8 * 32 * 4;         // 8-row Z ring per warp
+// The E and Z rings hold 8 row slots, each stored twice (slots s and s + 8): the
+// interior walk addresses them relative to its 8-row chunk, so every read is a
+// fixed offset from one per-step base and never wraps.  Edge-row
+// walks use the first 8 slots with absolute (clamped) row indices.
+constexpr int kEBytes = 16 * kERow;         // 8-row E ring per warp, mirrored
+constexpr int kZBytes = 16 * 32 * 4;        // 8-row Z ring per warp, mirrored
 constexpr int kRBytes = 2 * 32 * 32;        // 2-row r ring per warp (zero-pixel slow path)
 constexpr int kHBytes = 4 * kERow;          // 4-row ring of first-median-level rows (second level only)
 constexpr int kHdr = 128;                   // mbarriers
@@ -490,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool isL = false, isR = false;
     uint32_t zmask = 0x88888888u;  // flag bits of this lane's pixels inside the image
     uint32_t in_lo = 0, in_hi = 0;
+    uint32_t chk_lo = 0, chk_hi = 0;  // the range-check masks of the current chunk
     float acc[2][4][4];
     uint32_t PA, NA, PB, NB, Um, Up, Ung, V;
 
@@ -499,27 +504,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto prow = [&](int rho) { return min(max(rho, it.plo), it.phi - 1); };
 
+    // output: this lane's pixel 0 at the item's first row (set per item), and
+    // what this lane stores: 0 nothing (halo lane or right of the image), 1 four
+    // pixels, 2 the 1..3 pixels left of the image's right edge
+    char *obase = nullptr;
+    int skind = 0;
     auto store = [&](int row, uint32_t o0, uint32_t o1) {
-        if (lane < 2 || lane >= 30) return;
-        char *orow = reinterpret_cast<char *>(a.out) + it.band * a.out_band_stride + (long long)(row - a.o0) * a.out_pitch;
+        if (skind == 0) return;
+        char *orow = obase + (unsigned long long)(unsigned)(row - it.ys) * (unsigned)a.out_pitch;
         if (IN16 && !MASKOUT) {
-            if (x0 + 3 < W) {
-                *reinterpret_cast<uint2 *>(orow + 2LL * x0) = make_uint2(o0, o1);
+            if (skind == 1) {
+                *reinterpret_cast<uint2 *>(orow) = make_uint2(o0, o1);
             } else {
                 uint16_t *p = reinterpret_cast<uint16_t *>(orow);
-                if (x0 < W) p[x0] = (uint16_t)o0;
-                if (x0 + 1 < W) p[x0 + 1] = (uint16_t)(o0 >> 16);
-                if (x0 + 2 < W) p[x0 + 2] = (uint16_t)o1;
+                p[0] = (uint16_t)o0;
+                if (x0 + 1 < W) p[1] = (uint16_t)(o0 >> 16);
+                if (x0 + 2 < W) p[2] = (uint16_t)o1;
             }
         } else {
             const uint32_t b = prmt(o0, o1, 0x6420);
-            if (x0 + 3 < W) {
-                *reinterpret_cast<uint32_t *>(orow + x0) = b;
+            if (skind == 1) {
+                *reinterpret_cast<uint32_t *>(orow) = b;
             } else {
                 uint8_t *p = reinterpret_cast<uint8_t *>(orow);
-                if (x0 < W) p[x0] = (uint8_t)b;
-                if (x0 + 1 < W) p[x0 + 1] = (uint8_t)(b >> 8);
-                if (x0 + 2 < W) p[x0 + 2] = (uint8_t)(b >> 16);
+                p[0] = (uint8_t)b;
+                if (x0 + 1 < W) p[1] = (uint8_t)(b >> 8);
+                if (x0 + 2 < W) p[2] = (uint8_t)(b >> 16);
             }
         }
     };
@@ -529,7 +539,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // reads only what earlier steps left in registers / the smem rings), so the
     // compiler can interleave them: std+merge for row rho-6, hybrid median for row
     // rho-9, input+LoG for row rho, zero crossings for row rho-3.
-    auto step = [&](auto fix_tag, int rho, float(&rB)[2][4], float(&rC)[2][4]) {
+    //
+    // Interior walks (not YF) address every ring relative to the current 8-row chunk
+    // (= one TMA stage: chunk m of the walk is stage g_base + m): k = rho's row in the
+    // chunk, cb / pb = this lane's pixel 0 in the chunk's / the previous chunk's stage.
+    // A row rho - c then sits in ring slot (k - c) & 7, read from its mirror at the
+    // fixed index k + ((8 - c) & 7) or one 8 above -- always inside the 16 stored slots.
+    auto step = [&](auto fix_tag, int rho, float(&rB)[2][4], float(&rC)[2][4], int k, const unsigned char *cb,
+                    const unsigned char *pb) {
         constexpr bool XF = decltype(fix_tag)::value & 1, YF = decltype(fix_tag)::value & 2;
         constexpr bool XQ = decltype(fix_tag)::value & 4;
         // XQ: cheap column edges (W % 4 == 0; chosen per CTA piece, so all warps of an SM
@@ -540,17 +557,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_z = rho - 3, row_e = rho - 6;
         // ---------------- std gate + merge for row rho-6 (Z rows rho-8 .. rho-4) ----------------
         uint32_t Zc;
+        const uint32_t *zk = zRing + k * 32 + lane;
         if constexpr (!YF) {
-            const uint32_t z_new = zRing[((row_e + 2) & 7) * 32 + lane];
-            const uint32_t z_old = zRing[((row_e - 3) & 7) * 32 + lane];
+            const uint32_t z_new = zk[4 * 32];  // row rho-4
+            const uint32_t z_old = zk[7 * 32];  // row rho-9
             V = V + z_new - z_old;  // running 5-row count (bytes; <= 5 per nibble, no carries)
-            Zc = zRing[(row_e & 7) * 32 + lane];
+            Zc = zk[2 * 32];        // row rho-6
         } else {
             V = 0;
             Zc = 0;
             if (row_e >= 0) {  // rows above the image only feed discarded outputs (and row 0 may be in flight)
 #pragma unroll
-                for (int k = -2; k <= 2; ++k) V += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
+                for (int d = -2; d <= 2; ++d) V += zRing[(min(max(row_e + d, 0), H - 1) & 7) * 32 + lane];
                 Zc = zRing[(min(row_e, H - 1) & 7) * 32 + lane];
             }
         }
@@ -568,12 +586,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // count of Z rows rho-7 .. rho-5, then the same byte-wise horizontal sum over +-1
             uint32_t W3;
             if constexpr (!YF) {
-                W3 = zRing[((row_e - 1) & 7) * 32 + lane] + Zc + zRing[((row_e + 1) & 7) * 32 + lane];
+                W3 = zk[1 * 32] + Zc + zk[3 * 32];  // rows rho-7, rho-6, rho-5
             } else {
                 W3 = 0;
                 if (row_e >= 0) {
 #pragma unroll
-                    for (int k = -1; k <= 1; ++k) W3 += zRing[(min(max(row_e + k, 0), H - 1) & 7) * 32 + lane];
+                    for (int d = -1; d <= 1; ++d) W3 += zRing[(min(max(row_e + d, 0), H - 1) & 7) * 32 + lane];
                 }
             }
             const uint32_t W30 = W3 & 0x0F0F0F0Fu, W31 = (W3 >> 4) & 0x0F0F0F0Fu;
@@ -593,13 +611,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (MASKOUT) {
                 i0 = i1 = 0x00FF00FFu;
             } else {
-                const unsigned char *rp = row_ptr(prow(row_e));
+                const unsigned char *rp;
+                if constexpr (YF)
+                    rp = row_ptr(prow(row_e)) + off_own;
+                else
+                    rp = k >= 6 ? cb + (k - 6) * kRowBytes : pb + (k + 2) * kRowBytes;
                 if constexpr (IN16) {
-                    const uint2 own = *reinterpret_cast<const uint2 *>(rp + off_own);
+                    const uint2 own = *reinterpret_cast<const uint2 *>(rp);
                     i0 = own.x;
                     i1 = own.y;
                 } else {
-                    const uint32_t own = *reinterpret_cast<const uint32_t *>(rp + off_own);
+                    const uint32_t own = *reinterpret_cast<const uint32_t *>(rp);
                     i0 = prmt(own, 0, 0x4140);
                     i1 = prmt(own, 0, 0x4342);
                 }
@@ -614,22 +636,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (HM) {
             const int row_o = rho - 9;
             uint32_t E[5][4];  // rows row_o-2 .. row_o+2: (x-2,x-1) (x,x+1) (x+2,x+3) (x+4,x+5)
+            const unsigned char *ek = eRing + k * kERow + 8 * lane;
 #pragma unroll
-            for (int k = 0; k < 5; ++k) {
-                int r = row_o - 2 + k;
-                if constexpr (YF) r = min(max(r, 0), H - 1);
-                const unsigned char *b = eRing + (r & 7) * kERow + 8 * lane;
+            for (int kk = 0; kk < 5; ++kk) {
+                const unsigned char *b;
+                if constexpr (YF) {
+                    const int r = min(max(row_o - 2 + kk, 0), H - 1);
+                    b = eRing + (r & 7) * kERow + 8 * lane;
+                } else {
+                    constexpr int kIdx[5] = {5, 6, 7, 8, 1};  // rows rho-11 .. rho-7
+                    b = ek + kIdx[kk] * kERow;
+                }
                 uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
                 if (!YF || row_o >= 0) {  // (YF) outputs above the image are discarded; row 0 may be in flight
                     lo = *reinterpret_cast<const uint2 *>(b);
                     hi = *reinterpret_cast<const uint2 *>(b + 8);
                 }
-                E[k][0] = lo.x;
-                E[k][1] = lo.y;
-                E[k][2] = hi.x;
-                E[k][3] = hi.y;
-                if constexpr (XQ) E[k][0] = isL ? prmt(E[k][1], 0, 0x1010) : E[k][0];
-                if constexpr (XQ) E[k][3] = isR ? prmt(E[k][2], 0, 0x3232) : E[k][3];
+                E[kk][0] = lo.x;
+                E[kk][1] = lo.y;
+                E[kk][2] = hi.x;
+                E[kk][3] = hi.y;
+                if constexpr (XQ) E[kk][0] = isL ? prmt(E[kk][1], 0, 0x1010) : E[kk][0];
+                if constexpr (XQ) E[kk][3] = isR ? prmt(E[kk][2], 0, 0x3232) : E[kk][3];
             }
             const uint32_t s2a = sh1(E[2][0], E[2][1]), s2b = sh1(E[2][1], E[2][2]), s2c = sh1(E[2][2], E[2][3]);
             const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
@@ -651,8 +679,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row_q = rho - 11;
             uint32_t Hq[3][4];  // rows row_q-1 .. row_q+1, pairs as in E above
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                int r = row_q - 1 + k;
+            for (int kk = 0; kk < 3; ++kk) {
+                int r = row_q - 1 + kk;
                 if constexpr (YF) r = min(max(r, 0), H - 1);
                 const unsigned char *b = hRing + (r & 3) * kERow + 8 * lane;
                 uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
@@ -660,12 +688,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     lo = *reinterpret_cast<const uint2 *>(b);
                     hi = *reinterpret_cast<const uint2 *>(b + 8);
                 }
-                Hq[k][0] = lo.x;
-                Hq[k][1] = lo.y;
-                Hq[k][2] = hi.x;
-                Hq[k][3] = hi.y;
-                if constexpr (XQ) Hq[k][0] = isL ? prmt(Hq[k][1], 0, 0x1010) : Hq[k][0];
-                if constexpr (XQ) Hq[k][3] = isR ? prmt(Hq[k][2], 0, 0x3232) : Hq[k][3];
+                Hq[kk][0] = lo.x;
+                Hq[kk][1] = lo.y;
+                Hq[kk][2] = hi.x;
+                Hq[kk][3] = hi.y;
+                if constexpr (XQ) Hq[kk][0] = isL ? prmt(Hq[kk][1], 0, 0x1010) : Hq[kk][0];
+                if constexpr (XQ) Hq[kk][3] = isR ? prmt(Hq[kk][2], 0, 0x3232) : Hq[kk][3];
             }
             // '+' group (centre, left, right, up, down) and 'x' group (centre, 4 diagonals), R16
             const uint32_t u01 = sh1(Hq[0][0], Hq[0][1]), u12 = sh1(Hq[0][1], Hq[0][2]), u23 = sh1(Hq[0][2], Hq[0][3]);
@@ -677,18 +705,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         // ---------------- input row ----------------
-        const unsigned char *rowp = row_ptr(prow(rho));
+        const unsigned char *rowp = YF ? row_ptr(prow(rho)) + off_own : cb + k * kRowBytes;
         float I[8];  // columns x0-2 .. x0+5
         if constexpr (IN16) {
-            const uint2 own = *reinterpret_cast<const uint2 *>(rowp + off_own);
-            range_acc |= (own.x & in_lo) | (own.y & in_hi);
+            const uint2 own = *reinterpret_cast<const uint2 *>(rowp);
+            range_acc |= (own.x & chk_lo) | (own.y & chk_hi);
             I[2] = lo16f(own.x);
             I[3] = hi16f(own.x);
             I[4] = lo16f(own.y);
             I[5] = hi16f(own.y);
         } else {
-            const uint32_t own = *reinterpret_cast<const uint32_t *>(rowp + off_own);
-            range_acc |= own & in_lo;
+            const uint32_t own = *reinterpret_cast<const uint32_t *>(rowp);
+            range_acc |= own & chk_lo;
             I[2] = byte_f(own, 0x5440);
             I[3] = byte_f(own, 0x5441);
             I[4] = byte_f(own, 0x5442);
@@ -776,11 +804,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rB[j][i] + rC[j][i]);
         const uint32_t Dp = pack_flags(t);
         uint32_t Dng = 0, Rng = 0;
+        // gap failure on an edge between opposite signs: |r_p| + |r_n| < t (R9), as
+        // sat(-(u_p + |r_n|)) with u_p = |r_p| - t shared by the down and right edges
+        // (every term an integer below 2^24: the sign is exact; flags of same-sign
+        // edges are never used)
+        float uB[2][4];
         if constexpr (GAP) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(a.tg[j] - fabsf(rB[j][i] - rC[j][i]));
+                for (int i = 0; i < 4; ++i) uB[j][i] = fabsf(rB[j][i]) - a.tg[j];
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-uB[j][i] - fabsf(rC[j][i]));
             Dng = pack_flags(t);
         }
 #pragma unroll
@@ -797,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(a.tg[j] - fabsf(rB[j][i] - rn[j][i]));
+                for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-uB[j][i] - fabsf(rn[j][i]));
             Rng = pack_flags(t);
         }
         // neighbours' flag bytes across lanes
@@ -888,12 +925,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         // ---------------- ring writes and the output row ----------------
-        if (!YF || (row_z >= 0 && row_z <= H - 1)) zRing[(row_z & 7) * 32 + lane] = Z;
+        if constexpr (YF) {
+            if (row_z >= 0 && row_z <= H - 1) zRing[(row_z & 7) * 32 + lane] = Z;
+        } else {
+            const int sz = (k + 5) & 7;  // slot of row rho-3, and its mirror
+            zRing[sz * 32 + lane] = Z;
+            zRing[(sz + 8) * 32 + lane] = Z;
+        }
         if constexpr (HM) {
-            if (!YF || (row_e >= 0 && row_e <= H - 1)) {
-                uint32_t *erow = reinterpret_cast<uint32_t *>(eRing + (row_e & 7) * kERow + 4 + 8 * lane);
+            if constexpr (YF) {
+                if (row_e >= 0 && row_e <= H - 1) {
+                    uint32_t *erow = reinterpret_cast<uint32_t *>(eRing + (row_e & 7) * kERow + 4 + 8 * lane);
+                    erow[0] = e0;
+                    erow[1] = e1;
+                }
+            } else {
+                const int se = (k + 2) & 7;  // slot of row rho-6, and its mirror
+                uint32_t *erow = reinterpret_cast<uint32_t *>(eRing + se * kERow + 4 + 8 * lane);
+                uint32_t *emir = reinterpret_cast<uint32_t *>(eRing + (se + 8) * kERow + 4 + 8 * lane);
                 erow[0] = e0;
                 erow[1] = e1;
+                emir[0] = e0;
+                emir[1] = e1;
             }
             if constexpr (HM2) {
                 const int row_o = rho - 9;
@@ -923,7 +976,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         V = 0;
         if constexpr (!YF) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) zRing[k * 32 + lane] = 0;
+            for (int k = 0; k < 16; ++k) zRing[k * 32 + lane] = 0;
         }
         __syncwarp();
         float rX[2][4], rY[2][4];
@@ -942,9 +995,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&full[g % kS], (g / kS) & 1);
             }
             const int n = min(kR, rho_end - rho);
+            const unsigned char *cb = nullptr, *pb = nullptr;
+            chk_lo = in_lo;
+            chk_hi = in_hi;
+            if constexpr (!YF) {  // interior: the chunk is stage g_base + m (rho starts at plo)
+                const int m = (rho - it.plo) >> 3;
+                cb = ring + ((g_base + m) % kS) * kStageBytes + off_own;
+                pb = ring + ((g_base + m + kS - 1) % kS) * kStageBytes + off_own;
+                // The walk runs up to kLag - kHalo (+1) rows past phi, unclamped: rows of
+                // the item's staged boxes are image rows (or TMA zero fill), but a chunk
+                // past the last stage reads a slot no TMA filled for this item.  Its rows
+                // are all >= phi, so they only reach discarded outputs; skip their range
+                // check.
+                if (m >= it.nst) chk_lo = chk_hi = 0;
+            }
             for (int k = 0; k < n; k += 2) {  // x2: the centre / new r rows swap roles without moves
-                step(fix_tag, rho + k, rX, rY);
-                step(fix_tag, rho + k + 1, rY, rX);
+                step(fix_tag, rho + k, rX, rY, k, cb, pb);
+                step(fix_tag, rho + k + 1, rY, rX, k + 1, cb, pb);
             }
             // release ring stages that no later step reads (the E stage reads row rho-6)
             const int next_e = prow(rho + n - 6);
@@ -967,6 +1034,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         released = 0;
         const int xw = it.xo - kHaloX + warp * kWarpOut;  // image column of this warp's column 0
         x0 = xw + 4 * lane;
+        skind = (lane < 2 || lane >= 30 || x0 >= W) ? 0 : x0 + 3 < W ? 1 : 2;
+        obase = reinterpret_cast<char *>(a.out) + it.band * a.out_band_stride + (long long)(it.ys - a.o0) * a.out_pitch +
+                (long long)((IN16 && !MASKOUT) ? 2 : 1) * x0;
         fx.oobL = fx.oobR = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

@@ -32,6 +32,9 @@ __device__ __forceinline__ void op(uint32_t (&a)[CHAINS], uint32_t k1, uint32_t 
         if (OP == 15) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(x) : "r"(k1), "r"(k2));      // IMAD.HI + acc
         if (OP == 16) asm volatile("mul.rn.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));                   // FMUL
         if (OP == 17) asm volatile("add.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));                      // FADD
+        if (OP == 18) asm volatile("cvt.rn.f16x2.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));             // F2FP.F16.F32.PACK_AB
+        if (OP == 19) asm volatile("add.sat.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));                  // FADD.SAT
+        if (OP == 20) asm volatile("cvt.rn.bf16x2.f32 %0, %0, %1;" : "+r"(x) : "r"(k1));            // F2FP.BF16.F32.PACK_AB
         if (OP == 13) { int p; asm volatile("{.reg .pred q; setp.lt.s32 q, %1, %2; selp.b32 %0, 1, 0, q;}" : "=r"(p) : "r"(x), "r"(k1)); x += p; }  // ISETP+SEL+IADD
         a[c] = x;
     }
@@ -113,5 +116,12 @@ int main()
     run<7, 3>("HMNMX2 + FFMA");
     run<6, 3>("VIMNMX3.U32 + FFMA");
     run<8, 1>("SHFL + LOP3");
+    run<18, -1>("F2FP.F16 (cvt f16x2)");
+    run<20, -1>("F2FP.BF16 (cvt bf16x2)");
+    run<19, -1>("FADD.SAT");
+    run<18, 3>("F2FP.F16 + FFMA");
+    run<18, 1>("F2FP.F16 + LOP3");
+    run<18, 9>("F2FP.F16 + PRMT");
+    run<19, 1>("FADD.SAT + LOP3");
     return 0;
 }

@@ -509,13 +509,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // pixels, 2 the 1..3 pixels left of the image's right edge
     char *obase = nullptr;
     int skind = 0;
-    auto store = [&](int row, uint32_t o0, uint32_t o1) {
-        if (skind == 0) return;
+    // (partial stores only happen on general fix-up walks: interior and cheap
+    // column-edge walks have x0 + 3 < W on every lane they store)
+    auto store = [&](auto xf_tag, int row, uint32_t o0, uint32_t o1) {
+        constexpr bool kPartial = decltype(xf_tag)::value;
         char *orow = obase + (unsigned long long)(unsigned)(row - it.ys) * (unsigned)a.out_pitch;
         if (IN16 && !MASKOUT) {
             if (skind == 1) {
                 *reinterpret_cast<uint2 *>(orow) = make_uint2(o0, o1);
-            } else {
+            } else if (kPartial && skind == 2) {
                 uint16_t *p = reinterpret_cast<uint16_t *>(orow);
                 p[0] = (uint16_t)o0;
                 if (x0 + 1 < W) p[1] = (uint16_t)(o0 >> 16);
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b = prmt(o0, o1, 0x6420);
             if (skind == 1) {
                 *reinterpret_cast<uint32_t *>(orow) = b;
-            } else {
+            } else if (kPartial && skind == 2) {
                 uint8_t *p = reinterpret_cast<uint8_t *>(orow);
                 p[0] = (uint8_t)b;
                 if (x0 + 1 < W) p[1] = (uint8_t)(b >> 8);
@@ -955,12 +957,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     hrow[0] = o0;
                     hrow[1] = o1;
                 }
-                if (rho - 11 >= it.ys && rho - 11 < it.ye) store(rho - 11, q0, q1);
+                if (rho - 11 >= it.ys && rho - 11 < it.ye) store(std::bool_constant<XF>{}, rho - 11, q0, q1);
             } else {
-                if (rho - 9 >= it.ys && rho - 9 < it.ye) store(rho - 9, o0, o1);
+                if (rho - 9 >= it.ys && rho - 9 < it.ye) store(std::bool_constant<XF>{}, rho - 9, o0, o1);
             }
         } else {
-            if (row_e >= it.ys && row_e < it.ye) store(row_e, e0, e1);
+            if (row_e >= it.ys && row_e < it.ye) store(std::bool_constant<XF>{}, row_e, e0, e1);
         }
         __syncwarp();
     };

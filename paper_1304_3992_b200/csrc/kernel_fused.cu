@@ -508,12 +508,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // what this lane stores: 0 nothing (halo lane or right of the image), 1 four
     // pixels, 2 the 1..3 pixels left of the image's right edge
     char *obase = nullptr;
+    char *optr = nullptr;  // this lane's output pixel 0 in the row the current step outputs
     int skind = 0;
     // (partial stores only happen on general fix-up walks: interior and cheap
     // column-edge walks have x0 + 3 < W on every lane they store)
     auto store = [&](auto xf_tag, int row, uint32_t o0, uint32_t o1) {
         constexpr bool kPartial = decltype(xf_tag)::value;
-        char *orow = obase + (unsigned long long)(unsigned)(row - it.ys) * (unsigned)a.out_pitch;
+        (void)row;
+        char *orow = optr;
         if (IN16 && !MASKOUT) {
             if (skind == 1) {
                 *reinterpret_cast<uint2 *>(orow) = make_uint2(o0, o1);
@@ -964,6 +966,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
             if (row_e >= it.ys && row_e < it.ye) store(std::bool_constant<XF>{}, row_e, e0, e1);
         }
+        optr += a.out_pitch;
         __syncwarp();
     };
 
@@ -988,6 +991,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 4; ++i) rX[j][i] = rY[j][i] = 0.0f;
 
         const int rho_end = it.ye + kLag;
+        optr = obase - (long long)(kHalo + kLag) * a.out_pitch;  // output row of step rho = rho - kLag
         for (int rho = it.ys - kHalo; rho < rho_end; rho += kR) {
             // wait for the ring stages holding this chunk's input rows
             const int st = (prow(rho + kR - 1) - it.plo) >> 3;

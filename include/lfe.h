@@ -175,13 +175,15 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch_bytes
  * integer sums, additive over disjoint row ranges -- strips or ranks may be
  * combined by summing every field (e.g. an int64 all-reduce).  r_j is branch
  * j's integer LoG response (R3) with replicate padding at the true image edges
- * (R5); r_j^2 is split so no 64-bit sum overflows:
- * sum r_j^2 = r_sq_hi[j] * 2^24 + r_sq_lo[j].  72 bytes. */
+ * (R5); sum r_j^2 is carried as two non-negative parts so no 64-bit sum
+ * overflows: sum r_j^2 = r_sq_hi[j] * 2^24 + r_sq_lo[j] (partial sums over
+ * groups of pixels, each split at 2^24 before it is added; only the combined
+ * value is specified).  72 bytes. */
 typedef struct lfe_stats {
     int64_t n;           /* pixels                            */
     int64_t r_sum[2];    /* sum r_j                           */
-    int64_t r_sq_hi[2];  /* sum (r_j^2 >> 24)                 */
-    int64_t r_sq_lo[2];  /* sum (r_j^2 & (2^24 - 1))          */
+    int64_t r_sq_hi[2];  /* sum of (partial sum r_j^2) >> 24  */
+    int64_t r_sq_lo[2];  /* sum of (partial sum r_j^2) mod 2^24 */
     int64_t i_sum;       /* sum I                             */
     int64_t i_sq;        /* sum I^2                           */
 } lfe_stats;

@@ -8,8 +8,9 @@
 // with clamped (edge-replicated, R5) coordinates, both integer LoG responses
 // r_j are evaluated exactly (int32, |r| < 2^24 by R3) by per-column streaming
 // over the rows (symmetric pair sums, per-offset row partials), and every thread keeps
-// exact integer sums: n, sum r_j, sum r_j^2 split as (r^2 >> 24, r^2 & 2^24-1)
-// so that no 64-bit sum can overflow, sum I and sum I^2.  The block reduces them
+// exact integer sums per tile column (sum r_j in int32, sum r_j^2 in uint64, sum I),
+// added to its running totals with sum r_j^2 split as (s >> 24, s & 2^24-1) so
+// that no 64-bit sum can overflow (lfe.h: sum r^2 = r_sq_hi * 2^24 + r_sq_lo).  The block reduces them
 // and adds them to the caller's lfe_stats with 64-bit atomics -- integer sums,
 // so the result is independent of the order (deterministic).
 #include <cuda_runtime.h>
@@ -70,14 +71,22 @@ __global__ void __launch_bounds__(kThreads)
         const int tx = (int)(t % tiles_x), ty = (int)(t / tiles_x);
         const int x0 = tx * kTileW, y0 = g.o0 + ty * kTileH;
         __syncthreads();  // previous tile's readers are done
-        for (int i = threadIdx.x; i < THh * TWh; i += kThreads) {
-            const int vy = clampi(y0 - R + i / TWh, 0, Hv - 1);
-            const int vx = clampi(x0 - R + i % TWh, 0, W - 1);
+        // stage row by row: this thread's (clamped) columns are fixed for the whole tile
+        const int vxa = clampi(x0 - R + lx, 0, W - 1);
+        const int vxb = clampi(x0 - R + lx + kThreads, 0, W - 1);  // used when lx + kThreads < TWh
+        for (int yy = 0; yy < THh; ++yy) {
+            const int vy = clampi(y0 - R + yy, 0, Hv - 1);
             const Tin *row = reinterpret_cast<const Tin *>(reinterpret_cast<const char *>(g.in) + (int64_t)vy * g.in_pitch);
-            sI[i] = (uint16_t)row[vx];
+            sI[yy * TWh + lx] = (uint16_t)row[vxa];
+            if (lx + kThreads < TWh) sI[yy * TWh + lx + kThreads] = (uint16_t)row[vxb];
         }
         __syncthreads();
         const bool col_ok = x0 + lx < W;
+        // this tile column's sums: |sum r| < 32 * 2^24, sum r^2 < 32 * 2^48 = 2^53, sum I < 2^21
+        int32_t t0 = 0, t1 = 0;
+        unsigned long long u0 = 0, u1 = 0;
+        uint32_t ti = 0;
+        int tn = 0;
         int32_t acc[2][2 * R + 1];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -105,17 +114,13 @@ __global__ void __launch_bounds__(kThreads)
             if (i >= 2 * R && col_ok && y < g.o1) {
                 const int32_t r0 = acc[0][0], r1 = acc[1][0];
                 const uint32_t v = sI[(i - R) * TWh + lx + R];
-                ++n;
-                rs0 += r0;
-                rs1 += r1;
-                const unsigned long long s0 = (unsigned long long)((long long)r0 * r0);
-                const unsigned long long s1 = (unsigned long long)((long long)r1 * r1);
-                hi0 += s0 >> 24;
-                lo0 += s0 & 0xFFFFFFull;
-                hi1 += s1 >> 24;
-                lo1 += s1 & 0xFFFFFFull;
-                is += v;
-                iq += (unsigned long long)v * v;
+                ++tn;
+                t0 += r0;
+                t1 += r1;
+                u0 += (unsigned long long)((long long)r0 * r0);
+                u1 += (unsigned long long)((long long)r1 * r1);
+                ti += v;
+                iq += (unsigned long long)(v * v);
             }
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -124,6 +129,14 @@ __global__ void __launch_bounds__(kThreads)
                 acc[j][2 * R] = 0;
             }
         }
+        n += tn;
+        rs0 += t0;
+        rs1 += t1;
+        hi0 += u0 >> 24;
+        lo0 += u0 & 0xFFFFFFull;
+        hi1 += u1 >> 24;
+        lo1 += u1 & 0xFFFFFFull;
+        is += ti;
     }
     unsigned long long s[9] = {(unsigned long long)n,  (unsigned long long)rs0, (unsigned long long)rs1,
                                hi0, hi1, lo0, lo1, (unsigned long long)is, iq};

@@ -1,0 +1,7 @@
+# A/B/C... timing of several liblfe builds (abtest/liblfe_<v>.so) on one bench command; $1 = variants, rest = bench args
+V="$1"; shift
+for i in 1 2 3; do
+  for v in $V; do
+    LFE_LIB=$PWD/abtest/liblfe_$v.so python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu-baseline "$@" | python -c "import json,sys; d=json.load(sys.stdin); print('$v', d['ms_per_step'], d['roofline']['kernel_ms'])"
+  done
+done

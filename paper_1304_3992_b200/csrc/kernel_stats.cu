@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(kThreads)
         for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int k = 0; k <= 2 * R; ++k) acc[j][k] = 0;
+        constexpr int kU = 2 * R + 1;  // the pending-row shift has period 2R+1: unrolled, it costs no moves
+#pragma unroll kU
         for (int i = 0; i < THh; ++i) {  // input row y0 - R + i
             const uint16_t *sr = sI + i * TWh + lx + R;  // tile entries hold clamped values (R5)
             int32_t h[R + 1];

@@ -4,7 +4,7 @@
 // readings R21, R22 in DESIGN.md).
 //
 // One persistent grid walks the output rows [o0, o1) of a virtual image in
-// 32 x 128 tiles.  Each tile plus the LoG radius is staged in shared memory
+// 64 x 128 tiles.  Each tile plus the LoG radius is staged in shared memory
 // with clamped (edge-replicated, R5) coordinates, both integer LoG responses
 // r_j are evaluated exactly (int32, |r| < 2^24 by R3) by per-column streaming
 // over the rows (symmetric pair sums, per-offset row partials), and every thread keeps
@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kThreads = 128;  // one image column per thread
 constexpr int kTileW = 128;
-constexpr int kTileH = 32;
+constexpr int kTileH = 64;
 constexpr int kMaxR = kMaxMask / 2;
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -35,7 +35,7 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v)
     return v;
 }
 
-// R = the larger mask radius.  Each thread walks one column of a 32-row tile
+// R = the larger mask radius.  Each thread walks one column of a 64-row tile
 // down its rows: per input row it forms the symmetric pair sums
 // h_b = I(x-b) + I(x+b) (h_0 = I(x)), the per-offset row partials
 // p_a = sum_b q(a, b) h_b of each 8-fold symmetric mask (the smaller mask is
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads)
         }
         __syncthreads();
         const bool col_ok = x0 + lx < W;
-        // this tile column's sums: |sum r| < 32 * 2^24, sum r^2 < 32 * 2^48 = 2^53, sum I < 2^21
+        // this tile column's sums: |sum r| < 64 * 2^24 = 2^30, sum r^2 < 64 * 2^48 = 2^54, sum I < 2^22
         int32_t t0 = 0, t1 = 0;
         unsigned long long u0 = 0, u1 = 0;
         uint32_t ti = 0;

@@ -803,3 +803,30 @@ def test_c4_bands_dealt_to_ranks(world):
         got = out.cpu().numpy()
     for b in range(B):
         assert_same(got[b], O.run(img[b], _oparams(p)), f"band {b}")
+
+
+@pytest.mark.parametrize("where", ["interior", "first_row", "last_row", "last_col", "none"])
+def test_fused_range_check_and_rows_past_the_call(where):
+    """The fused kernel's ERANGE check (R20) sees every pixel of the call's rows,
+    and nothing beyond them: rows after the image in the same allocation hold
+    out-of-range values (interior walks run a few rows past their last staged
+    row, unclamped; the tensor map ends at the image), and the output still
+    equals the oracle."""
+    H, W = 600, 1400
+    img = scenes.scene_c3(size=W, height=H)
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    big = torch.full((H + 24, W), 0xFFFF, dtype=torch.uint16, device="cuda")
+    big[:H].copy_(torch.from_numpy(img))
+    bad = {"interior": (300, 700), "first_row": (0, 5), "last_row": (H - 1, W // 2), "last_col": (250, W - 1)}
+    if where != "none":
+        big[bad[where]] = 1024
+    out = torch.zeros((H, W), dtype=torch.uint16, device="cuda")
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_KERNEL, lfe.LFE_KERNEL_FUSED)
+        ctx.extract(big[:H], out)
+        err = ctx.last_async_error()
+    if where != "none":
+        assert err == lfe.LFE_ERANGE
+    else:
+        assert err == lfe.LFE_OK
+        assert_same(out.cpu().numpy(), O.run(img, _oparams(p)), "rows past the call")

@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--kernel", choices=["auto", "staged", "fused"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify", action="store_true",
+                    help="after timing, check every rank's owned output rows against a whole-scene "
+                         "extraction on its own GPU (bit-exact); adds \"verify\" to the line")
     ap.add_argument("--size", type=int, default=12000, help="scene side (default: c3's 12000)")
     ap.add_argument("--tile", type=str, default="", help="TWxTH override (tuning only)")
     ap.add_argument("--median2", type=int, default=0, choices=[0, 3, 5, 7],
@@ -78,6 +81,15 @@ def halo_rows(p):
     return h
 
 
+def _backend_name():
+    try:
+        import torch.distributed as dist
+        b = dist.get_backend() if dist.is_initialized() else "nccl"
+    except Exception:
+        b = "nccl"
+    return "NCCL" if b == "nccl" else f"{b} (host-staged; ranks sharing a GPU: test hook, not a measurement)"
+
+
 def config_dict(size, world, p):
     hm = "5x5 hybrid median" + (f" + {p.median_window2}x{p.median_window2} second level" if p.median_window2 else "")
     zc = (f"ZC (adaptive gap {p.zc_threshold[0]} x global std of r, statistics pre-pass)" if p.adaptive
@@ -86,7 +98,8 @@ def config_dict(size, world, p):
         "workload": f"c3: {size}x{size} uint16 (10-bit) synthetic Cartosat-1-like PAN scene, "
                     f"dual LoG (sigma 0.5, 20; 5x5) + {zc} + 5x5 std gate (T=0.3) + OR + {hm}, extract",
         "width": size, "height": size, "bit_depth": 10, "bands": 1,
-        "parallelism": f"row strips x{world}, {halo_rows(p)}-row NCCL halo exchange" if world > 1 else "single GPU",
+        "parallelism": (f"row strips x{world}, {halo_rows(p)}-row {_backend_name()} halo exchange" if world > 1
+                        else "single GPU"),
         "l2": "inputs larger than L2 (288 MB in + 288 MB out per step > 126 MB L2); no flush",
         "params": {"sigma": list(p.sigma), "log_size": list(p.log_size), "zc_threshold": list(p.zc_threshold),
                    "std_source": "zc", "std_window": p.std_window, "std_threshold": list(p.std_threshold),
@@ -180,14 +193,35 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "lfe" and os.environ.get("LFE_BENCH_SHARE_GPUS"):
+        # test hook only: fold ranks onto the visible GPUs (exercises the N > 1 step on one GPU)
+        import torch
+        local %= max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
         if args.impl == "lfe":
             import torch
             torch.cuda.set_device(local)  # before the first NCCL call (P2P needs the device set)
-        dist.init_process_group("nccl" if args.impl == "lfe" else "gloo")
+        share = args.impl == "lfe" and os.environ.get("LFE_BENCH_SHARE_GPUS")
+        # NCCL refuses two ranks on one GPU: the test hook runs the same step over gloo
+        # (shard.py stages the halo rows through host memory)
+        dist.init_process_group("nccl" if args.impl == "lfe" and not share else "gloo")
         dist.barrier()  # a full-group collective first: batch_isend_irecv's first call must not be partial
     return world, rank, local
+
+
+def all_reduce_dev(t, op=None):
+    """all_reduce of a device tensor; through host memory when the group is gloo
+    (the one-GPU test hook)."""
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and dist.get_backend() == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+    return t
 
 
 def cpu_baseline(img, p, rows=None):
@@ -363,7 +397,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        all_reduce_dev(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
         dist.barrier()
     ctx.check()
@@ -398,19 +432,29 @@ def main():
         e2e_s = time.perf_counter() - tw0
         if world > 1:
             tt = torch.tensor([e2e_s], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            all_reduce_dev(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt.item())
         nst = (erows + strip_rows - 1) // strip_rows
         h2d_rows = sum(min(erows, (i + 1) * strip_rows + halo) - max(0, i * strip_rows - halo) for i in range(nst))
         h2d_tot = torch.tensor([h2d_rows * W * 2, erows * W * 2], dtype=torch.int64, device=dev)
         if world > 1:
-            dist.all_reduce(h2d_tot)
+            all_reduce_dev(h2d_tot)
         h2d_b, d2h_b = (int(v) for v in h2d_tot.tolist())
         e2e = {"value": round(H * W * K / e2e_s / 1e6, 3), "unit": UNIT,
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                "how": "lfe_extract_host on pinned host buffers: strip-pipelined H2D -> kernel -> D2H on 3 streams, "
                       f"{strip_rows}-row strips, wall clock of {K} synchronous calls (max over ranks); each rank "
                       "streams its strip plus its neighbours' halo rows"}
+
+    verify = None
+    if args.verify:  # the last timed step's owned rows == a whole-scene extraction on this GPU
+        whole = ctx.extract(torch.from_numpy(img).to(dev))
+        ctx.check()
+        bad = torch.tensor([int((out != whole[shard.a:shard.b]).sum().item())], dtype=torch.int64, device=dev)
+        if world > 1:
+            all_reduce_dev(bad)
+        verify = {"bit_exact_vs_whole_scene": int(bad.item()) == 0, "differing_pixels": int(bad.item())}
+        del whole
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -438,6 +482,8 @@ def main():
                               "(AWiFS, Table 7, PAPER.md:236)",
                               "this_gpu_vs_oracle": round(value / cpu["value"], 1) if cpu else None},
         }
+        if verify is not None:
+            line["verify"] = verify
         iss = ncu_issue()
         if iss and not p.adaptive and not p.median_window2:
             # the binding resource: instruction issue, 4 warp-instructions

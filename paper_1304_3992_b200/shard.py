@@ -69,6 +69,8 @@ class StripShard:
         works to wait on.  Owned rows are not modified."""
         import torch
         import torch.distributed as dist
+        if self.buf.is_cuda and dist.get_backend(group) == "gloo":
+            return self._exchange_host_staged(group)
         h, ops = self.halo, []
         # rows travel as bytes: NCCL has no uint16 type, and a byte view of whole
         # contiguous rows is the same memory
@@ -82,13 +84,49 @@ class StripShard:
             ops.append(dist.P2POp(dist.irecv, B[e:e + self.hb], self.rank + 1, group))
         return dist.batch_isend_irecv(ops) if ops else []
 
+    def _exchange_host_staged(self, group):
+        """The same exchange for a gloo group over device buffers (no NCCL, e.g.
+        several ranks sharing one GPU in tests): rows go through host memory; the
+        returned works copy the received rows into the device buffer on wait()."""
+        import torch
+        import torch.distributed as dist
+        h, ops, recv = self.halo, [], []
+        B = self.buf if self.buf.dtype == torch.uint8 else self.buf.view(torch.uint8)
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, B[self.ha:self.ha + h].cpu(), self.rank - 1, group))
+            r = torch.empty_like(B[0:self.ha], device="cpu")
+            ops.append(dist.P2POp(dist.irecv, r, self.rank - 1, group))
+            recv.append((B[0:self.ha], r))
+        if self.rank < self.world - 1:
+            e = self.ha + self.rows
+            ops.append(dist.P2POp(dist.isend, B[e - h:e].cpu(), self.rank + 1, group))
+            r = torch.empty_like(B[e:e + self.hb], device="cpu")
+            ops.append(dist.P2POp(dist.irecv, r, self.rank + 1, group))
+            recv.append((B[e:e + self.hb], r))
+        works = dist.batch_isend_irecv(ops) if ops else []
+
+        class _Staged:
+            def wait(self_inner):
+                for w in works:
+                    w.wait()
+                for dst, src in recv:
+                    dst.copy_(src)
+                return True
+
+        return [_Staged()] if works else []
+
     def allreduce_stats(self, t_stats, group=None):
         """Adaptive thresholds (NEXT-2): the 9 exact int64 sums of lfe_stats are
         additive over disjoint row ranges, so one SUM all-reduce of every rank's
         owned-row partial gives the whole-image statistics (bit-exact)."""
         import torch.distributed as dist
         if self.world > 1:
-            dist.all_reduce(t_stats, op=dist.ReduceOp.SUM, group=group)
+            if t_stats.is_cuda and dist.get_backend(group) == "gloo":
+                h = t_stats.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+                t_stats.copy_(h)
+            else:
+                dist.all_reduce(t_stats, op=dist.ReduceOp.SUM, group=group)
         return t_stats
 
     def edge_flags(self) -> int:

@@ -830,3 +830,23 @@ def test_fused_range_check_and_rows_past_the_call(where):
     else:
         assert err == lfe.LFE_OK
         assert_same(out.cpu().numpy(), O.run(img, _oparams(p)), "rows past the call")
+
+
+def test_bench_two_ranks_on_one_gpu_verify():
+    """bench.py's N > 1 step (row strips, halo exchange, interior band overlapped
+    with the exchange, boundary bands, max-over-ranks timing) run as 2 ranks
+    sharing this GPU over gloo (LFE_BENCH_SHARE_GPUS; NCCL refuses duplicate
+    GPUs), with --verify: every rank's owned rows equal a whole-scene extraction."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LFE_BENCH_SHARE_GPUS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--size", "2048", "--no-cpu-baseline", "--verify"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["verify"]["bit_exact_vs_whole_scene"], line

@@ -1154,9 +1154,9 @@ bool interval_of(uint64_t lut, int L, int *lo, int *hi)
 // search on the per-CTA cost cap balances the CTAs.  Constants fitted to a
 // per-CTA globaltimer trace (LFE_DEBUG_TIMING, scripts/partition_fit.py).
 namespace part {
-constexpr double kPiece = 16.0;      // row-equivalents per piece (pipeline warm-up)
-constexpr double kEdgePiece = 5.0;    // extra for an edge-row piece (general path; ~0 once paired)
-constexpr double kEdgeCol = 1.066;   // column-edge group, cheap path (W % 4 == 0)
+constexpr double kPiece = 19.5;      // row-equivalents per piece (pipeline warm-up)
+constexpr double kEdgePiece = 2.7;    // extra for an edge-row piece (general path)
+constexpr double kEdgeCol = 1.048;   // column-edge group, cheap path (W % 4 == 0)
 constexpr double kEdgeColGen = 1.40; // column-edge group, general path
 
 // per-CTA cost of units [u0, u1); `paired`: the cost of one CTA of a pair

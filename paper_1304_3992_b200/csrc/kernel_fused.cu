@@ -797,16 +797,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rC[j][i]);
         const uint32_t NC = pack_flags(t);
+        // Three-way sign of an edge sum s = r_p + r_n in ONE flag op: sat(0.5 s + 0.5) is
+        // 0, 0.5 or 1 for s < 0, s = 0, s > 0 (evaluated as fma(r_n, 0.5, tB) with
+        // tB = 0.5 r_p + 0.5: both exact, |r| < 2^24 by R3, so a tie gives exactly 0.5).
+        // pack_flags' weights then put s > 0 at bit 3/7 and the tie at bit 2/6, and
+        // s < 0 = neither.  Words carry garbage outside bits 3/7 only where every use
+        // ANDs them with a sign word.
+        float tB[2][4];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rB[j][i] - rC[j][i]);
-        const uint32_t Dm = pack_flags(t);
+            for (int i = 0; i < 4; ++i) tB[j][i] = fmaf(rB[j][i], 0.5f, 0.5f);
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rB[j][i] + rC[j][i]);
-        const uint32_t Dp = pack_flags(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(fmaf(rC[j][i], 0.5f, tB[j][i]));
+        const uint32_t Dp = pack_flags(t);           // bit 3/7: r_B + r_C > 0 (bit 2/6: tie)
+        const uint32_t Dm = ~(Dp | (Dp << 1));        // bit 3/7: r_B + r_C < 0
         uint32_t Dng = 0, Rng = 0;
         // gap failure on an edge between opposite signs: |r_p| + |r_n| < t (R9), as
         // sat(-(u_p + |r_n|)) with u_p = |r_p| - t shared by the down and right edges
@@ -827,13 +834,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rB[j][i] - rn[j][i]);
-        const uint32_t Rm = pack_flags(t);
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rB[j][i] + rn[j][i]);
-        const uint32_t Rp = pack_flags(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(fmaf(rn[j][i], 0.5f, tB[j][i]));
+        const uint32_t Rp = pack_flags(t);           // bit 3/7: r_B + r_right > 0 (bit 2/6: tie)
+        const uint32_t Rm = ~(Rp | (Rp << 1));        // bit 3/7: r_B + r_right < 0
         if constexpr (GAP) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)

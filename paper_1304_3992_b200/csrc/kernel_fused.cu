@@ -787,16 +787,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (XQ) rn[j][3] = isR ? rB[j][3] : rn[j][3];
         }
         float t[2][4];
+        // signs of r_C the same way: sat(0.5 r + 0.5) = 0 / 0.5 / 1 for r < 0 / r = 0 / r > 0
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(rC[j][i]);
-        const uint32_t PC = pack_flags(t);
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(-rC[j][i]);
-        const uint32_t NC = pack_flags(t);
+            for (int i = 0; i < 4; ++i) t[j][i] = __saturatef(fmaf(rC[j][i], 0.5f, 0.5f));
+        const uint32_t PC = pack_flags(t);           // bit 3/7: r_C > 0 (bit 2/6: r_C = 0)
+        const uint32_t NC = ~(PC | (PC << 1));        // bit 3/7: r_C < 0
         // Three-way sign of an edge sum s = r_p + r_n in ONE flag op: sat(0.5 s + 0.5) is
         // 0, 0.5 or 1 for s < 0, s = 0, s > 0 (evaluated as fma(r_n, 0.5, tB) with
         // tB = 0.5 r_p + 0.5: both exact, |r| < 2^24 by R3, so a tie gives exactly 0.5).
@@ -872,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             XG = NA | NC | NR | NL;
             YG = PA | PC | PR | PL;
         }
-        uint32_t Z = (PB & ~X & XG) | (NB & ~Y & YG);
+        uint32_t Z = ((PB & ~X & XG) | (NB & ~Y & YG)) & 0x88888888u;  // (flag words are clean at bits 3/7 only)
         // a pixel exactly at zero: a positive and a negative neighbour (R6)
         const uint32_t z0 = ~PB & ~NB & (PA | PC | PR | PL) & (NA | NC | NR | NL) & zmask;
         if constexpr (!GAP) {

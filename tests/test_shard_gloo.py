@@ -49,7 +49,7 @@ def test_bands_partition_each_strip():
             assert bands[0][5] is False
 
 
-def _worker(rank, world, port, H, W, hm, q):
+def _worker(rank, world, port, H, W, hm, q, staged=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -59,7 +59,9 @@ def _worker(rank, world, port, H, W, hm, q):
         sh = StripShard(H, W, rank, world, halo)
         buf = sh.alloc(torch.uint8, "cpu")
         sh.load_owned(img)
-        for w in sh.exchange():
+        # staged: the host-staged variant used for gloo groups over device buffers
+        # (the one-GPU N > 1 bench hook), here exercised on CPU buffers
+        for w in (sh._exchange_host_staged(None) if staged else sh.exchange()):
             w.wait()
         # received halos equal the neighbours' boundary rows
         if sh.ha:
@@ -78,13 +80,14 @@ def _worker(rank, world, port, H, W, hm, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,H,hm", [(2, 96, True), (3, 61, True), (2, 40, False)])
-def test_gloo_strips_reproduce_whole_image(world, H, hm):
+@pytest.mark.parametrize("world,H,hm,staged", [(2, 96, True, False), (3, 61, True, False), (2, 40, False, False),
+                                               (3, 61, True, True)])
+def test_gloo_strips_reproduce_whole_image(world, H, hm, staged):
     W = 72
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, hm, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, hm, q, staged)) for r in range(world)]
     for pr in procs:
         pr.start()
     got = [q.get(timeout=240) for _ in range(world)]

@@ -28,6 +28,17 @@ lfe_status lfe_test_validate(const lfe_params *p);
 lfe_status lfe_test_response(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
                              int32_t height, int32_t branch, void *d_r, void *cuda_stream);
 
+/* The fused kernel with its LoG stage replaced by INJECTED responses, so the
+ * zero-crossing rule (R6-R9), the std gate (Eq. 2, R10-R13) and
+ * the merge can be checked exhaustively: for a W x H uint16 device image I,
+ * branch 0 uses r_0(y, x) = I(min(y + 2, H - 1), x) - 32768 and branch 1
+ * r_1 = -r_0 (row offset 2 = the kernel's LoG lag).  The ctx must have
+ * bit_depth 16, hybrid_median 0, out_mode LFE_OUT_MASK and no 3x3 re-check;
+ * d_out is uint8 0/255.  Both pitches and bases 16-byte aligned.  Enqueued on
+ * cuda_stream.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+lfe_status lfe_test_extract_r(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
+                              int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

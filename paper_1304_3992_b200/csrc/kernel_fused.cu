@@ -413,7 +413,10 @@ __host__ __device__ constexpr int warp_bytes(int hml) { return kEBytes + kZBytes
 
 // HML: hybrid-median levels -- 0 none, 1 the 5x5 filter, 2 the 5x5 filter followed
 // by a 3x3 one on its output (the water pipeline's second level, R17)
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC>
+// RT (test only, lfe_test_extract_r): the LoG stage is replaced by r_0(y) = I(y+2) - 32768,
+// r_1 = -r_0, so the zero-crossing / std / merge stages can be checked exhaustively on
+// injected responses
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool RT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ FusedArgs a, int *err_flag)
 {
@@ -746,6 +749,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (XQ) I[7] = isR ? I[5] : I[7];
 
         // ---------------- LoG x 2, streaming over rows ----------------
+        if constexpr (RT) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                rC[0][i] = I[i + 2] - 32768.0f;
+                rC[1][i] = 32768.0f - I[i + 2];
+            }
+        } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float x = I[i + 2], h1 = I[i + 1] + I[i + 3], h2 = I[i] + I[i + 4];
@@ -761,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc[j][2][i] = acc[j][3][i] + B;
                 acc[j][3][i] = C;
             }
+        }
         }
         const int row_r = rho - 2;
         if constexpr (XF) {
@@ -1277,10 +1288,10 @@ constexpr size_t fused_smem()
     return kHdr + (size_t)kS * nbox * (IN16 ? 232 * 2 : 480) * kR + (size_t)kWarps * warp_bytes(HML);
 }
 
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool RT = false>
 cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC>;
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, RT>;
     constexpr size_t smem = fused_smem<IN16, HML>();
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)
@@ -1344,7 +1355,7 @@ bool fused_supports(const KParams &kp, int bit_depth)
 }
 
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h, int *err_flag,
-                         cudaStream_t s)
+                         cudaStream_t s, bool rtest)
 {
     (void)tile_w;
     FusedArgs fa;
@@ -1400,6 +1411,10 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     // the GAP variant is exact for t = 0 as well; the two-level filter and the 3x3
     // re-check only have that one
     const bool gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || hml == 2 || rc;
+    if (rtest) {  // test entry: u16 input, no median, mask output, the GAP variant
+        if (!in16 || hml != 0 || !mask || rc) return cudaErrorNotSupported;
+        return launch_t<true, 0, true, true, false, true>(fa, map, err_flag, s);
+    }
 #define LFE_DISPATCH(A, B, C, D, E) \
     if (in16 == A && hml == B && mask == C && gap == D && rc == E) return launch_t<A, B, C, D, E>(fa, map, err_flag, s);
     LFE_DISPATCH(true, 1, false, true, false)

@@ -755,6 +755,26 @@ lfe_status lfe_test_response(lfe_ctx *c, const void *d_in, int64_t in_pitch, int
     return LFE_OK;
 }
 
+lfe_status lfe_test_extract_r(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
+                              int64_t out_pitch, void *stream)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (c->p.bit_depth != 16 || c->p.hybrid_median || c->p.out_mode != LFE_OUT_MASK || c->kp.recheck[0] ||
+        c->kp.recheck[1])
+        return fail(LFE_EUNSUPPORTED, "test_extract_r needs bit_depth 16, no median, MASK output, no 3x3 re-check");
+    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
+    if (st != LFE_OK) return st;
+    if (((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out) | (uintptr_t)in_pitch |
+          (uintptr_t)out_pitch) & 15u) != 0 || !fused_supports(c->kp, c->p.bit_depth))
+        return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
+    st = check_bound_device(c);
+    if (st != LFE_OK) return st;
+    Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H};
+    cudaError_t e = launch_fused(c->kp, g, true, c->cfg.tile_w, c->cfg.tile_h, c->d_err, (cudaStream_t)stream, true);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return LFE_OK;
+}
+
 void lfe_destroy(lfe_ctx *c)
 {
     if (!c) return;

@@ -74,7 +74,7 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
                           int *err_flag, cudaStream_t s);
 // err_flag[0] = sticky ERANGE flag, err_flag[1] = scratch work counter (fused kernel)
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
-                         int *err_flag, cudaStream_t s);
+                         int *err_flag, cudaStream_t s, bool rtest = false);
 bool fused_supports(const KParams &kp, int bit_depth);
 // test entry: branch j's response for every pixel of a whole image (int32 or float bits)
 cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int branch, void *d_r, cudaStream_t s);

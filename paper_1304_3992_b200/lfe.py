@@ -84,7 +84,7 @@ EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows"
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
            "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
            "lfe_set_stats", "lfe_get_thresholds", "lfe_extract_bands"]
-TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response"]  # include/lfe_test.h
+TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response", "lfe_test_extract_r"]  # include/lfe_test.h
 
 
 def load():
@@ -139,6 +139,8 @@ def load():
     L.lfe_test_validate.restype = st
     L.lfe_test_response.argtypes = [P, P, I64, I32, I32, I32, P, P]
     L.lfe_test_response.restype = st
+    L.lfe_test_extract_r.argtypes = [P, P, I64, I32, I32, P, I64, P]
+    L.lfe_test_extract_r.restype = st
     _lib = L
     return L
 
@@ -432,6 +434,15 @@ class Context:
         _check(load().lfe_test_response(self.handle, pi, pin, W, H, branch, out.data_ptr(), self._stream(stream)),
                "lfe_test_response")
         return out
+
+    def test_extract_r(self, t_in, t_out, stream=None):
+        """lfe_test_extract_r: the fused kernel on injected responses (include/lfe_test.h)."""
+        pi, pin = self._torch_img(t_in, "input")
+        po, pout = self._torch_img(t_out, "output")
+        H, W = t_in.shape
+        _check(load().lfe_test_extract_r(self.handle, pi, pin, W, H, po, pout, self._stream(stream)),
+               "lfe_test_extract_r")
+        return t_out
 
     def last_async_error(self, stream=None) -> int:
         return lfe_last_async_error(self.handle, self._stream(stream))

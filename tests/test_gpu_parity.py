@@ -850,3 +850,63 @@ def test_bench_two_ranks_on_one_gpu_verify():
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["verify"]["bit_exact_vs_whole_scene"], line
+
+
+def _extract_r_case(r0: np.ndarray, t_int, T: float):
+    """The fused kernel on injected responses r_0 (and r_1 = -r_0) through
+    lfe_test_extract_r, against the oracle's zero crossing (R*), std gate on the
+    ZC image and OR merge of the same responses."""
+    H, W = r0.shape
+    bd = 16
+    thr = []
+    for j, s in enumerate((0.5, 20.0)):
+        _, F = O.mask_int(s, 5, bd)
+        x = (t_int[j] - 0.5) / (2.0 ** F * (2 ** bd - 1)) if t_int[j] > 0 else 0.0
+        assert O.zc_threshold_int(x, F, bd) == t_int[j]
+        thr.append(x)
+    # the kernel reads r_0(y) = I(min(y + 2, H - 1)) - 32768: rows 0, 1 of I are unused
+    I = np.full((H, W), 32768, np.int64)
+    I[2:] = r0[:H - 2] + 32768
+    r = I[np.minimum(np.arange(H) + 2, H - 1)] - 32768   # what the kernel sees (last two rows replicated)
+    p = lfe.Params(bit_depth=bd, hybrid_median=False, out_mode=lfe.LFE_OUT_MASK, zc_threshold=tuple(thr),
+                   std_threshold=(T, T))
+    d = _pitched((H, W), torch.uint16)
+    d.copy_(torch.from_numpy(I.astype(np.uint16)))
+    out = _pitched((H, W), torch.uint8)
+    with lfe.Context(p) as ctx:
+        ctx.test_extract_r(d, out)
+        ctx.check()
+    keep = []
+    for j, rj in enumerate((r, -r)):
+        Z = O.zero_crossing(rj, t_int[j])
+        keep.append(O.std_gate(Z, Z, 5, T))
+    want = O.merge(keep[0], keep[1], I.astype(np.uint16), 1).astype(np.uint8)
+    assert_same(out.cpu().numpy(), want, f"injected responses t={t_int} T={T}")
+
+
+@pytest.mark.parametrize("t_int", [(0, 0), (1, 0), (2000, 3999), (4000, 4001), (6001, 2000)])
+def test_fused_zero_crossing_exhaustive_crosses(t_int):
+    """Every 5-pixel cross with centre and 4-neighbour values in {-3, -1, 0, 1, 3}
+    x 1000 (5^5 = 3125 cases, SURVEY.md 8(c) ZC pins), each alone in a 5x5 cell,
+    through the fused kernel's bit-sliced rule R* (branch 1 sees the negated
+    responses), with gap thresholds below, at and above every reachable gap."""
+    vals = np.array([-3, -1, 0, 1, 3], np.int64) * 1000
+    cells = np.array(list(itertools.product(range(5), repeat=5)))
+    n = 56  # 56 x 56 >= 3125 cells
+    r0 = np.zeros((5 * n + 6, 5 * n), np.int64)
+    for k, (c, u, d_, l, rr) in enumerate(cells):
+        y, x = 2 + 5 * (k // n) + 2, 5 * (k % n) + 2
+        r0[y, x] = vals[c]
+        r0[y - 1, x], r0[y + 1, x], r0[y, x - 1], r0[y, x + 1] = vals[u], vals[d_], vals[l], vals[rr]
+    _extract_r_case(r0, t_int, 0.0)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fused_zero_crossing_dense_random_responses(seed):
+    """Dense random responses from a small value set (many ties, zero pixels and
+    gaps at the threshold) over an image with both column edges and edge-row
+    pieces; std threshold 0.3."""
+    rng = np.random.default_rng(4000 + seed)
+    H, W = 203, 456
+    r0 = rng.choice(np.array([-5, -3, -2, -1, 0, 0, 1, 2, 3, 5], np.int64), size=(H, W)) * 997
+    _extract_r_case(r0, (3 * 997, 4 * 997 + 1), 0.3)

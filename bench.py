@@ -210,6 +210,17 @@ def dist_setup(args):
     return world, rank, local
 
 
+def host_strip_cuts(H, S):
+    """The row cuts lfe_extract_host streams (lfe_host.cu host_strip_cuts): S-row
+    strips, with S/4- and S/2-row strips at both ends when more than 4 strips."""
+    q, hf = max(1, S // 4), max(1, S // 2)
+    if H <= 4 * S or q == hf:
+        return list(range(0, H, S)) + [H]
+    mid = H - 2 * (q + hf)
+    n = -(-mid // S)
+    return [0, q, q + hf] + [q + hf + mid * k // n for k in range(1, n)] + [H - q - hf, H - q, H]
+
+
 def all_reduce_dev(t, op=None):
     """all_reduce of a device tensor; through host memory when the group is gloo
     (the one-GPU test hook)."""
@@ -434,8 +445,8 @@ def main():
             tt = torch.tensor([e2e_s], device=dev)
             all_reduce_dev(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt.item())
-        nst = (erows + strip_rows - 1) // strip_rows
-        h2d_rows = sum(min(erows, (i + 1) * strip_rows + halo) - max(0, i * strip_rows - halo) for i in range(nst))
+        cuts = host_strip_cuts(erows, strip_rows)
+        h2d_rows = sum(min(erows, b + halo) - max(0, a - halo) for a, b in zip(cuts, cuts[1:]))
         h2d_tot = torch.tensor([h2d_rows * W * 2, erows * W * 2], dtype=torch.int64, device=dev)
         if world > 1:
             all_reduce_dev(h2d_tot)

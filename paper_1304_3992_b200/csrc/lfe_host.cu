@@ -13,6 +13,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <new>
+#include <vector>
 
 #include "lfe.h"
 #include "lfe_internal.h"
@@ -640,6 +641,28 @@ static lfe_status host_prepare(lfe_ctx *c, size_t in_bytes, size_t out_bytes)
     return LFE_OK;
 }
 
+// Row ranges of the streamed strips: at most S rows each.  When the image spans
+// more than 4 strips, the first and last two are S/4 and S/2 rows, so the
+// pipeline fills (first H2D + kernel before the first D2H can start) and drains
+// (last kernel + D2H) on short strips; the middle is split evenly.
+static std::vector<int> host_strip_cuts(int H, int S)
+{
+    std::vector<int> cut{0};
+    const int q = S / 4 > 0 ? S / 4 : 1, hf = S / 2 > 0 ? S / 2 : 1;
+    if (H <= 4 * S || q == hf) {
+        for (int a = S; a < H; a += S) cut.push_back(a);
+    } else {
+        const int mid = H - 2 * (q + hf), n = (mid + S - 1) / S;
+        cut.push_back(q);
+        cut.push_back(q + hf);
+        for (int k = 1; k < n; ++k) cut.push_back(q + hf + (int)((long long)mid * k / n));
+        cut.push_back(H - q - hf);
+        cut.push_back(H - q);
+    }
+    cut.push_back(H);
+    return cut;
+}
+
 lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int32_t W, int32_t H, void *h_out,
                             int64_t out_pitch)
 {
@@ -655,14 +678,15 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
     st = host_prepare(c, dpi * (size_t)(S + 2 * h), dpo * (size_t)S);
     if (st != LFE_OK) return st;
     cudaStream_t sh = c->st[0], sc = c->st[1], sd = c->st[2];
-    const int nstrips = (H + S - 1) / S;
+    const std::vector<int> cut = host_strip_cuts(H, S);
+    const int nstrips = (int)cut.size() - 1;
     if (c->p.adaptive) {  // NEXT-2: stream the image once for the whole-image statistics
         st = stats_buffers(c);
         if (st != LFE_OK) return st;
         cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), sc);
         for (int i = 0; i < nstrips; ++i) {
             const int b = i % kHostBuffers;
-            const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
+            const int a0 = cut[i], a1 = cut[i + 1];
             const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
             if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);
             cudaError_t e = copy_rows(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
@@ -687,7 +711,7 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
     if (ndbg) cudaEventRecord(dev[6 * ndbg], sh);
     for (int i = 0; i < nstrips; ++i) {
         const int b = i % kHostBuffers;
-        const int a0 = i * S, a1 = a0 + S < H ? a0 + S : H;
+        const int a0 = cut[i], a1 = cut[i + 1];
         const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;
         if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);  // input buffer free
         if (ndbg) cudaEventRecord(dev[6 * i + 0], sh);

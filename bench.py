@@ -454,7 +454,7 @@ def main():
         e2e = {"value": round(H * W * K / e2e_s / 1e6, 3), "unit": UNIT,
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                "how": "lfe_extract_host on pinned host buffers: strip-pipelined H2D -> kernel -> D2H on 3 streams, "
-                      f"{strip_rows}-row strips, wall clock of {K} synchronous calls (max over ranks); each rank "
+                      f"{strip_rows}-row strips ({strip_rows // 4} and {strip_rows // 2} rows at both ends), wall clock of {K} synchronous calls (max over ranks); each rank "
                       "streams its strip plus its neighbours' halo rows"}
 
     verify = None

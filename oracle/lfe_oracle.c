@@ -116,11 +116,19 @@ int lfo_mask_int(double sigma, int n, int bit_depth, int32_t *q, int *F_out)
     return -1;
 }
 
+/* ceil(x) as an int64 threshold; x beyond int64 saturates (every gap is < 2^25,
+ * R3, so a saturated t still rejects every crossing, as the exact t would). */
+static int64_t lfo_ceil_threshold(double x)
+{
+    if (x >= 0x1p62) return (int64_t)1 << 62;
+    return (int64_t)ceil(x);
+}
+
 /* ZC gap threshold in integer response units (R9): t = ceil(thr * 2^F * M). */
 int64_t lfo_zc_threshold_int(double thr, int F, int bit_depth)
 {
     double M = (double)(((int64_t)1 << bit_depth) - 1);
-    return (int64_t)ceil(thr * ldexp(1.0, F) * M);
+    return lfo_ceil_threshold(thr * ldexp(1.0, F) * M);
 }
 
 /* ------------------------------------------------------------------ */
@@ -491,7 +499,7 @@ double lfo_std_of_intensity(const uint16_t *I, size_t N)
 }
 
 /* R21: adaptive ZC gap threshold in response units, t = ceil(k * sigma_r) */
-int64_t lfo_adaptive_zc_threshold(double k, double sigma_r) { return (int64_t)ceil(k * sigma_r); }
+int64_t lfo_adaptive_zc_threshold(double k, double sigma_r) { return lfo_ceil_threshold(k * sigma_r); }
 
 typedef struct lfo_params {
     int32_t bit_depth;

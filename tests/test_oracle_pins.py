@@ -237,6 +237,50 @@ def test_zc_step_marks_the_two_straddling_columns():
             assert Z[:, 9].all() and Z[:, 10].all()
 
 
+def test_zc_threshold_decides_at_the_step_gap():
+    """Pins the normalised-threshold conversion t = ceil(thr * 2^F * M) (R9) to
+    numbers outside the oracle: the A.3 step (sigma 0.5, 8-bit, A = 200) has one
+    opposite-sign pair with gap 2 * 2246600 (golden profile), and A.2 gives F = 15
+    for that mask.  The crossing survives exactly up to thr = gap / (2^F * 255):
+    a wrong scale, a dropped M or 2^F, or floor instead of ceil flips one case."""
+    (row,) = _golden_rows("step_profile_A3.txt")
+    gap = int(row[2]) - int(row[3])
+    F = next(int(r[2]) for r in _golden_rows("masks_A2.txt") if float(r[0]) == 0.5 and int(r[1]) == 8)
+    thr0 = gap / (2.0**F * 255)
+    I = np.full((12, 16), 0, np.uint16)
+    I[:, 8:] = 200
+    def kept(thr):
+        p = O.Params(bit_depth=8, sigma=(0.5, 0.5), zc_threshold=(thr, thr), hybrid_median=False, out_mode=1)
+        return sorted(set(np.nonzero(O.run(I, p))[1].tolist()))
+    assert kept(thr0 * (1 - 1e-12)) == [7, 8]
+    assert kept(thr0 * (1 + 1e-9)) == []
+    assert kept(0.0) == [7, 8]
+    # thresholds far beyond any gap (2^25, R3) reject everything, without overflow
+    assert kept(1e30) == [] and kept(1e300) == []
+    assert O.zc_threshold_int(1e300, F, 8) >= 2**26
+
+
+@pytest.mark.parametrize("w", [3, 5, 7])
+def test_std_gate_windows_vs_statistics(w):
+    """Eq. 2 at every window size of NEXT-4: the gate at the centre
+    of a w x w image (no padding reaches it) against statistics.stdev of the
+    whole window, for the intensity source and for a binary ZC window."""
+    rng = np.random.default_rng(40 + w)
+    c = w // 2
+    for _ in range(200):
+        I = rng.integers(0, 1024, (w, w)).astype(np.uint16)
+        Z = np.zeros((w, w), np.uint8)
+        Z[c, c] = 1
+        T = float(rng.uniform(0, 500))
+        keep = O.std_gate(I, Z, w, T)
+        assert bool(keep[c, c]) == (statistics.stdev(I.ravel().astype(float)) > T)
+        B = (rng.random((w, w)) < rng.uniform(0.05, 0.95)).astype(np.uint8)
+        B[c, c] = 1
+        Tb = float(rng.uniform(0.05, 0.55))
+        keep = O.std_gate(B, B, w, Tb)
+        assert bool(keep[c, c]) == (statistics.stdev(B.ravel().astype(float)) > Tb)
+
+
 def test_zc_ramp_marks_the_middle_column():
     q, _ = O.mask_int(0.5, 5, 8)
     I = np.zeros((8, 17), np.uint16)

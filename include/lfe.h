@@ -12,7 +12,7 @@
  *   urban pipeline / padding ..... :94  (Sec. 4.1, Fig. 1)
  *   water pipeline (median) ...... :102 (Sec. 4.2, Fig. 2)
  *   adaptive thresholds .......... SPEC.md:233, :235 (NEXT-2)
- * Readings of silent or ambiguous points are R1..R22 in DESIGN.md.
+ * Readings of silent or ambiguous points are R1..R24 in DESIGN.md.
  *
  * Conventions for every call:
  *   - No C++ exception crosses this ABI; every call returns an lfe_status.
@@ -119,9 +119,11 @@ void lfe_params_default(lfe_params *p);
 lfe_status lfe_create(const lfe_params *p, lfe_ctx **out);
 
 /* Whole-image extraction on the device (the Fig. 1 / Fig. 2 pipeline).
- * With adaptive thresholds it first runs the statistics pass over the image,
- * synchronises cuda_stream once to resolve the thresholds on the host (as
- * lfe_set_stats), then enqueues the extraction.
+ * With adaptive thresholds it first runs the statistics pass over THIS image,
+ * synchronises cuda_stream once to resolve the thresholds on the host (by the
+ * lfe_set_stats formulas), then enqueues the extraction with them.  Those
+ * thresholds apply to this call only: thresholds installed with lfe_set_stats
+ * are neither used nor changed.
  * d_in/d_out: device pointers to W x H pitched images; pitches must be >= the
  * row bytes and multiples of the element size; in and out must not overlap.
  * 16-byte aligned bases and pitches select the fast fused kernel; anything
@@ -163,8 +165,12 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_
 /* End-to-end call on HOST buffers (the paper's H2D -> kernel -> D2H flow,
  * PAPER.md:150, Table 6): copies the image in row strips to device staging
  * buffers owned by the ctx, runs lfe_extract_rows per strip and copies the
- * result back, overlapping the three on separate streams (an adaptive ctx first
- * streams the image once for lfe_stats_rows).  Synchronous:
+ * result back, overlapping the three on separate streams.  An adaptive ctx uses
+ * the thresholds installed with lfe_set_stats (e.g. whole-scene statistics when
+ * the call streams one rank's strip); without them it first streams THIS image
+ * once for its statistics and uses the resulting thresholds for this call only
+ * (nothing is installed).  Every error return happens after the call's
+ * enqueued work has drained (no copy is left in flight).  Synchronous:
  * returns when h_out is complete.  Pinned (page-locked) host buffers give
  * full PCIe bandwidth; pageable ones work but are slower.  Errors: EINVAL,
  * ENOMEM, ECUDA, ERANGE (checked at the end of the call). */
@@ -199,13 +205,17 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_by
 /* Resolves the adaptive thresholds of a ctx from whole-image statistics
  * (HOST pointer): sigma = sqrt(n*S2 - S1^2) / n with the integer numerator
  * exact, rounded once to double (R21).  Subsequent lfe_extract_rows /
- * lfe_extract_host calls use them; lfe_extract computes its own.  NULL clears.
- * Errors: EINVAL (n < 1, or the ctx is not adaptive). */
+ * lfe_extract_host calls use them; lfe_extract always resolves its own from
+ * the image it is given (per call, leaving these in place).  NULL clears.
+ * Gap thresholds above 2^26 integer units act alike (no gap reaches 2^25, R3)
+ * and are clamped there.  Errors: EINVAL (n < 1, or the ctx is not adaptive). */
 lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h_stats);
 
-/* The thresholds in force: zc_t[j] in integer response units, std_T[j] and
- * std3_T[j] in Eq. 2 units (< 0: re-check off).  Any pointer may be NULL.
- * Errors: EINVAL (NULL ctx; adaptive ctx without statistics). */
+/* The ctx's thresholds (fixed ones, or those installed with lfe_set_stats):
+ * zc_t[j] in integer response units, std_T[j] and std3_T[j] in Eq. 2 units
+ * (< 0: re-check off).  Any pointer may be NULL.  Errors: EINVAL (NULL ctx;
+ * adaptive ctx without lfe_set_stats -- per-call thresholds of lfe_extract /
+ * lfe_extract_host are not recorded). */
 lfe_status lfe_get_thresholds(const lfe_ctx *c, int64_t *zc_t, double *std_T, double *std3_T);
 
 /* Rows of real input needed above/below a strip for a bit-exact result:

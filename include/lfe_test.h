@@ -1,6 +1,8 @@
 /*
- * lfe_test.h -- test-only entry points of liblfe (not part of the product
- * API; used by tests/ to check host-side logic without a GPU).  Same
+ * lfe_test.h -- test-only entry points, exported by liblfe_test.so (a separate
+ * library built next to liblfe.so and linked against it; not part of the
+ * product API).  tests/ uses them to check host-side logic without a GPU and
+ * to drive single stages of the fused kernel with injected values.  Same
  * conventions as lfe.h.
  */
 #ifndef LFE_TEST_H
@@ -37,6 +39,18 @@ lfe_status lfe_test_response(lfe_ctx *c, const void *d_in, int64_t in_pitch_byte
  * d_out is uint8 0/255.  Both pitches and bases 16-byte aligned.  Enqueued on
  * cuda_stream.  Errors: EINVAL, EUNSUPPORTED, ECUDA. */
 lfe_status lfe_test_extract_r(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
+                              int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
+
+/* The fused kernel with its merged image replaced by the INPUT, E = I, so the
+ * hybrid-median stages can be checked on arbitrary E (Sec. 3.4;
+ * readings R16, R17): d_out = the 5x5 hybrid median of I (replicate padding,
+ * R5), or with median_window2 = 3 the 3x3 hybrid median of that.  The ctx must
+ * have bit_depth 16 (every uint16 value is a valid E), hybrid_median 1,
+ * median_window 5, median_window2 0 or 3, out_mode LFE_OUT_EXTRACT and no 3x3
+ * re-check; d_in / d_out are W x H uint16 device images, bases and pitches
+ * 16-byte aligned.  Enqueued on cuda_stream.  Errors: EINVAL, EUNSUPPORTED,
+ * ECUDA. */
+lfe_status lfe_test_extract_e(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
                               int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
 
 #ifdef __cplusplus

@@ -12,18 +12,23 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
 #include <new>
 #include <vector>
 
 #include "lfe.h"
 #include "lfe_internal.h"
-#include "lfe_test.h"
 
 using namespace lfe;
 
 namespace {
-
 thread_local char g_msg[512] = "";
+}  // namespace
+
+const char *lfe_last_message(void) { return g_msg; }
+
+namespace lfe {
+namespace host {
 
 lfe_status fail(lfe_status s, const char *fmt, ...)
 {
@@ -33,34 +38,6 @@ lfe_status fail(lfe_status s, const char *fmt, ...)
     va_end(ap);
     return s;
 }
-
-constexpr int kHostBuffers = 3;
-
-}  // namespace
-
-struct lfe_ctx {
-    lfe_params p;
-    KParams kp;
-    int F[2];
-    int device;
-    int *d_err = nullptr;
-    LaunchCfg cfg{LFE_KERNEL_AUTO, 0, 0};
-    int64_t launches = 0;
-    // lfe_extract_host staging
-    int host_strip_rows = 1024;
-    cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
-    cudaEvent_t ev_h2d[kHostBuffers] = {}, ev_comp[kHostBuffers] = {}, ev_d2h[kHostBuffers] = {};
-    void *d_in[kHostBuffers] = {}, *d_out[kHostBuffers] = {};
-    size_t in_cap = 0, out_cap = 0;
-    // resolved thresholds (absolute at create; adaptive ones after lfe_set_stats)
-    bool have_thresholds = false;
-    int64_t zc_t[2] = {0, 0};
-    double std_T[2] = {0, 0}, std3_T[2] = {-1, -1};
-    // adaptive pre-pass (NEXT-2): device accumulator + pinned host copy
-    lfe_stats *d_stats = nullptr, *h_stats = nullptr;
-};
-
-namespace {
 
 // ---- Eq. 1, sampled at integer offsets (R2) ----------------
 double eq1(double s, int x, int y)
@@ -181,11 +158,12 @@ double global_std(int64_t n, __int128 S1, unsigned __int128 S2)
     return std::sqrt((double)D) / (double)n;
 }
 
-// Installs resolved thresholds into the kernel parameters: ZC gap t (integer
-// units, R9/R21) and the Eq. 2 thresholds T, T3 (R11, R12, R22).
-void apply_thresholds(lfe_ctx *c, const int64_t zt[2], const double T[2], const double T3[2])
+// Writes resolved thresholds into kernel parameters: ZC gap t (integer units,
+// R9/R21) and the Eq. 2 thresholds T, T3 (R11, R12, R22).  `kp` is either the
+// ctx's own parameters (fixed thresholds, lfe_set_stats) or a per-call copy
+// (lfe_extract / lfe_extract_host resolving their own statistics).
+void write_thresholds(const lfe_ctx *c, KParams &kp, const int64_t zt[2], const double T[2], const double T3[2])
 {
-    KParams &kp = c->kp;
     const int L = c->p.std_window * c->p.std_window;
     for (int j = 0; j < 2; ++j) {
         // a gap never exceeds 2^25, so any t above it acts alike
@@ -206,12 +184,24 @@ void apply_thresholds(lfe_ctx *c, const int64_t zt[2], const double T[2], const 
         kp.pass3_lut[j] = 0;
         for (int k = 0; k <= 9; ++k)
             if ((double)(9 * k - k * k) > kp.rhs3[j]) kp.pass3_lut[j] |= 1u << k;
+    }
+}
+
+// Installs thresholds on the ctx (fixed ones at create; lfe_set_stats).
+void install_thresholds(lfe_ctx *c, const int64_t zt[2], const double T[2], const double T3[2])
+{
+    write_thresholds(c, c->kp, zt, T, T3);
+    for (int j = 0; j < 2; ++j) {
         c->zc_t[j] = zt[j];
         c->std_T[j] = T[j];
         c->std3_T[j] = T3[j];
     }
     c->have_thresholds = true;
 }
+
+// ceil(x) as an integer gap threshold.  Gaps never exceed 2^25 (R3), so every x
+// above 2^26 acts alike; clamping in double first keeps the conversion defined.
+int64_t gap_units(double x) { return (int64_t)std::ceil(std::min(x, 0x1p26)); }
 
 bool overlap(const void *a, size_t na, const void *b, size_t nb)
 {
@@ -228,7 +218,9 @@ lfe_status check_bound_device(const lfe_ctx *c)
     return LFE_OK;
 }
 
-lfe_status run(lfe_ctx *c, const Geometry &g, cudaStream_t s)
+// `kp`: the ctx's parameters, or a per-call copy carrying thresholds the call
+// resolved itself (adaptive lfe_extract / lfe_extract_host)
+lfe_status run(lfe_ctx *c, const KParams &kp, const Geometry &g, cudaStream_t s)
 {
     lfe_status bound = check_bound_device(c);
     if (bound != LFE_OK) return bound;
@@ -237,13 +229,13 @@ lfe_status run(lfe_ctx *c, const Geometry &g, cudaStream_t s)
     const bool aligned = ((reinterpret_cast<uintptr_t>(g.in) | reinterpret_cast<uintptr_t>(g.out) |
                            (uintptr_t)g.in_pitch | (uintptr_t)g.out_pitch | (uintptr_t)g.in_band_stride |
                            (uintptr_t)g.out_band_stride) & 15u) == 0;
-    const bool fused_ok = aligned && fused_supports(c->kp, c->p.bit_depth);
+    const bool fused_ok = aligned && fused_supports(kp, c->p.bit_depth);
     if (k == LFE_KERNEL_AUTO) k = fused_ok ? LFE_KERNEL_FUSED : LFE_KERNEL_STAGED;
     if (k == LFE_KERNEL_FUSED && !fused_ok)
         return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
     cudaError_t e = k == LFE_KERNEL_FUSED
-                        ? launch_fused(c->kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s)
-                        : launch_staged(c->kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s);
+                        ? launch_fused(kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s)
+                        : launch_staged(kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
     ++c->launches;
     return LFE_OK;
@@ -266,13 +258,39 @@ lfe_status check_image_args(const lfe_ctx *c, const void *in, int64_t in_pitch, 
     return LFE_OK;
 }
 
-}  // namespace
+// Adaptive thresholds from whole-image statistics (R21, R22); nothing installed.
+void thresholds_from_stats(const lfe_ctx *c, const lfe_stats &h, int64_t zt[2], double T[2], double T3[2])
+{
+    const lfe_params &p = c->p;
+    const unsigned __int128 Si2 = (unsigned __int128)(uint64_t)h.i_sq;
+    const double sI = global_std(h.n, (__int128)h.i_sum, Si2);
+    for (int j = 0; j < 2; ++j) {
+        if (p.adaptive & LFE_ADAPT_ZC) {  // R21: t_j = ceil(k_j * sigma(r_j))
+            const unsigned __int128 S2 =
+                ((unsigned __int128)(uint64_t)h.r_sq_hi[j] << 24) + (unsigned __int128)(uint64_t)h.r_sq_lo[j];
+            zt[j] = gap_units(p.zc_threshold[j] * global_std(h.n, (__int128)h.r_sum[j], S2));
+        } else {
+            const double M = (double)((int64_t(1) << p.bit_depth) - 1);
+            zt[j] = gap_units(p.zc_threshold[j] * std::ldexp(1.0, c->F[j]) * M);
+        }
+        if (p.adaptive & LFE_ADAPT_STD) {  // R22: multiples of sigma(I)
+            T[j] = p.std_threshold[j] * sI;
+            T3[j] = p.std3_threshold[j] >= 0.0 ? p.std3_threshold[j] * sI : p.std3_threshold[j];
+        } else {
+            T[j] = p.std_threshold[j];
+            T3[j] = p.std3_threshold[j];
+        }
+    }
+}
+
+}  // namespace host
+}  // namespace lfe
+
+using namespace lfe::host;
 
 extern "C" {
 
 int32_t lfe_abi_version(void) { return LFE_ABI_VERSION; }
-
-const char *lfe_last_message(void) { return g_msg; }
 
 const char *lfe_strerror(lfe_status s)
 {
@@ -370,8 +388,8 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out)
     if (!p->adaptive) {
         int64_t zt[2];
         for (int j = 0; j < 2; ++j)  // gap threshold in integer units, t = ceil(thr * 2^F * M) (R9)
-            zt[j] = (int64_t)std::ceil(p->zc_threshold[j] * std::ldexp(1.0, c->F[j]) * (double)maxv);
-        apply_thresholds(c, zt, p->std_threshold, p->std3_threshold);
+            zt[j] = gap_units(p->zc_threshold[j] * std::ldexp(1.0, c->F[j]) * (double)maxv);
+        install_thresholds(c, zt, p->std_threshold, p->std3_threshold);
     }
 
     // d_err[0]: sticky ERANGE flag; d_err[1]: the fused kernel's work-queue counter
@@ -434,29 +452,10 @@ lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h)
         return LFE_OK;
     }
     if (h->n < 1) return fail(LFE_EINVAL, "statistics of %lld pixels", (long long)h->n);
-    const lfe_params &p = c->p;
     int64_t zt[2];
     double T[2], T3[2];
-    const unsigned __int128 Si2 = (unsigned __int128)(uint64_t)h->i_sq;
-    const double sI = global_std(h->n, (__int128)h->i_sum, Si2);
-    for (int j = 0; j < 2; ++j) {
-        if (p.adaptive & LFE_ADAPT_ZC) {  // R21: t_j = ceil(k_j * sigma(r_j))
-            const unsigned __int128 S2 =
-                ((unsigned __int128)(uint64_t)h->r_sq_hi[j] << 24) + (unsigned __int128)(uint64_t)h->r_sq_lo[j];
-            zt[j] = (int64_t)std::ceil(p.zc_threshold[j] * global_std(h->n, (__int128)h->r_sum[j], S2));
-        } else {
-            const double M = (double)((int64_t(1) << p.bit_depth) - 1);
-            zt[j] = (int64_t)std::ceil(p.zc_threshold[j] * std::ldexp(1.0, c->F[j]) * M);
-        }
-        if (p.adaptive & LFE_ADAPT_STD) {  // R22: multiples of sigma(I)
-            T[j] = p.std_threshold[j] * sI;
-            T3[j] = p.std3_threshold[j] >= 0.0 ? p.std3_threshold[j] * sI : p.std3_threshold[j];
-        } else {
-            T[j] = p.std_threshold[j];
-            T3[j] = p.std3_threshold[j];
-        }
-    }
-    apply_thresholds(c, zt, T, T3);
+    thresholds_from_stats(c, *h, zt, T, T3);
+    install_thresholds(c, zt, T, T3);
     return LFE_OK;
 }
 
@@ -492,13 +491,14 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, i
                           int32_t halo_above, int32_t halo_below, uint32_t edge_flags, lfe_stats *d_stats,
                           void *stream)
 {
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    lfe_status st = check_bound_device(c);
+    if (st != LFE_OK) return st;
     if (!d_stats || reinterpret_cast<uintptr_t>(d_stats) % 8) return fail(LFE_EINVAL, "d_stats NULL or misaligned");
-    lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_stats, (int64_t)W * 2, rows);
+    st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_stats, (int64_t)W * 2, rows);
     if (st != LFE_OK) return st;
     Geometry g;
     st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, c->kp.RL, &g);
-    if (st != LFE_OK) return st;
-    st = check_bound_device(c);
     if (st != LFE_OK) return st;
     cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
@@ -517,36 +517,47 @@ static lfe_status stats_buffers(lfe_ctx *c)
     return LFE_OK;
 }
 
-// whole-image statistics -> thresholds (one stream synchronisation)
-static lfe_status resolve_from_device(lfe_ctx *c, cudaStream_t s)
+// whole-image statistics on the device -> thresholds written into the per-call
+// parameters `kp` (one stream synchronisation; the ctx's own state is untouched)
+static lfe_status resolve_from_device(lfe_ctx *c, cudaStream_t s, KParams &kp)
 {
     if (cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(lfe_stats), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return fail(LFE_ECUDA, "statistics: %s", cudaGetErrorString(cudaGetLastError()));
-    return lfe_set_stats(c, c->h_stats);
+    if (c->h_stats->n < 1) return fail(LFE_EINVAL, "statistics of %lld pixels", (long long)c->h_stats->n);
+    int64_t zt[2];
+    double T[2], T3[2];
+    thresholds_from_stats(c, *c->h_stats, zt, T, T3);
+    write_thresholds(c, kp, zt, T, T3);
+    return LFE_OK;
 }
 
 lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
                        int64_t out_pitch, void *stream)
 {
-    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    lfe_status st = check_bound_device(c);
+    if (st != LFE_OK) return st;
+    st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
     if (st != LFE_OK) return st;
     if (overlap(d_in, (size_t)(H - 1) * in_pitch + W * elem_in(c), d_out, (size_t)(H - 1) * out_pitch + W * elem_out(c)))
         return fail(LFE_EINVAL, "input and output overlap");
     Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H};
-    if (c->p.adaptive) {  // NEXT-2: statistics pre-pass over the whole image
-        st = stats_buffers(c);
-        if (st != LFE_OK) return st;
-        cudaStream_t s = (cudaStream_t)stream;
-        if (cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), s) != cudaSuccess)
-            return fail(LFE_ECUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
-        cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, s);
-        if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
-        ++c->launches;
-        st = resolve_from_device(c, s);
-        if (st != LFE_OK) return st;
-    }
-    return run(c, g, (cudaStream_t)stream);
+    if (!c->p.adaptive) return run(c, c->kp, g, (cudaStream_t)stream);
+    // NEXT-2: statistics pre-pass over THIS image; its thresholds apply to this call
+    // only (thresholds installed with lfe_set_stats are left as they are)
+    st = stats_buffers(c);
+    if (st != LFE_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), s) != cudaSuccess)
+        return fail(LFE_ECUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, s);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
+    ++c->launches;
+    KParams kp = c->kp;
+    st = resolve_from_device(c, s, kp);
+    if (st != LFE_OK) return st;
+    return run(c, kp, g, s);
 }
 
 lfe_status lfe_extract_bands(lfe_ctx *c, const void *d_in, int64_t in_pitch, int64_t in_band_stride, int32_t W,
@@ -568,25 +579,35 @@ lfe_status lfe_extract_bands(lfe_ctx *c, const void *d_in, int64_t in_pitch, int
         return fail(LFE_EINVAL, "input and output overlap");
     Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H, bands, bands > 1 ? in_band_stride : 0,
                bands > 1 ? out_band_stride : 0};
-    return run(c, g, (cudaStream_t)stream);
+    return run(c, c->kp, g, (cudaStream_t)stream);
 }
 
-lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
-                            int32_t halo_above, int32_t halo_below, uint32_t edge_flags, void *d_out_row0,
-                            int64_t out_pitch, void *stream)
+// one strip with the thresholds in `kp` (the ctx's, or a per-call copy)
+static lfe_status extract_rows(lfe_ctx *c, const KParams &kp, const void *d_in_row0, int64_t in_pitch, int32_t W,
+                               int32_t rows, int32_t halo_above, int32_t halo_below, uint32_t edge_flags,
+                               void *d_out_row0, int64_t out_pitch, cudaStream_t stream)
 {
     lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_out_row0, out_pitch, rows);
     if (st != LFE_OK) return st;
-    if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
     Geometry g;
-    st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, c->kp.halo, &g);
+    st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, kp.halo, &g);
     if (st != LFE_OK) return st;
     if (overlap(g.in, (size_t)(g.Hv - 1) * in_pitch + W * elem_in(c), d_out_row0,
                 (size_t)(rows - 1) * out_pitch + W * elem_out(c)))
         return fail(LFE_EINVAL, "input and output overlap");
     g.out = d_out_row0;
     g.out_pitch = out_pitch;
-    return run(c, g, (cudaStream_t)stream);
+    return run(c, kp, g, stream);
+}
+
+lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
+                            int32_t halo_above, int32_t halo_below, uint32_t edge_flags, void *d_out_row0,
+                            int64_t out_pitch, void *stream)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
+    return extract_rows(c, c->kp, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, d_out_row0,
+                        out_pitch, (cudaStream_t)stream);
 }
 
 lfe_status lfe_last_async_error(lfe_ctx *c, void *stream)
@@ -666,7 +687,10 @@ static std::vector<int> host_strip_cuts(int H, int S)
 lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int32_t W, int32_t H, void *h_out,
                             int64_t out_pitch)
 {
-    lfe_status st = check_image_args(c, h_in, in_pitch, W, H, h_out, out_pitch, H);
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    lfe_status st = check_bound_device(c);
+    if (st != LFE_OK) return st;
+    st = check_image_args(c, h_in, in_pitch, W, H, h_out, out_pitch, H);
     if (st != LFE_OK) return st;
     const int h = c->kp.halo;
     const int S = c->host_strip_rows < H ? c->host_strip_rows : H;
@@ -680,9 +704,26 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
     cudaStream_t sh = c->st[0], sc = c->st[1], sd = c->st[2];
     const std::vector<int> cut = host_strip_cuts(H, S);
     const int nstrips = (int)cut.size() - 1;
-    if (c->p.adaptive) {  // NEXT-2: stream the image once for the whole-image statistics
+    // LFE_DEBUG_HOST=<file>: per-strip event timeline of the three streams (debug only)
+    static const char *dbg_path = getenv("LFE_DEBUG_HOST");
+    cudaEvent_t dev[6 * 64 + 1];
+    const int ndbg = dbg_path && nstrips <= 64 ? nstrips : 0;
+    // every exit after the first enqueue: nothing of this call may still be in flight on
+    // the staging buffers when it returns (the next call reuses them without waiting)
+    auto finish = [&](lfe_status r) {
+        for (auto s : c->st) cudaStreamSynchronize(s);
+        for (int k = 0; k < (ndbg ? 6 * ndbg + 1 : 0); ++k) cudaEventDestroy(dev[k]);
+        return r;
+    };
+    for (int k = 0; k < (ndbg ? 6 * ndbg + 1 : 0); ++k) cudaEventCreate(&dev[k]);
+    // Thresholds: the ctx's own (fixed, or installed with lfe_set_stats -- e.g. whole-scene
+    // statistics when this call streams one rank's strip); an adaptive ctx without them
+    // first streams THIS image once for its statistics, used by this call only.
+    KParams kp_call;
+    const KParams *kp = &c->kp;
+    if (!c->have_thresholds) {
         st = stats_buffers(c);
-        if (st != LFE_OK) return st;
+        if (st != LFE_OK) return finish(st);
         cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), sc);
         for (int i = 0; i < nstrips; ++i) {
             const int b = i % kHostBuffers;
@@ -691,23 +732,20 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
             if (i >= kHostBuffers) cudaStreamWaitEvent(sh, c->ev_comp[b], 0);
             cudaError_t e = copy_rows(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
                                       in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
-            if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
+            if (e != cudaSuccess) return finish(fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e)));
             cudaEventRecord(c->ev_h2d[b], sh);
             cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
             const uint32_t flags = (lo == 0 ? LFE_TOP_IS_EDGE : 0u) | (hi == H ? LFE_BOTTOM_IS_EDGE : 0u);
             const char *row0 = reinterpret_cast<const char *>(c->d_in[b]) + (size_t)(a0 - lo) * dpi;
             st = lfe_stats_rows(c, row0, (int64_t)dpi, W, a1 - a0, a0 - lo, hi - a1, flags, c->d_stats, sc);
-            if (st != LFE_OK) return st;
+            if (st != LFE_OK) return finish(st);
             cudaEventRecord(c->ev_comp[b], sc);
         }
-        st = resolve_from_device(c, sc);
-        if (st != LFE_OK) return st;
+        kp_call = c->kp;
+        st = resolve_from_device(c, sc, kp_call);
+        if (st != LFE_OK) return finish(st);
+        kp = &kp_call;
     }
-    // LFE_DEBUG_HOST=<file>: per-strip event timeline of the three streams (debug only)
-    static const char *dbg_path = getenv("LFE_DEBUG_HOST");
-    cudaEvent_t dev[6 * 64 + 1];
-    const int ndbg = dbg_path && nstrips <= 64 ? nstrips : 0;
-    for (int k = 0; k < (ndbg ? 6 * ndbg + 1 : 0); ++k) cudaEventCreate(&dev[k]);
     if (ndbg) cudaEventRecord(dev[6 * ndbg], sh);
     for (int i = 0; i < nstrips; ++i) {
         const int b = i % kHostBuffers;
@@ -717,7 +755,7 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
         if (ndbg) cudaEventRecord(dev[6 * i + 0], sh);
         cudaError_t e = copy_rows(c->d_in[b], dpi, reinterpret_cast<const char *>(h_in) + (int64_t)lo * in_pitch,
                                   in_pitch, (size_t)W * ei, hi - lo, cudaMemcpyHostToDevice, sh);
-        if (e != cudaSuccess) return fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e));
+        if (e != cudaSuccess) return finish(fail(LFE_ECUDA, "H2D: %s", cudaGetErrorString(e)));
         if (ndbg) cudaEventRecord(dev[6 * i + 1], sh);
         cudaEventRecord(c->ev_h2d[b], sh);
         cudaStreamWaitEvent(sc, c->ev_h2d[b], 0);
@@ -725,15 +763,16 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
         if (ndbg) cudaEventRecord(dev[6 * i + 2], sc);
         const uint32_t flags = (lo == 0 ? LFE_TOP_IS_EDGE : 0u) | (hi == H ? LFE_BOTTOM_IS_EDGE : 0u);
         const char *row0 = reinterpret_cast<const char *>(c->d_in[b]) + (size_t)(a0 - lo) * dpi;
-        st = lfe_extract_rows(c, row0, (int64_t)dpi, W, a1 - a0, a0 - lo, hi - a1, flags, c->d_out[b], (int64_t)dpo, sc);
-        if (st != LFE_OK) return st;
+        st = extract_rows(c, *kp, row0, (int64_t)dpi, W, a1 - a0, a0 - lo, hi - a1, flags, c->d_out[b], (int64_t)dpo,
+                          sc);
+        if (st != LFE_OK) return finish(st);
         if (ndbg) cudaEventRecord(dev[6 * i + 3], sc);
         cudaEventRecord(c->ev_comp[b], sc);
         cudaStreamWaitEvent(sd, c->ev_comp[b], 0);
         if (ndbg) cudaEventRecord(dev[6 * i + 4], sd);
         e = copy_rows(reinterpret_cast<char *>(h_out) + (int64_t)a0 * out_pitch, out_pitch, c->d_out[b], dpo,
                       (size_t)W * eo, a1 - a0, cudaMemcpyDeviceToHost, sd);
-        if (e != cudaSuccess) return fail(LFE_ECUDA, "D2H: %s", cudaGetErrorString(e));
+        if (e != cudaSuccess) return finish(fail(LFE_ECUDA, "D2H: %s", cudaGetErrorString(e)));
         if (ndbg) cudaEventRecord(dev[6 * i + 5], sd);
         cudaEventRecord(c->ev_d2h[b], sd);
     }
@@ -748,55 +787,8 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
             fprintf(f, "---\n");
             fclose(f);
         }
-        for (int k = 0; k < 6 * ndbg + 1; ++k) cudaEventDestroy(dev[k]);
     }
-    return lfe_last_async_error(c, sd);
-}
-
-lfe_status lfe_test_mask(double sigma, int32_t n, int32_t bit_depth, int32_t *q, int32_t *shift_F)
-{
-    if (!q || !shift_F) return fail(LFE_EINVAL, "NULL output");
-    if (!std::isfinite(sigma) || !(sigma > 0.0)) return fail(LFE_EINVAL, "sigma must be > 0");
-    if (!odd_in(n, 1, kMaxMask)) return fail(LFE_EINVAL, "n must be odd 1..9");
-    if (bit_depth < 1 || bit_depth > 16) return fail(LFE_EINVAL, "bit depth");
-    int F = 0;
-    if (!make_mask(sigma, n, bit_depth, q, &F)) return fail(LFE_EINVAL, "no quantisation");
-    *shift_F = F;
-    return LFE_OK;
-}
-
-lfe_status lfe_test_validate(const lfe_params *p) { return validate(p); }
-
-lfe_status lfe_test_response(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, int32_t branch,
-                             void *d_r, void *stream)
-{
-    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_r, (int64_t)W * 4, H);
-    if (st != LFE_OK) return st;
-    if (branch != 0 && branch != 1) return fail(LFE_EINVAL, "branch must be 0 or 1");
-    Geometry g{d_in, in_pitch, nullptr, 0, W, H, 0, H};
-    cudaError_t e = launch_response(c->kp, g, c->p.bit_depth > 8, branch, d_r, (cudaStream_t)stream);
-    if (e != cudaSuccess) return fail(LFE_ECUDA, "response launch: %s", cudaGetErrorString(e));
-    return LFE_OK;
-}
-
-lfe_status lfe_test_extract_r(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
-                              int64_t out_pitch, void *stream)
-{
-    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
-    if (c->p.bit_depth != 16 || c->p.hybrid_median || c->p.out_mode != LFE_OUT_MASK || c->kp.recheck[0] ||
-        c->kp.recheck[1])
-        return fail(LFE_EUNSUPPORTED, "test_extract_r needs bit_depth 16, no median, MASK output, no 3x3 re-check");
-    lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
-    if (st != LFE_OK) return st;
-    if (((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out) | (uintptr_t)in_pitch |
-          (uintptr_t)out_pitch) & 15u) != 0 || !fused_supports(c->kp, c->p.bit_depth))
-        return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
-    st = check_bound_device(c);
-    if (st != LFE_OK) return st;
-    Geometry g{d_in, in_pitch, d_out, out_pitch, W, H, 0, H};
-    cudaError_t e = launch_fused(c->kp, g, true, c->cfg.tile_w, c->cfg.tile_h, c->d_err, (cudaStream_t)stream, true);
-    if (e != cudaSuccess) return fail(LFE_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
-    return LFE_OK;
+    return finish(lfe_last_async_error(c, sd));
 }
 
 void lfe_destroy(lfe_ctx *c)

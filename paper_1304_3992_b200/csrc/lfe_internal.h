@@ -74,11 +74,52 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
                           int *err_flag, cudaStream_t s);
 // err_flag[0] = sticky ERANGE flag, err_flag[1] = scratch work counter (fused kernel)
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
-                         int *err_flag, cudaStream_t s, bool rtest = false);
+                         int *err_flag, cudaStream_t s);
 bool fused_supports(const KParams &kp, int bit_depth);
 // test entry: branch j's response for every pixel of a whole image (int32 or float bits)
 cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int branch, void *d_r, cudaStream_t s);
 // adds the exact global sums of output rows [o0, o1) to *d_stats (NEXT-2)
 cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, cudaStream_t s);
 
+// ---- host core (lfe_host.cu), shared with the test-only library (csrc/test/) ----
+namespace host {
+lfe_status fail(lfe_status s, const char *fmt, ...);       // sets lfe_last_message(), returns s
+lfe_status validate(const lfe_params *p);                   // every lfe_create parameter check
+bool make_mask(double sigma, int n, int bit_depth, int32_t *q, int *F_out);  // reading R3
+bool odd_in(int v, int lo, int hi);
+}  // namespace host
+
+constexpr int kHostBuffers = 3;  // lfe_extract_host staging buffers
+
+}  // namespace lfe
+
+// The ctx behind the opaque lfe_ctx handle of lfe.h.
+struct lfe_ctx {
+    lfe_params p;
+    lfe::KParams kp;
+    int F[2];
+    int device;
+    int *d_err = nullptr;
+    lfe::LaunchCfg cfg{LFE_KERNEL_AUTO, 0, 0};
+    int64_t launches = 0;
+    // lfe_extract_host staging
+    int host_strip_rows = 1024;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+    cudaEvent_t ev_h2d[lfe::kHostBuffers] = {}, ev_comp[lfe::kHostBuffers] = {}, ev_d2h[lfe::kHostBuffers] = {};
+    void *d_in[lfe::kHostBuffers] = {}, *d_out[lfe::kHostBuffers] = {};
+    size_t in_cap = 0, out_cap = 0;
+    // resolved thresholds (absolute at create; adaptive ones after lfe_set_stats)
+    bool have_thresholds = false;
+    int64_t zc_t[2] = {0, 0};
+    double std_T[2] = {0, 0}, std3_T[2] = {-1, -1};
+    // adaptive pre-pass (NEXT-2): device accumulator + pinned host copy
+    lfe_stats *d_stats = nullptr, *h_stats = nullptr;
+};
+
+namespace lfe {
+namespace host {
+lfe_status check_image_args(const lfe_ctx *c, const void *in, int64_t in_pitch, int32_t W, int64_t rows_total,
+                            const void *out, int64_t out_pitch, int64_t out_rows);
+lfe_status check_bound_device(const lfe_ctx *c);  // EINVAL unless c's device is current
+}  // namespace host
 }  // namespace lfe

@@ -18,6 +18,7 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LFE_LIB") or os.path.join(_PKG, "liblfe.so")  # LFE_LIB: A/B experiments only
+TEST_LIB_PATH = os.path.join(_PKG, "liblfe_test.so")  # include/lfe_test.h: test-only entry points
 
 LFE_OK, LFE_EINVAL, LFE_EUNSUPPORTED, LFE_ENOMEM, LFE_ENODEV, LFE_ECUDA, LFE_ERANGE = range(7)
 LFE_STD_ZC, LFE_STD_INTENSITY, LFE_STD_RESPONSE, LFE_STD_RESPONSE_AT_ZC = 0, 1, 2, 3
@@ -84,7 +85,9 @@ EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows"
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
            "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
            "lfe_set_stats", "lfe_get_thresholds", "lfe_extract_bands"]
-TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response", "lfe_test_extract_r"]  # include/lfe_test.h
+# include/lfe_test.h, exported by the separate liblfe_test.so
+TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response", "lfe_test_extract_r", "lfe_test_extract_e"]
+_test_lib = None
 
 
 def load():
@@ -133,16 +136,34 @@ def load():
     L.lfe_set_stats.restype = st
     L.lfe_get_thresholds.argtypes = [P, P, P, P]
     L.lfe_get_thresholds.restype = st
-    L.lfe_test_mask.argtypes = [ctypes.c_double, I32, I32, P, P]
-    L.lfe_test_mask.restype = st
-    L.lfe_test_validate.argtypes = [ctypes.POINTER(lfe_params)]
-    L.lfe_test_validate.restype = st
-    L.lfe_test_response.argtypes = [P, P, I64, I32, I32, I32, P, P]
-    L.lfe_test_response.restype = st
-    L.lfe_test_extract_r.argtypes = [P, P, I64, I32, I32, P, I64, P]
-    L.lfe_test_extract_r.restype = st
     _lib = L
     return L
+
+
+def load_test():
+    """Load liblfe_test.so, the test-only entry points (include/lfe_test.h); it
+    resolves the host core from the liblfe.so next to it."""
+    global _test_lib
+    if _test_lib is not None:
+        return _test_lib
+    load()
+    if not os.path.exists(TEST_LIB_PATH):
+        raise RuntimeError(f"liblfe_test.so not built ({TEST_LIB_PATH}); run __graft_entry__.build()")
+    T = ctypes.CDLL(TEST_LIB_PATH)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    st = ctypes.c_int
+    T.lfe_test_mask.argtypes = [ctypes.c_double, I32, I32, P, P]
+    T.lfe_test_mask.restype = st
+    T.lfe_test_validate.argtypes = [ctypes.POINTER(lfe_params)]
+    T.lfe_test_validate.restype = st
+    T.lfe_test_response.argtypes = [P, P, I64, I32, I32, I32, P, P]
+    T.lfe_test_response.restype = st
+    T.lfe_test_extract_r.argtypes = [P, P, I64, I32, I32, P, I64, P]
+    T.lfe_test_extract_r.restype = st
+    T.lfe_test_extract_e.argtypes = [P, P, I64, I32, I32, P, I64, P]
+    T.lfe_test_extract_e.restype = st
+    _test_lib = T
+    return T
 
 
 def _check(status: int, where: str):
@@ -244,12 +265,12 @@ def lfe_test_mask(sigma: float, n: int, bit_depth: int):
     """Host-side mask synthesis of the library (include/lfe_test.h)."""
     q = np.zeros(n * n, np.int32)
     F = ctypes.c_int32()
-    _check(load().lfe_test_mask(float(sigma), n, bit_depth, q.ctypes.data, ctypes.byref(F)), "lfe_test_mask")
+    _check(load_test().lfe_test_mask(float(sigma), n, bit_depth, q.ctypes.data, ctypes.byref(F)), "lfe_test_mask")
     return q.reshape(n, n), F.value
 
 
 def lfe_test_validate(p: lfe_params) -> int:
-    return int(load().lfe_test_validate(ctypes.byref(p)))
+    return int(load_test().lfe_test_validate(ctypes.byref(p)))
 
 
 # ------------------------------------------------------ convenience ----
@@ -431,7 +452,7 @@ class Context:
         H, W = t_in.shape
         dt = torch.float32 if self.params.mask_mode == LFE_MASK_F32 else torch.int32
         out = torch.empty((H, W), dtype=dt, device=t_in.device)
-        _check(load().lfe_test_response(self.handle, pi, pin, W, H, branch, out.data_ptr(), self._stream(stream)),
+        _check(load_test().lfe_test_response(self.handle, pi, pin, W, H, branch, out.data_ptr(), self._stream(stream)),
                "lfe_test_response")
         return out
 
@@ -440,8 +461,18 @@ class Context:
         pi, pin = self._torch_img(t_in, "input")
         po, pout = self._torch_img(t_out, "output")
         H, W = t_in.shape
-        _check(load().lfe_test_extract_r(self.handle, pi, pin, W, H, po, pout, self._stream(stream)),
+        _check(load_test().lfe_test_extract_r(self.handle, pi, pin, W, H, po, pout, self._stream(stream)),
                "lfe_test_extract_r")
+        return t_out
+
+    def test_extract_e(self, t_in, t_out, stream=None):
+        """lfe_test_extract_e: the fused kernel's hybrid-median stages on E = the input
+        (include/lfe_test.h)."""
+        pi, pin = self._torch_img(t_in, "input")
+        po, pout = self._torch_img(t_out, "output")
+        H, W = t_in.shape
+        _check(load_test().lfe_test_extract_e(self.handle, pi, pin, W, H, po, pout, self._stream(stream)),
+               "lfe_test_extract_e")
         return t_out
 
     def last_async_error(self, stream=None) -> int:

@@ -176,7 +176,9 @@ def plan_bands(bands: int, H: int, world: int, halo: int):
     when it would leave fewer than `halo` rows of a band on one side (so one
     neighbour exchange still suffices).  When world divides bands this deals
     out whole bands and needs no collective at all.  Returns, per rank, a list
-    of (band, a, b) owned row ranges."""
+    of (band, a, b) owned row ranges.  Raises ValueError when a piece of a band
+    that is cut on either side would still hold fewer than `halo` rows (as
+    plan_strips does)."""
     if bands < 1 or world < 1 or H < 1:
         raise ValueError("bad bands/H/world")
     T = bands * H
@@ -184,9 +186,11 @@ def plan_bands(bands: int, H: int, world: int, halo: int):
     for k in range(1, world):
         c = round(k * T / world)
         b0 = (c // H) * H
-        if 0 < c - b0 < halo:
+        if c == b0:
+            pass  # already on a band boundary
+        elif c - b0 < halo:
             c = b0
-        elif 0 < b0 + H - c < halo:
+        elif b0 + H - c < halo:
             c = b0 + H
         cuts.append(max(c, cuts[-1]))
     cuts.append(T)
@@ -200,4 +204,11 @@ def plan_bands(bands: int, H: int, world: int, halo: int):
             items.append((b, u - b * H, e - b * H))
             u = e
         work.append(items)
+    # a piece of a band cut on either side must itself hold a halo of rows, or its
+    # neighbour's exchange would need rows from beyond the adjacent rank
+    short = [(k, it) for k, items in enumerate(work) for it in items
+             if (it[1] > 0 or it[2] < H) and it[2] - it[1] < halo]
+    if short:
+        k, (b, a, e) = short[0]
+        raise ValueError(f"rank {k} would own rows [{a}, {e}) of band {b}: {e - a} rows < halo {halo}; use fewer ranks")
     return work

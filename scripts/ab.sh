@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 # A/B timing of two liblfe builds on the same box: abtest/liblfe_A.so vs abtest/liblfe_B.so
 for i in 1 2 3; do
   for v in A B; do

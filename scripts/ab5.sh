@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 for i in 1 2 3 4 5; do
   for v in A B; do
     LFE_LIB=$PWD/abtest/liblfe_$v.so python bench.py --steps 30 --warmup 5 --no-e2e --no-cpu-baseline | python -c "import json,sys; d=json.load(sys.stdin); print('$v', d['ms_per_step'], d['roofline']['kernel_ms'])"

@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 # A/B of the adaptive-threshold variant (statistics pass + extraction): abtest/liblfe_A.so vs _B.so,
 # then the adaptive GPU tests on the in-tree build
 for i in 1 2 3; do

@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 # A/B of the end-to-end (host buffers) number: abtest/liblfe_A.so vs _B.so, then the host-path GPU tests
 for i in 1 2 3; do
   for v in A B; do

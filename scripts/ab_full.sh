@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 # A/B timing of abtest/liblfe_A.so vs abtest/liblfe_B.so, then the FULL GPU suite on the in-tree build
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv

@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 # A/B/C... timing of several liblfe builds (abtest/liblfe_<v>.so) on one bench command; $1 = variants, rest = bench args
 V="$1"; shift
 for i in 1 2 3; do

@@ -1,3 +1,4 @@
+# inputs abtest/liblfe_{A,B}.so: scripts/ab_build.sh A <git-rev>; scripts/ab_build.sh B
 # A/B timing (abtest/liblfe_A.so vs abtest/liblfe_B.so) + GPU tests of the fused path + one ncu
 # --set full capture of the in-tree build's fused kernel (source page for scripts/ncu_lines.py)
 set -x

@@ -1,6 +1,6 @@
 """Dynamic instruction counts of one fused-kernel variant per source line:
 joins the ncu source page (--page source --csv --print-source sass; executed
-warp-instructions per SASS address) with nvdisasm -g line info (abtest/kf.sass).
+warp-instructions per SASS address) with nvdisasm -g line info (abtest/kf.sass, made by scripts/ab_build.sh B).
     python scripts/ncu_lines.py gpurun_out/src_sass.csv VARIANT"""
 import collections
 import csv

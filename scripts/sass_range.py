@@ -1,5 +1,5 @@
 """Print / summarise SASS of one fused-kernel variant in an address range, with
-source lines (CPU only; reads abtest/kf.sass made by `nvdisasm -c -g`).
+source lines (CPU only; reads abtest/kf.sass made by scripts/ab_build.sh B).
     python scripts/sass_range.py VARIANT LO HI [filter-regex]"""
 import collections
 import re

@@ -179,3 +179,18 @@ def test_plan_bands_covers_every_band_row_once(bands, world):
             assert e - a >= 7 or (a, e) == (0, H)
     if bands % world == 0:  # whole bands, no exchange
         assert all(a == 0 and e == H for items in work for _, a, e in items)
+
+
+@pytest.mark.parametrize("bands,H,world", [(1, 100, 30), (2, 40, 13), (1, 20, 3)])
+def test_plan_bands_rejects_pieces_shorter_than_the_halo(bands, H, world):
+    """A band piece cut on either side needs a halo of rows of its own, or one
+    neighbour exchange no longer suffices (as plan_strips, which raises)."""
+    from paper_1304_3992_b200.shard import plan_bands
+    with pytest.raises(ValueError):
+        plan_bands(bands, H, world, 7)
+
+
+def test_plan_bands_short_whole_bands_are_fine():
+    from paper_1304_3992_b200.shard import plan_bands
+    work = plan_bands(4, 5, 4, 7)  # bands shorter than the halo, dealt out whole
+    assert work == [[(0, 0, 5)], [(1, 0, 5)], [(2, 0, 5)], [(3, 0, 5)]]

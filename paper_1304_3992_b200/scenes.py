@@ -228,3 +228,18 @@ def random_image(rng: np.random.Generator, H: int, W: int, bit_depth: int, kind:
         m = rng.random((H, W)) < 0.05
         img[m] = rng.integers(0, maxv + 1, int(m.sum()))
     return img.astype(dtype)
+
+
+def scene_c5_rows(a: int, b: int, out: np.ndarray | None = None, tile: int = 12000, tiles: int = 4) -> np.ndarray:
+    """Rows [a, b) of the c5 mosaic (tiles x tiles c3-generator tiles, seeds
+    13045 + i, row-major), generating only the tiles those rows cross; written
+    into ``out`` ((b - a) x tiles*tile uint16, e.g. pinned host memory) if given."""
+    W = tile * tiles
+    if out is None:
+        out = np.empty((b - a, W), np.uint16)
+    for ty in range(a // tile, (b - 1) // tile + 1):
+        y0, y1 = max(a, ty * tile), min(b, (ty + 1) * tile)
+        for tx in range(tiles):
+            t = scene_c5_tile(ty * tiles + tx, tile)
+            out[y0 - a:y1 - a, tx * tile:(tx + 1) * tile] = t[y0 - ty * tile:y1 - ty * tile]
+    return out

@@ -16,6 +16,51 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 
+def _bytes(t):
+    """Rows travel as bytes: NCCL has no uint16 type, and a byte view of whole
+    contiguous rows is the same memory."""
+    import torch
+    return t if t.dtype == torch.uint8 else t.view(torch.uint8)
+
+
+def exchange_rows(pairs, group=None, staged=None):
+    """Post one neighbour exchange: for each (send_rows, recv_rows, peer) an
+    isend of send_rows and an irecv into recv_rows (NCCL P2P on GPUs); returns
+    the works to wait on.  For a gloo group over device buffers (several ranks
+    sharing one GPU in tests; NCCL refuses that) the rows go through host
+    memory and the returned work copies the received rows into place on wait()
+    (``staged=True`` forces that path, e.g. to test it on CPU buffers)."""
+    import torch
+    import torch.distributed as dist
+    if not pairs:
+        return []
+    if staged is None:
+        staged = pairs[0][0].is_cuda and dist.get_backend(group) == "gloo"
+    ops, recv = [], []
+    for snd, rcv, peer in pairs:
+        if staged:
+            r = torch.empty_like(rcv, device="cpu")
+            ops.append(dist.P2POp(dist.isend, snd.cpu(), peer, group))
+            ops.append(dist.P2POp(dist.irecv, r, peer, group))
+            recv.append((rcv, r))
+        else:
+            ops.append(dist.P2POp(dist.isend, snd, peer, group))
+            ops.append(dist.P2POp(dist.irecv, rcv, peer, group))
+    works = dist.batch_isend_irecv(ops)
+    if not staged:
+        return works
+
+    class _Staged:
+        def wait(self):
+            for w in works:
+                w.wait()
+            for dst, src in recv:
+                dst.copy_(src)
+            return True
+
+    return [_Staged()]
+
+
 def plan_strips(H: int, world: int, halo: int):
     """Contiguous, balanced row ranges [a, b) covering [0, H).  Every strip must
     hold at least ``halo`` rows so one neighbour exchange suffices."""
@@ -64,56 +109,17 @@ class StripShard:
             src = torch.from_numpy(src)
         self.buf[self.ha:self.ha + self.rows].copy_(src)
 
-    def exchange(self, group=None):
+    def exchange(self, group=None, staged=None):
         """Post the halo exchange (isend/irecv with both neighbours); returns the
         works to wait on.  Owned rows are not modified."""
-        import torch
-        import torch.distributed as dist
-        if self.buf.is_cuda and dist.get_backend(group) == "gloo":
-            return self._exchange_host_staged(group)
-        h, ops = self.halo, []
-        # rows travel as bytes: NCCL has no uint16 type, and a byte view of whole
-        # contiguous rows is the same memory
-        B = self.buf if self.buf.dtype == torch.uint8 else self.buf.view(torch.uint8)
+        h, pairs = self.halo, []
+        B = _bytes(self.buf)
         if self.rank > 0:
-            ops.append(dist.P2POp(dist.isend, B[self.ha:self.ha + h], self.rank - 1, group))
-            ops.append(dist.P2POp(dist.irecv, B[0:self.ha], self.rank - 1, group))
+            pairs.append((B[self.ha:self.ha + h], B[0:self.ha], self.rank - 1))
         if self.rank < self.world - 1:
             e = self.ha + self.rows
-            ops.append(dist.P2POp(dist.isend, B[e - h:e], self.rank + 1, group))
-            ops.append(dist.P2POp(dist.irecv, B[e:e + self.hb], self.rank + 1, group))
-        return dist.batch_isend_irecv(ops) if ops else []
-
-    def _exchange_host_staged(self, group):
-        """The same exchange for a gloo group over device buffers (no NCCL, e.g.
-        several ranks sharing one GPU in tests): rows go through host memory; the
-        returned works copy the received rows into the device buffer on wait()."""
-        import torch
-        import torch.distributed as dist
-        h, ops, recv = self.halo, [], []
-        B = self.buf if self.buf.dtype == torch.uint8 else self.buf.view(torch.uint8)
-        if self.rank > 0:
-            ops.append(dist.P2POp(dist.isend, B[self.ha:self.ha + h].cpu(), self.rank - 1, group))
-            r = torch.empty_like(B[0:self.ha], device="cpu")
-            ops.append(dist.P2POp(dist.irecv, r, self.rank - 1, group))
-            recv.append((B[0:self.ha], r))
-        if self.rank < self.world - 1:
-            e = self.ha + self.rows
-            ops.append(dist.P2POp(dist.isend, B[e - h:e].cpu(), self.rank + 1, group))
-            r = torch.empty_like(B[e:e + self.hb], device="cpu")
-            ops.append(dist.P2POp(dist.irecv, r, self.rank + 1, group))
-            recv.append((B[e:e + self.hb], r))
-        works = dist.batch_isend_irecv(ops) if ops else []
-
-        class _Staged:
-            def wait(self_inner):
-                for w in works:
-                    w.wait()
-                for dst, src in recv:
-                    dst.copy_(src)
-                return True
-
-        return [_Staged()] if works else []
+            pairs.append((B[e - h:e], B[e:e + self.hb], self.rank + 1))
+        return exchange_rows(pairs, group, staged)
 
     def allreduce_stats(self, t_stats, group=None):
         """Adaptive thresholds (NEXT-2): the 9 exact int64 sums of lfe_stats are
@@ -212,3 +218,101 @@ def plan_bands(bands: int, H: int, world: int, halo: int):
         k, (b, a, e) = short[0]
         raise ValueError(f"rank {k} would own rows [{a}, {e}) of band {b}: {e - a} rows < halo {halo}; use fewer ranks")
     return work
+
+
+class BandShard:
+    """One rank's share of a multispectral scene (c4): the row ranges
+    ``plan_bands`` gives it.  Whole bands are computed in ONE lfe_extract_bands
+    launch with no collective; a band cut between two ranks is a strip of that
+    band, with the same one-hop halo exchange as a scene (only between the two
+    ranks sharing the band).
+
+    ``whole``: the bands owned entirely (consecutive); ``parts``: (band, a, b,
+    peer_above, peer_below) for pieces of cut bands, each with its own buffer
+    [halo above | rows | halo below] (peers are ranks, or None at a band edge)."""
+
+    def __init__(self, bands: int, H: int, W: int, rank: int, world: int, halo: int):
+        self.nbands, self.H, self.W, self.rank, self.world, self.halo = bands, H, W, rank, world, halo
+        items = plan_bands(bands, H, world, halo)[rank]
+        self.whole = [b for b, a, e in items if a == 0 and e == H]
+        if self.whole and self.whole != list(range(self.whole[0], self.whole[-1] + 1)):
+            raise AssertionError("whole bands of one rank are consecutive")
+        self.parts = []
+        for k, (b, a, e) in enumerate(items):
+            if a == 0 and e == H:
+                continue
+            # a cut piece is the first item (continues the previous rank's band) and/or
+            # the last (continued by the next rank)
+            above = rank - 1 if a > 0 else None
+            below = rank + 1 if e < H else None
+            self.parts.append((b, a, e, above, below))
+
+    def alloc(self, dtype, device):
+        import torch
+        self.whole_buf = (torch.zeros((len(self.whole), self.H, self.W), dtype=dtype, device=device)
+                          if self.whole else None)
+        self.part_bufs = []
+        for b, a, e, above, below in self.parts:
+            ha = self.halo if above is not None else 0
+            hb = self.halo if below is not None else 0
+            self.part_bufs.append(torch.zeros((ha + e - a + hb, self.W), dtype=dtype, device=device))
+        return self
+
+    def load_owned(self, scene):
+        """Copy the owned rows from a [bands, H, W] host array."""
+        import torch
+        if self.whole:
+            self.whole_buf.copy_(torch.from_numpy(scene[self.whole[0]:self.whole[-1] + 1]))
+        for (b, a, e, above, _), buf in zip(self.parts, self.part_bufs):
+            ha = self.halo if above is not None else 0
+            buf[ha:ha + e - a].copy_(torch.from_numpy(scene[b, a:e]))
+
+    def exchange(self, group=None, staged=None):
+        """Post the halo exchange of the cut pieces (isend/irecv with the rank
+        sharing the band); returns the works to wait on."""
+        h, pairs = self.halo, []
+        for (b, a, e, above, below), buf in zip(self.parts, self.part_bufs):
+            B = _bytes(buf)
+            ha = h if above is not None else 0
+            if above is not None:
+                pairs.append((B[ha:ha + h], B[0:ha], above))
+            if below is not None:
+                end = ha + e - a
+                pairs.append((B[end - h:end], B[end:end + h], below))
+        return exchange_rows(pairs, group, staged)
+
+    def part_calls(self):
+        """lfe_extract_rows arguments per cut piece: (piece index, s, n, halo_above,
+        halo_below, flags, needs_exchange) -- the rows computable before the
+        exchange completes first, the boundary rows after."""
+        from .lfe import LFE_BOTTOM_IS_EDGE, LFE_TOP_IS_EDGE
+        h, out_first, out_after = self.halo, [], []
+        for k, (b, a, e, above, below) in enumerate(self.parts):
+            R = e - a
+            lo = h if above is not None else 0
+            hi = R - h if below is not None else R
+
+            def call(s, n):
+                flags, need = 0, False
+                if above is None:
+                    ha, flags = s, flags | LFE_TOP_IS_EDGE
+                else:
+                    ha, need = h, need or s < h
+                if below is None:
+                    hb, flags = R - s - n, flags | LFE_BOTTOM_IS_EDGE
+                else:
+                    hb, need = h, need or s + n > R - h
+                return (k, s, n, ha, hb, flags, need)
+
+            if hi - lo <= 0:
+                out_after.append(call(0, R))
+                continue
+            out_first.append(call(lo, hi - lo))
+            if lo > 0:
+                out_after.append(call(0, lo))
+            if hi < R:
+                out_after.append(call(hi, R - hi))
+        return out_first + out_after
+
+    def owned_pixels(self) -> int:
+        return (len(self.whole) * self.H + sum(e - a for _, a, e, _, _ in self.parts)) * self.W

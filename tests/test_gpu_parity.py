@@ -152,21 +152,21 @@ def _sampled_rows(img, p, got, bands):
         assert_same(got[a:b], ref[a - lo:a - lo + (b - a)], f"rows {a}:{b}")
 
 
-def test_c3_full_size_sampled():
-    """c3 at its full 12000x12000 u16 size in bench.py's configuration; the
-    oracle checks sampled row bands including the first and last rows."""
+def test_c3_full_size():
+    """c3 at its full 12000x12000 u16 size in bench.py's configuration, every
+    pixel against the oracle's whole-scene run (the 148-CTA cost-weighted, TPC-
+    paired partition at the exact bench geometry)."""
     img = scenes.scene_c3()
     p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
-    got = run_gpu(img, p)
-    _sampled_rows(img, p, got, [(0, 40), (5997, 6031), (11960, 12000)])
+    assert_same(run_gpu(img, p), O.run(img, _oparams(p)), "c3 whole scene")
 
 
-def test_c4_band_full_size_sampled():
+def test_c4_band_full_size():
+    """Bands 0 and 3 of c4 (8192^2, 12-bit) each as a single image, in full."""
     img = scenes.scene_c4(size=8192)
     p = lfe.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
     for b in (0, 3):
-        got = run_gpu(img[b], p)
-        _sampled_rows(img[b], p, got, [(0, 24), (4100, 4124), (8170, 8192)])
+        assert_same(run_gpu(img[b], p), O.run(img[b], _oparams(p)), f"c4 band {b}")
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -435,13 +435,16 @@ def test_adaptive_thresholds_and_sums_equal_oracle():
             ctx.thresholds()
         d = torch.from_numpy(img).cuda()
         ctx.extract(d)
-        z, T, T3 = ctx.thresholds()
-        assert list(z) == [t for t, _ in zt]
-        assert T == (1.0 * sI, 1.0 * sI) and T3 == (1.5 * sI, -1.0)
+        with pytest.raises(lfe.LfeError):  # lfe_extract's thresholds are per call (lfe.h)
+            ctx.thresholds()
         # the raw sums of lfe_stats_rows against numpy integer sums of the oracle's r
         st = torch.zeros(9, dtype=torch.int64, device="cuda")
         ctx.stats_rows(d, 0, img.shape[0], 0, 0, lfe.LFE_TOP_IS_EDGE | lfe.LFE_BOTTOM_IS_EDGE, st)
         v = [int(x) for x in st.cpu()]
+        ctx.set_stats(v)
+        z, T, T3 = ctx.thresholds()
+        assert list(z) == [t for t, _ in zt]
+        assert T == (1.0 * sI, 1.0 * sI) and T3 == (1.5 * sI, -1.0)
     I = img.astype(np.int64)
     want = [I.size]
     rs, rq = [], []
@@ -497,18 +500,14 @@ def test_adaptive_extract_host():
             assert_same(ctx.extract_host(img), want, f"host strips {strip}")
 
 
-def test_adaptive_c3_full_size_sampled():
+def test_adaptive_c3_full_size():
     """c3 at full size with SPEC's adaptive default (t = 0.75 sigma(r)); the
-    whole-image thresholds come from the oracle's own 12000^2 pass."""
+    whole-image thresholds come from the oracle's own 12000^2 pass, and every
+    pixel is compared."""
     img = scenes.scene_c3()
     p = lfe.Params(bit_depth=10, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
     got = run_gpu(img, p)
-    op = _absolute_oparams(img, p)
-    H = img.shape[0]
-    for a, b in [(0, 24), (6000, 6030), (11976, 12000)]:
-        lo, hi = max(0, a - 8), min(H, b + 8)
-        ref = O.run(np.ascontiguousarray(img[lo:hi]), op)
-        assert_same(got[a:b], ref[a - lo:a - lo + (b - a)], f"rows {a}:{b}")
+    assert_same(got, O.run(img, _absolute_oparams(img, p)), "adaptive c3 whole scene")
 
 
 # ------------------------------ F32 masks (tolerance contract) and response std (NEXT-3) ----
@@ -645,10 +644,21 @@ def test_extract_is_cuda_graph_capturable():
         assert_same(out.cpu().numpy(), want, "graph replay")
 
 
-def test_c5_full_size_streamed_sampled():
+def c5_check_bands(H=48000, tile=12000, strip=2048):
+    """Row bands of the c5 mosaic the oracle checks: the first
+    and last rows, every tile seam, and a band across every host-strip boundary
+    near the middle of each tile row."""
+    bands = [(0, 16), (H - 16, H)]
+    bands += [(s - 10, s + 10) for s in range(tile, H, tile)]
+    bands += [(t * tile + 5 * strip - 8, t * tile + 5 * strip + 8) for t in range(H // tile)]
+    return bands
+
+
+def test_c5_full_size_streamed():
     """c5: the 48000 x 48000 u16 mosaic (4.6 GB) streamed from host memory through
-    lfe_extract_host; the oracle checks row bands at the image edges and across
-    the mosaic's tile seams."""
+    lfe_extract_host (2048-row strips); the oracle checks full-width row bands at
+    the image edges, across all three tile seams and across host-strip
+    boundaries in every tile row (9 bands + the 2 edges)."""
     T = 12000
     img = np.empty((4 * T, 4 * T), np.uint16)
     for i in range(16):
@@ -657,7 +667,7 @@ def test_c5_full_size_streamed_sampled():
     with lfe.Context(p) as ctx:
         ctx.set_option(lfe.LFE_OPT_HOST_STRIP_ROWS, 2048)
         got = ctx.extract_host(img)
-    _sampled_rows(img, p, got, [(0, 12), (11994, 12006), (23990, 24010), (47988, 48000)])
+    _sampled_rows(img, p, got, c5_check_bands())
 
 
 # ------------------------------------------------ multi-band scenes (NEXT-4) ----
@@ -686,9 +696,9 @@ def test_extract_bands_one_launch(kernel, bd, shape):
         assert_same(got[b], O.run(img[b], _oparams(p)), f"band {b}")
 
 
-def test_c4_all_bands_one_launch_full_size_sampled():
+def test_c4_all_bands_one_launch_full_size():
     """c4 at full size: 4 x 8192 x 8192 u16 (12-bit) bands in one lfe_extract_bands
-    call (fused kernel, 3-D tensor map), sampled rows of every band."""
+    call (fused kernel, 3-D tensor map), every pixel of every band."""
     img = scenes.scene_c4(size=8192)
     p = lfe.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
     with lfe.Context(p) as ctx:
@@ -696,7 +706,7 @@ def test_c4_all_bands_one_launch_full_size_sampled():
         got = ctx.extract_bands(d).cpu().numpy()
         ctx.check()
     for b in range(4):
-        _sampled_rows(img[b], p, got[b], [(0, 12), (4090 + b, 4106 + b), (8180, 8192)])
+        assert_same(got[b], O.run(img[b], _oparams(p)), f"band {b}")
 
 
 # ------------------------------ the paper's 5x5 -> 3x3 re-check on the fused path ----
@@ -832,24 +842,34 @@ def test_fused_range_check_and_rows_past_the_call(where):
         assert_same(out.cpu().numpy(), O.run(img, _oparams(p)), "rows past the call")
 
 
-def test_bench_two_ranks_on_one_gpu_verify():
-    """bench.py's N > 1 step (row strips, halo exchange, interior band overlapped
-    with the exchange, boundary bands, max-over-ranks timing) run as 2 ranks
-    sharing this GPU over gloo (LFE_BENCH_SHARE_GPUS; NCCL refuses duplicate
-    GPUs), with --verify: every rank's owned rows equal a whole-scene extraction."""
+@pytest.mark.parametrize("world,config,extra", [(2, "c3", ["--verify"]), (3, "c3", ["--adaptive", "0.75", "--verify"]),
+                                                (2, "c4", []), (8, "c4", [])])
+def test_bench_ranks_on_one_gpu(world, config, extra):
+    """bench.py's N > 1 step run as `world` ranks sharing this GPU over gloo
+    (LFE_BENCH_SHARE_GPUS; NCCL refuses duplicate GPUs): c3 row strips (halo
+    exchange, interior band overlapped with it, boundary bands, max-over-ranks
+    timing) with --verify (every rank's owned rows equal a whole-scene
+    extraction), and c4 bands dealt to 2 ranks (whole bands, no exchange) and 8
+    ranks (every band cut between two ranks).  Every rank also checks its rows
+    against the CPU oracle: the line's parity must be bit-exact."""
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, LFE_BENCH_SHARE_GPUS="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3", "--size", "2048", "--no-cpu-baseline", "--verify"]
-    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    size = "2048" if config == "c3" else "1024"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29517 + world), os.path.join(root, "bench.py"),
+           "--gpus", str(world), "--steps", "3", "--warmup", "3", "--config", config, "--size", size] + extra
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
-    assert line["n_gpus"] == 2 and line["verify"]["bit_exact_vs_whole_scene"], line
+    assert line["n_gpus"] == world, line
+    if "--verify" in extra:
+        assert line["verify"]["bit_exact_vs_whole_scene"], line
+    if "--adaptive" not in extra:
+        assert line["parity"]["differing"] == 0 and line["parity"]["pixels"] > 0, line
 
 
 def _extract_r_case(r0: np.ndarray, t_int, T: float):
@@ -910,3 +930,91 @@ def test_fused_zero_crossing_dense_random_responses(seed):
     H, W = 203, 456
     r0 = rng.choice(np.array([-5, -3, -2, -1, 0, 0, 1, 2, 3, 5], np.int64), size=(H, W)) * 997
     _extract_r_case(r0, (3 * 997, 4 * 997 + 1), 0.3)
+
+
+# ------------------------ hybrid median on device (Sec. 3.4; R16, R17) ----
+# lfe_test_extract_e runs the fused kernel with its merged image replaced by the
+# input (E = I), so the packed u16x2 median networks (med9 / med3 for the 5x5
+# filter, med5 / med3 for the second 3x3 level) are compared with the oracle's
+# sort-based definition on arbitrary E.
+def _extract_e(E: np.ndarray, m2: int = 0) -> np.ndarray:
+    H, W = E.shape
+    p = lfe.Params(bit_depth=16, hybrid_median=True, median_window=5, median_window2=m2,
+                   out_mode=lfe.LFE_OUT_EXTRACT)
+    d = _pitched((H, W), torch.uint16)
+    d.copy_(torch.from_numpy(np.ascontiguousarray(E, dtype=np.uint16)))
+    out = _pitched((H, W), torch.uint16)
+    with lfe.Context(p) as ctx:
+        ctx.test_extract_e(d, out)
+        ctx.check()
+    return out.cpu().numpy()
+
+
+def _hm_oracle(E: np.ndarray, m2: int = 0) -> np.ndarray:
+    o = O.hybrid_median(E, 5)
+    return O.hybrid_median(o, m2) if m2 else o
+
+
+# cell offsets of the '+' and 'x' groups of a 5x5 window (centre (2, 2) first)
+_PLUS = [(2, 2), (2, 0), (2, 1), (2, 3), (2, 4), (0, 2), (1, 2), (3, 2), (4, 2)]
+_CROSS = [(0, 0), (1, 1), (3, 3), (4, 4), (0, 4), (1, 3), (3, 1), (4, 0)]
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 1), (0x7FFF, 0x8000), (1, 0xFFFF), (300, 301)])
+def test_fused_hybrid_median_all_binary_groups(lo, hi):
+    """Every binary assignment of the 17 window positions the 5x5 hybrid median
+    reads (the '+' group, the 'x' group, shared centre: 2^17 = 131072 cells of
+    5x5, so all 512 patterns of each 9-group occur with every pattern of the
+    other), the remaining 8 positions random; values straddling the sign bit of
+    a u16 half and the pair/lane boundaries (cells are 5 wide, lanes 4).  The
+    whole image is compared, so pixels whose windows span several cells count
+    too."""
+    rng = np.random.default_rng(7000 + lo)
+    ncy, ncx = 256, 512
+    codes = np.arange(ncy * ncx, dtype=np.int64).reshape(ncy, ncx)
+    E = rng.choice(np.array([lo, hi], np.uint16), size=(5 * ncy, 5 * ncx))
+    for b, (dy, dx) in enumerate(_PLUS + _CROSS):
+        E[dy::5, dx::5] = np.where((codes >> b) & 1, hi, lo).astype(np.uint16)
+    got = _extract_e(E)
+    assert_same(got, _hm_oracle(E), f"binary groups {lo}/{hi}")
+    # the cell centres are exactly med3(med9(+), med9(x), centre) of the cell's own bits
+    bits = [(codes >> b) & 1 for b in range(17)]
+    plus = sum(bits[:9])
+    cross = bits[0] + sum(bits[9:])
+    want_c = np.where((((plus >= 5).astype(int) + (cross >= 5) + bits[0]) >= 2), hi, lo)
+    assert np.array_equal(got[2::5, 2::5], want_c.astype(np.uint16))
+
+
+@pytest.mark.parametrize("m2", [0, 3])
+@pytest.mark.parametrize("kind", ["full", "ties", "high", "binary"])
+def test_fused_hybrid_median_random_patches(m2, kind):
+    """Random multi-valued E through one (5x5) or two (5 then 3) median levels:
+    full-range u16 values, few-valued images full of ties, values at and above
+    0x8000, and random binary images (the second level then sees every 3x3
+    pattern the first level produces); ragged widths (W % 4 != 0: the general
+    column fix-up path) and multiples of 4 (the cheap column-edge path), edge-row
+    pieces, several column groups."""
+    rng = np.random.default_rng(7100 + 7 * m2 + len(kind))
+    for H, W in [(37, 150), (203, 1400), (130, 2701), (64, 2688)]:
+        if kind == "full":
+            E = rng.integers(0, 65536, size=(H, W), dtype=np.uint16)
+        elif kind == "ties":
+            E = rng.choice(np.array([0, 1, 2, 0x8000, 0xFFFF], np.uint16), size=(H, W))
+        elif kind == "high":
+            E = rng.integers(0x7FF0, 0x8010, size=(H, W), dtype=np.int64).astype(np.uint16)
+        else:
+            E = rng.choice(np.array([0, 0xFFFF], np.uint16), size=(H, W), p=[0.6, 0.4])
+        assert_same(_extract_e(E, m2), _hm_oracle(E, m2), f"{kind} {H}x{W} m2={m2}")
+
+
+def test_fused_second_level_all_binary_groups():
+    """The 3x3 second level (med5 network, R17): an image of 3x3 blocks carrying
+    every 9-bit binary code (plus random background bits), through both levels,
+    compared whole with the oracle's two sort-based levels."""
+    rng = np.random.default_rng(7200)
+    E = rng.choice(np.array([5, 0xFFF0], np.uint16), size=(3 * 96, 3 * 700))
+    codes = np.arange(96 * 700) % 512
+    for b in range(9):
+        dy, dx = divmod(b, 3)
+        E[dy::3, dx::3] = np.where((codes.reshape(96, 700) >> b) & 1, 0xFFF0, 5).astype(np.uint16)
+    assert_same(_extract_e(E, 3), _hm_oracle(E, 3), "second level")

@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle as O
 from paper_1304_3992_b200 import scenes
-from paper_1304_3992_b200.shard import StripShard, plan_strips
+from paper_1304_3992_b200.shard import BandShard, StripShard, plan_bands, plan_strips
 
 
 def _free_port():
@@ -61,7 +61,7 @@ def _worker(rank, world, port, H, W, hm, q, staged=False):
         sh.load_owned(img)
         # staged: the host-staged variant used for gloo groups over device buffers
         # (the one-GPU N > 1 bench hook), here exercised on CPU buffers
-        for w in (sh._exchange_host_staged(None) if staged else sh.exchange()):
+        for w in sh.exchange(staged=staged):
             w.wait()
         # received halos equal the neighbours' boundary rows
         if sh.ha:
@@ -194,3 +194,68 @@ def test_plan_bands_short_whole_bands_are_fine():
     from paper_1304_3992_b200.shard import plan_bands
     work = plan_bands(4, 5, 4, 7)  # bands shorter than the halo, dealt out whole
     assert work == [[(0, 0, 5)], [(1, 0, 5)], [(2, 0, 5)], [(3, 0, 5)]]
+
+
+def _band_worker(rank, world, port, bands, H, W, staged, q):
+    """Each rank: its BandShard (whole bands + cut pieces), the halo exchange of
+    the cut pieces, then every piece computed the way bench.py hands it to
+    lfe_extract_bands / lfe_extract_rows -- with the oracle standing in."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(91)
+        scene = np.stack([scenes.random_image(rng, H, W, 12, "mixed") for _ in range(bands)])
+        p = O.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
+        halo = 7
+        bs = BandShard(bands, H, W, rank, world, halo)
+        bs.alloc(torch.int16, "cpu")  # 2-byte rows like the uint16 device buffers
+        bs.load_owned(scene.astype(np.int16))
+        for w in bs.exchange(staged=staged):
+            w.wait()
+        res = []
+        for b in bs.whole:
+            res.append((b, 0, O.run(scene[b], p)))
+        outs = [np.zeros((e - a, W), np.uint16) for _, a, e, _, _ in bs.parts]
+        for k, s, n, ha, hb, flags, need in bs.part_calls():
+            b, a, e, above, below = bs.parts[k]
+            B = bs.part_bufs[k].numpy().astype(np.uint16)
+            r0 = (halo if above is not None else 0) + s
+            sub = np.ascontiguousarray(B[r0 - ha:r0 + n + hb])
+            outs[k][s:s + n] = O.run(sub, p)[ha:ha + n]
+        for (b, a, e, _, _), o in zip(bs.parts, outs):
+            res.append((b, a, o))
+        q.put((rank, bs.owned_pixels(), res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,staged", [(2, False), (3, False), (8, False), (8, True)])
+def test_gloo_band_shards_reproduce_every_band(world, staged):
+    """c4's multi-GPU plan: 4 bands dealt to 2 ranks (whole bands, no exchange),
+    3 ranks (bands cut mid-way), 8 ranks (every band cut between two ranks, one
+    exchange per pair) -- the union of every rank's rows equals the oracle on
+    each band."""
+    bands, H, W = 4, 40, 56
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, bands, H, W, staged, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    rng = np.random.default_rng(91)
+    scene = np.stack([scenes.random_image(rng, H, W, 12, "mixed") for _ in range(bands)])
+    p = O.Params(bit_depth=12, zc_threshold=(0.01, 0.01))
+    full = np.zeros((bands, H, W), np.uint16)
+    cover = np.zeros((bands, H), np.int64)
+    for _, px, res in got:
+        assert px == sum(o.shape[0] * W for _, _, o in res)
+        for b, a, o in res:
+            full[b, a:a + o.shape[0]] = o
+            cover[b, a:a + o.shape[0]] += 1
+    assert (cover == 1).all()
+    for b in range(bands):
+        np.testing.assert_array_equal(full[b], O.run(scene[b], p))

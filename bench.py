@@ -82,6 +82,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true", help="do not report the oracle timing")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check of the last step")
     ap.add_argument("--no-graph", action="store_true", help="c1/c2 at N=1: plain launches instead of graph replay")
+    ap.add_argument("--halo", choices=["auto", "peer", "nccl"], default="auto",
+                    help="N > 1 row strips: 'peer' = one launch per step reading the halo rows from the "
+                         "neighbours' HBM (CUDA IPC, lfe_extract_rows_peer); 'nccl' = NCCL halo exchange with "
+                         "the interior band overlapped; auto = peer (nccl for --adaptive)")
     ap.add_argument("--verify", action="store_true",
                     help="after timing, check every rank's owned output rows against a whole-scene "
                          "extraction on its own GPU (bit-exact); adds \"verify\" to the line")
@@ -149,16 +153,22 @@ def _backend_name():
     return "NCCL" if b == "nccl" else f"{b} (host-staged; ranks sharing a GPU: test hook, not a measurement)"
 
 
-def config_dict(name, cfg, world, p, graph=False):
+def config_dict(name, cfg, world, p, graph=False, halo_mode=None):
     hm = "5x5 hybrid median" + (f" + {p.median_window2}x{p.median_window2} second level" if p.median_window2 else "")
     zc = (f"ZC (adaptive gap {p.zc_threshold[0]} x global std of r, statistics pre-pass)" if p.adaptive
           else f"ZC (gap {p.zc_threshold[0]})")
     H, W, B, e = cfg["H"], cfg["W"], cfg["bands"], elem(cfg)
     in_bytes = B * H * W * e
     if world > 1:
-        par = (f"bands dealt to {world} ranks (plan_bands; a band cut between two ranks gets a "
-               f"{halo_rows(p)}-row {_backend_name()} halo exchange)" if B > 1 else
-               f"row strips x{world}, {halo_rows(p)}-row {_backend_name()} halo exchange")
+        if B > 1:
+            par = (f"bands dealt to {world} ranks (plan_bands; a band cut between two ranks gets a "
+                   f"{halo_rows(p)}-row {_backend_name()} halo exchange)")
+        elif halo_mode == "peer":
+            par = (f"row strips x{world}; each rank's one launch per step TMA-loads the {halo_rows(p)} halo rows "
+                   "above/below from its neighbours' HBM (CUDA IPC peer mapping, NVLink), after their per-step "
+                   "'input ready' flag; no exchange step")
+        else:
+            par = f"row strips x{world}, {halo_rows(p)}-row {_backend_name()} halo exchange"
     else:
         par = "single GPU" + (", one launch per step replayed as a CUDA graph" if graph else "")
     l2 = (f"inputs larger than L2 ({in_bytes / 1e6:.0f} MB in + {in_bytes / 1e6:.0f} MB out per step > 126 MB L2); "
@@ -480,6 +490,8 @@ def main():
             kernel_events.append((e0, e1, px))
 
     # ---------------- device buffers and the step ----------------
+    import torch.distributed as dist  # noqa: F401 (N > 1 only)
+    halo_mode = None
     if NB > 1:  # c4: bands
         bs = shard_mod.BandShard(NB, H, W, rank, world, halo)
         bs.alloc(tdt, dev)
@@ -512,7 +524,42 @@ def main():
             if not waited:
                 for w in works:
                     w.wait()
+    elif world > 1 and args.halo != "nccl" and not p.adaptive:
+        # peer halos: every rank holds only its owned rows; one launch per step reads the
+        # neighbours' boundary rows in place (their HBM over NVLink), after their "input
+        # ready" flag for this step
+        scene = Scene(name, cfg)
+        shard = shard_mod.PeerStripShard(H, W, rank, world, halo)
+        buf = shard.alloc(tdt, dev)
+        scene.hold(shard.a - shard.ha, shard.b + shard.hb, pinned=not args.no_e2e)
+        buf.copy_(torch.from_numpy(scene.rows(shard.a, shard.b)))
+        out = torch.empty((shard.rows, W), dtype=tdt, device=dev)
+        torch.cuda.synchronize(dev)
+        shard.connect()
+        da, pa, db, pb, fa, fb = shard.call_args()
+        share = bool(os.environ.get("LFE_BENCH_SHARE_GPUS"))
+        if share:
+            # ranks sharing one GPU time-slice between processes: signal once, up front,
+            # so that no kernel ever spins on a neighbour that cannot run
+            lfe.lfe_signal(shard.flag.data_ptr(), 1 << 62, cur_stream().cuda_stream)
+            torch.cuda.synchronize(dev)
+        dist.barrier()  # every rank's rows are in place before any neighbour reads them
+        owned_px = shard.rows * W
+        counter = [0]
+        bpitch, opitch = buf.stride(0) * esz, out.stride(0) * esz
+        halo_mode = "peer"
+
+        def step(record=False):
+            counter[0] += 1
+            v = 1 if share else counter[0]
+            sp = cur_stream().cuda_stream
+            if not share:  # this step's input is in place: neighbours may read it
+                lfe.lfe_signal(shard.flag.data_ptr(), v, sp)
+            rec(record, lambda: lfe.lfe_extract_rows_peer(
+                ctx.handle, buf.data_ptr(), bpitch, W, shard.rows, da, pa, db, pb, shard.edge_flags(), fa, fb, v,
+                out.data_ptr(), opitch, sp), owned_px)
     else:
+        halo_mode = "nccl"
         scene = Scene(name, cfg)
         shard = shard_mod.StripShard(H, W, rank, world, halo)
         buf = shard.alloc(tdt, dev)
@@ -730,7 +777,7 @@ def main():
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": config_dict(name, cfg, world, p, graph=graph is not None),
+            "config": config_dict(name, cfg, world, p, graph=graph is not None, halo_mode=halo_mode),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel": "lfe fused stencil kernel (dominant launch: the interior band / all whole bands)"
@@ -777,9 +824,12 @@ def main():
                 line["roofline"]["traffic_stale"] = tr.get("bytes_per_launch")
         line["kernel_source_sha"] = src
         print(json.dumps(line), flush=True)
+    if halo_mode == "peer":
+        torch.cuda.synchronize(dev)
+        dist.barrier()  # no neighbour reads this rank's rows any more
+        shard.close()
     ctx.close()
     if world > 1:
-        import torch.distributed as dist
         dist.destroy_process_group()
 
 

@@ -162,6 +162,45 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_
                             uint32_t edge_flags, void *d_out_row0, int64_t out_pitch_bytes,
                             void *cuda_stream);
 
+/* One row strip whose halo rows stay in the NEIGHBOURS' memory (multi-GPU
+ * row strips on one NVLink/NVSwitch node, north_star; the paper's "data
+ * transfer ... to be minimized"): the fused kernel TMA-loads
+ * the rows above/below the strip straight from d_above / d_below (a peer
+ * GPU's HBM mapped with lfe_ipc_open, or any device pointer this device can
+ * read), so no exchange step runs.  d_in_row0: the strip's first owned row
+ * (`rows` rows, in_pitch_bytes).  d_above: the first of the lfe_halo(c) rows
+ * immediately above the strip (pitch above_pitch_bytes); NULL and ignored
+ * when edge_flags has LFE_TOP_IS_EDGE (the strip's row 0 is the image top).
+ * d_below: the first row below the strip, likewise with LFE_BOTTOM_IS_EDGE.
+ * wait_above / wait_below (device or mapped peer pointers to uint64, may be
+ * NULL): before reading a row of that neighbour the kernel waits until the
+ * flag is >= wait_value (acquire, system scope) -- the neighbour's "input
+ * ready" signal for this step (lfe_signal).  The result equals the
+ * whole-image result bit for bit.  Needs the fused kernel (5x5 masks, std on
+ * the ZC image, 16-byte aligned bases/pitches): EUNSUPPORTED otherwise.  The
+ * neighbours must not modify those rows until the enqueued work completes.
+ * Errors as lfe_extract_rows. */
+lfe_status lfe_extract_rows_peer(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_bytes, int32_t width,
+                                 int32_t rows, const void *d_above, int64_t above_pitch_bytes,
+                                 const void *d_below, int64_t below_pitch_bytes, uint32_t edge_flags,
+                                 const uint64_t *wait_above, const uint64_t *wait_below, uint64_t wait_value,
+                                 void *d_out_row0, int64_t out_pitch_bytes, void *cuda_stream);
+
+/* Enqueues on cuda_stream a system-scope release store of `value` to the
+ * device flag *d_flag (the "input ready" signal lfe_extract_rows_peer waits
+ * on; the flag lives in the signalling rank's memory).  Errors: EINVAL, ECUDA. */
+lfe_status lfe_signal(uint64_t *d_flag, uint64_t value, void *cuda_stream);
+
+/* CUDA IPC plumbing for peer-halo strips across processes (one process per
+ * GPU): lfe_ipc_export fills 64 opaque bytes naming the device allocation
+ * that holds d_ptr and the offset of d_ptr in it; lfe_ipc_open, in another
+ * process, maps that allocation (enabling peer access) and returns the same
+ * address in its space (*d_ptr); lfe_ipc_close(d_ptr, offset) unmaps it.
+ * Errors: EINVAL, ECUDA. */
+lfe_status lfe_ipc_export(const void *d_ptr, unsigned char handle[64], int64_t *offset);
+lfe_status lfe_ipc_open(const unsigned char handle[64], int64_t offset, void **d_ptr);
+lfe_status lfe_ipc_close(void *d_ptr, int64_t offset);
+
 /* End-to-end call on HOST buffers (the paper's H2D -> kernel -> D2H flow,
  * PAPER.md:150, Table 6): copies the image in row strips to device staging
  * buffers owned by the ctx, runs lfe_extract_rows per strip and copies the

@@ -188,7 +188,21 @@ bool fused_supports(const KParams &kp, int bit_depth)
 
 // FusedArgs and the input tensor map of one launch; false: nothing to do (empty
 // range) or no map (returned in *err)
-bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, fz::FusedArgs &fa, CUtensorMap &map,
+static bool encode_map(CUtensorMap *map, bool in16, const void *base, int width, int rows, int bands, int64_t pitch,
+                       int64_t band_stride, int box_rows)
+{
+    // u8 rows are fetched as u16 pairs (the row pitch is a multiple of 16 bytes,
+    // so the pair holding an odd last pixel stays inside the row)
+    const cuuint64_t dims[3] = {(cuuint64_t)(in16 ? width : (width + 1) / 2), (cuuint64_t)rows, (cuuint64_t)bands};
+    const cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)(bands > 1 ? band_stride : pitch * (int64_t)rows)};
+    const cuuint32_t box[3] = {(cuuint32_t)(in16 ? 232 : 240), (cuuint32_t)box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, fz::FusedArgs &fa, fz::Maps &maps,
                    cudaError_t *err)
 {
     using namespace fz;
@@ -223,24 +237,40 @@ bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, 
     fa.out_pitch = g.out_pitch;
     fa.dbg = nullptr;
     fa.dbg_nofix = getenv("LFE_DEBUG_NOFIX") != nullptr;
+    fa.peer = g.peer() ? 1 : 0;
+    fa.seg_a = g.ha_peer;
+    fa.seg_b = g.Hv - g.hb_peer;
+    fa.wait_flag[0] = g.wait_flag[0];
+    fa.wait_flag[1] = g.wait_flag[1];
+    fa.wait_value = g.wait_value;
     if (g.o1 <= g.o0 || g.width <= 0) return false;
 
-    // u8 rows are fetched as u16 pairs (the row pitch is a multiple of 16 bytes,
-    // so the pair holding an odd last pixel stays inside the row)
-    const cuuint64_t dims[3] = {(cuuint64_t)(in16 ? g.width : (g.width + 1) / 2), (cuuint64_t)g.Hv,
-                                (cuuint64_t)g.bands};
-    const cuuint64_t strides[2] = {(cuuint64_t)g.in_pitch,
-                                   (cuuint64_t)(g.bands > 1 ? g.in_band_stride : g.in_pitch * (int64_t)g.Hv)};
-    const cuuint32_t box[3] = {(cuuint32_t)(in16 ? 232 : 240), (cuuint32_t)kR, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(g.in), dims, strides, box,
-                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
+    fa.seg_base[0] = static_cast<const unsigned char *>(g.above);
+    fa.seg_base[1] = static_cast<const unsigned char *>(g.in);
+    fa.seg_base[2] = static_cast<const unsigned char *>(g.below);
+    fa.seg_pitch[0] = g.above_pitch;
+    fa.seg_pitch[1] = g.in_pitch;
+    fa.seg_pitch[2] = g.below_pitch;
+    const int own_rows = g.Hv - g.ha_peer - g.hb_peer;
+    const bool ok = encode_map(&maps.own, in16, g.in, g.width, own_rows, g.bands, g.in_pitch, g.in_band_stride, kR);
+    if (!ok) {
         *err = cudaErrorInvalidValue;
         return false;
     }
     return true;
+}
+
+namespace {
+__global__ void signal_kernel(unsigned long long *flag, unsigned long long value)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+}  // namespace
+
+cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cudaStream_t s)
+{
+    signal_kernel<<<1, 1, 0, s>>>(flag, value);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h, int *err_flag,
@@ -248,9 +278,9 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
 {
     (void)tile_w;
     fz::FusedArgs fa;
-    CUtensorMap map;
+    fz::Maps maps;
     cudaError_t e;
-    if (!prepare_fused(kp, g, in16, tile_h, fa, map, &e)) return e;
+    if (!prepare_fused(kp, g, in16, tile_h, fa, maps, &e)) return e;
     fz::Variant v;
     v.in16 = in16;
     v.hml = kp.m2 ? 2 : kp.hm ? 1 : 0;
@@ -258,9 +288,11 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     v.rc = kp.recheck[0] || kp.recheck[1];
     // the GAP variant is exact for t = 0 as well; the two-level filter and the 3x3
     // re-check only have that one
-    v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc;
-    for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3}) {
-        e = group(v, fa, map, err_flag, s);
+    v.peer = g.peer();
+    v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer;
+    for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
+                       fz::launch_group4, fz::launch_group5}) {
+        e = group(v, fa, maps, err_flag, s);
         if (e != cudaErrorNotSupported) return e;
     }
     return cudaErrorNotSupported;

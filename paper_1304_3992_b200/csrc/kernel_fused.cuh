@@ -101,6 +101,25 @@ struct FusedArgs {
     long long out_pitch;
     unsigned long long *dbg;  // optional per-CTA [start, end, items] globaltimer record (LFE_DEBUG_TIMING)
     int dbg_nofix;            // timing experiments only: never take the column-fix path (wrong borders)
+    // Peer-halo strips (lfe_extract_rows_peer): virtual rows [0, seg_a) are the rows
+    // above (seg_base[0], pitch seg_pitch[0]), [seg_a, seg_b) the own rows (the tensor
+    // map; own row = virtual row - seg_a; also seg_base[1]), [seg_b, H) the rows below
+    // (seg_base[2]) -- the neighbours' rows, read in place (their HBM over NVLink).  A
+    // stage touching a peer segment is loaded row by row with 1-D bulk copies (a
+    // tensor-map box row is not 128-byte aligned in shared memory).  Before its first
+    // peer row the producer waits until the neighbour's flag (*wait_flag[0] above,
+    // [1] below; NULL = none) reaches wait_value.
+    int peer, seg_a, seg_b;
+    const unsigned char *seg_base[3];
+    long long seg_pitch[3];
+    const unsigned long long *wait_flag[2];
+    unsigned long long wait_value;
+};
+
+// The launch's input tensor map(s): `own`, 8-row boxes over the whole virtual image
+// (or over the own rows of a peer-halo strip).
+struct alignas(64) Maps {
+    CUtensorMap own;
 };
 
 // rows of input needed beyond the output rows: LoG 2 + ZC 1 + std 2 (+ HM 2) (+ second level 1)
@@ -127,12 +146,15 @@ struct Variant {
     bool mask;  // LFE_OUT_MASK
     bool gap;   // ZC gap test compiled in
     bool rc;    // 3x3 re-check compiled in
+    bool peer;  // peer-halo strip (halo rows in the neighbours' memory)
 };
-using GroupFn = cudaError_t (*)(const Variant &, const FusedArgs &, const CUtensorMap &, int *, cudaStream_t);
-cudaError_t launch_group0(const Variant &, const FusedArgs &, const CUtensorMap &, int *, cudaStream_t);
-cudaError_t launch_group1(const Variant &, const FusedArgs &, const CUtensorMap &, int *, cudaStream_t);
-cudaError_t launch_group2(const Variant &, const FusedArgs &, const CUtensorMap &, int *, cudaStream_t);
-cudaError_t launch_group3(const Variant &, const FusedArgs &, const CUtensorMap &, int *, cudaStream_t);
+using GroupFn = cudaError_t (*)(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group0(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group1(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group2(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group3(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group4(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group5(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -142,7 +164,7 @@ enum { kTvNone = 0, kTvInjectR = 1, kTvInjectE = 2 };
 
 // parameters + tensor map of one launch (kernel_fused.cu); false: nothing to launch
 // (*err = cudaSuccess for an empty range, else the map error)
-bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, fz::FusedArgs &fa, CUtensorMap &map,
+bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, fz::FusedArgs &fa, fz::Maps &maps,
                    cudaError_t *err);
 
 namespace {
@@ -268,8 +290,13 @@ __device__ __forceinline__ float hi16f(uint32_t w) { return __uint_as_float(prmt
 __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uint_as_float(prmt(w, 0x4B00u, sel)) - 8388608.0f; }
 
 #define LFE_FUSED_VARIANT(A, B, C, D, E)                                                   \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E) \
-        return launch_t<A, B, C, D, E>(fa, map, err_flag, s);
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer) \
+        return launch_t<A, B, C, D, E>(fa, maps, err_flag, s);
+// peer-halo strips (lfe_extract_rows_peer): a separate instantiation, so that the
+// producer of every other launch is exactly the plain one
+#define LFE_FUSED_PEER_VARIANT(A, B, C)                                                    \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer) \
+        return launch_t<A, B, C, true, false, true>(fa, maps, err_flag, s);
 
 // ---- left/right image-edge fix-ups (border warps only) ----------------------
 struct Fix {
@@ -420,17 +447,77 @@ struct Pieces {
 };
 
 // ---- TMA producer (lane 0 of the last warp) -------------------------------------------
-template <bool IN16, int kHalo, int kStageBytes, int kBoxBytes, int kBoxCols, int kNBox>
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <bool IN16, bool PEER, int kHalo, int kStageBytes, int kBoxBytes, int kBoxCols, int kNBox>
 struct Producer {
     const FusedArgs *a;
-    const CUtensorMap *map;
+    const Maps *maps;
     uint64_t *full, *empty;
     unsigned char *ring;
     Pieces pcs;
     Item it;
     int k = 0;
     bool have = false, done = false;
+    bool peers_ready = false;
     uint32_t g = 0;
+
+    // the 8-row (or, for a peer-halo stage, the 1-row) boxes of one row band
+    __device__ __forceinline__ void load(unsigned char *dst, const CUtensorMap *map, int y, uint64_t *bar)
+    {
+#pragma unroll
+        for (int b = 0; b < kNBox; ++b) {
+            if constexpr (IN16)
+                tma_load_3d(dst + b * kBoxBytes, map, it.xo - kHaloX + b * kBoxCols, y, it.band, bar);
+            else
+                tma_load_3d(dst + b * kBoxBytes, map, (it.xo - 2 * kHaloX + b * kBoxCols) / 2, y, it.band, bar);
+        }
+    }
+
+    // a stage touching the neighbours' rows (peer-halo strips): row by row from the
+    // segment holding it (rows past the image end are never read: any valid row), each
+    // box row by one 1-D bulk copy of its in-image part (16-byte granules; the columns
+    // outside [0, W) are never read as image values).  Returns the bytes it requested.
+    // Out of line: only the first/last stages of a strip's edge pieces take it.
+    __device__ __forceinline__ uint32_t load_peer_rows(unsigned char *dst, int y, uint64_t *bar)
+    {
+        if (!peers_ready) {
+            for (int j = 0; j < 2; ++j)
+                if (a->wait_flag[j])
+                    while (ld_acquire_sys(a->wait_flag[j]) < a->wait_value) __nanosleep(64);
+            peers_ready = true;
+        }
+        constexpr int kE = IN16 ? 2 : 1;                      // bytes per pixel
+        const int wr = ((a->W * kE + 15) & ~15) / kE;          // row length rounded to 16 bytes
+        const int x0 = it.xo - (IN16 ? kHaloX : 2 * kHaloX);  // first column of box 0
+        uint32_t bytes = 0;
+#pragma unroll 1
+        for (int r = 0; r < kR; ++r) {
+            const int yr = min(y + r, a->H - 1);
+            const int sgi = yr < a->seg_a ? 0 : yr >= a->seg_b ? 2 : 1;
+            const int ym = yr - (sgi == 0 ? 0 : sgi == 2 ? a->seg_b : a->seg_a);
+            const unsigned char *row = a->seg_base[sgi] + (long long)ym * a->seg_pitch[sgi];
+#pragma unroll 1
+            for (int b = 0; b < kNBox; ++b) {
+                const int c0 = x0 + b * kBoxCols, c1 = c0 + kBoxCols;
+                const int lo = max(c0, 0), hi = min(c1, wr);
+                if (hi <= lo) continue;
+                const uint32_t n = (uint32_t)(hi - lo) * kE;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(dst + b * kBoxBytes + r * kBoxCols * kE + (lo - c0) * kE)),
+                    "l"(row + (long long)lo * kE), "r"(n), "r"(smem_u32(bar))
+                    : "memory");
+                bytes += n;
+            }
+        }
+        return bytes;
+    }
 
     // issue stages while fewer than kS are outstanding beyond `released`
     __device__ __forceinline__ void run(uint32_t released)
@@ -447,23 +534,23 @@ struct Producer {
             const int slot = g % kS;
             const uint32_t use = g / kS;
             if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
-            mbar_expect_tx(&full[slot], kStageBytes);
             unsigned char *dst = ring + slot * kStageBytes;
             const int y = it.plo + k * kR;
-#pragma unroll
-            for (int b = 0; b < kNBox; ++b) {
-                if constexpr (IN16)
-                    tma_load_3d(dst + b * kBoxBytes, map, it.xo - kHaloX + b * kBoxCols, y, it.band, &full[slot]);
-                else
-                    tma_load_3d(dst + b * kBoxBytes, map, (it.xo - 2 * kHaloX + b * kBoxCols) / 2, y, it.band,
-                                &full[slot]);
+            if (!PEER || (y >= a->seg_a && y + kR <= a->seg_b)) {
+                mbar_expect_tx(&full[slot], kStageBytes);
+                load(dst, &maps->own, PEER ? y - a->seg_a : y, &full[slot]);
+            } else {
+                // the bytes are known only after the copies are issued: count them, then
+                // arrive with that transaction count (the phase cannot complete before
+                // the arrival, and the copies' complete_tx may land before or after it)
+                const uint32_t bytes = load_peer_rows(dst, y, &full[slot]);
+                mbar_expect_tx(&full[slot], bytes);
             }
             ++g;
             if (++k == it.nst) have = false;
         }
     }
 };
-
 
 
 // HML: hybrid-median levels -- 0 none, 1 the 5x5 filter, 2 the 5x5 filter followed
@@ -474,9 +561,9 @@ struct Producer {
 //     injected responses;
 //   kTvInjectE (lfe_test_extract_e): the merged image is replaced by the input itself,
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, int TV = kTvNone>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone>
 __global__ void __launch_bounds__(kThreads, 1)
-    fused_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ FusedArgs a, int *err_flag)
+    fused_kernel(const __grid_constant__ Maps maps, const __grid_constant__ FusedArgs a, int *err_flag)
 {
     constexpr bool HM = HML >= 1, HM2 = HML == 2;
     constexpr int kElem = IN16 ? 2 : 1;
@@ -511,13 +598,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&empty[s], kWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.own)) : "memory");
     }
     __syncthreads();
 
-    Producer<IN16, kHalo, kStageBytes, kBoxBytes, kBoxCols, kNBox> prod;
+    Producer<IN16, PEER, kHalo, kStageBytes, kBoxBytes, kBoxCols, kNBox> prod;
     prod.a = &a;
-    prod.map = &tmap;
+    prod.maps = &maps;
     prod.full = full;
     prod.empty = empty;
     prod.pcs.init(a);
@@ -1181,10 +1268,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.dbg[6 * blockIdx.x + 5] = pr.u1;
     }
 }
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, int TV = kTvNone>
-cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone>
+cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, TV>;
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV>;
     constexpr size_t smem = fused_smem<IN16, HML>();
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)
@@ -1212,7 +1299,7 @@ cudaError_t launch_t(const FusedArgs &fa, const CUtensorMap &map, int *err_flag,
     FusedArgs fb = fw;
     fb.dbg = nullptr;
     if (dbg_path) cudaMalloc(&fb.dbg, sizeof(unsigned long long) * 6 * grid);
-    kfn<<<grid, kThreads, smem, s>>>(map, fb, err_flag);
+    kfn<<<grid, kThreads, smem, s>>>(maps, fb, err_flag);
     e = cudaGetLastError();
     if (dbg_path && fb.dbg) {  // debug only: synchronous dump of the per-CTA timeline
         cudaStreamSynchronize(s);

@@ -6,7 +6,7 @@
 namespace lfe {
 namespace fz {
 
-cudaError_t launch_group0(const Variant &v, const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
+cudaError_t launch_group0(const Variant &v, const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
     LFE_FUSED_VARIANT(true, 1, false, true, false)
     LFE_FUSED_VARIANT(true, 1, false, false, false)

@@ -6,7 +6,7 @@
 namespace lfe {
 namespace fz {
 
-cudaError_t launch_group3(const Variant &v, const FusedArgs &fa, const CUtensorMap &map, int *err_flag, cudaStream_t s)
+cudaError_t launch_group3(const Variant &v, const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
     LFE_FUSED_VARIANT(false, 2, false, true, false)
     LFE_FUSED_VARIANT(false, 2, true, true, false)

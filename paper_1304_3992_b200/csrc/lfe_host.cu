@@ -5,6 +5,7 @@
 // thresholds (R9, R11, R12), launch planning for the two kernels, the strip
 // entry point used by multi-GPU sharding and the host-buffer end-to-end call.
 // Product code: shares nothing with oracle/.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -229,7 +230,13 @@ lfe_status run(lfe_ctx *c, const KParams &kp, const Geometry &g, cudaStream_t s)
     const bool aligned = ((reinterpret_cast<uintptr_t>(g.in) | reinterpret_cast<uintptr_t>(g.out) |
                            (uintptr_t)g.in_pitch | (uintptr_t)g.out_pitch | (uintptr_t)g.in_band_stride |
                            (uintptr_t)g.out_band_stride) & 15u) == 0;
-    const bool fused_ok = aligned && fused_supports(kp, c->p.bit_depth);
+    const bool peer_aligned = ((reinterpret_cast<uintptr_t>(g.above) | reinterpret_cast<uintptr_t>(g.below) |
+                                (uintptr_t)g.above_pitch | (uintptr_t)g.below_pitch) & 15u) == 0;
+    const bool fused_ok = aligned && peer_aligned && fused_supports(kp, c->p.bit_depth);
+    if (g.peer() && !fused_ok)
+        return fail(LFE_EUNSUPPORTED, "peer-halo strips need the fused kernel (5x5 masks, std on the ZC image, "
+                                      "16-byte aligned bases and pitches)");
+    if (g.peer() && k == LFE_KERNEL_STAGED) return fail(LFE_EUNSUPPORTED, "peer-halo strips need the fused kernel");
     if (k == LFE_KERNEL_AUTO) k = fused_ok ? LFE_KERNEL_FUSED : LFE_KERNEL_STAGED;
     if (k == LFE_KERNEL_FUSED && !fused_ok)
         return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
@@ -608,6 +615,107 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch,
     if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
     return extract_rows(c, c->kp, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, d_out_row0,
                         out_pitch, (cudaStream_t)stream);
+}
+
+lfe_status lfe_extract_rows_peer(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
+                                 const void *d_above, int64_t above_pitch, const void *d_below, int64_t below_pitch,
+                                 uint32_t edge_flags, const uint64_t *wait_above, const uint64_t *wait_below,
+                                 uint64_t wait_value, void *d_out_row0, int64_t out_pitch, void *stream)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
+    lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_out_row0, out_pitch, rows);
+    if (st != LFE_OK) return st;
+    if (edge_flags & ~3u) return fail(LFE_EINVAL, "unknown edge flag");
+    const bool top = edge_flags & LFE_TOP_IS_EDGE, bot = edge_flags & LFE_BOTTOM_IS_EDGE;
+    const int h = c->kp.halo;
+    if ((!top || !bot) && (c->kp.recheck[0] || c->kp.recheck[1]))
+        return fail(LFE_EUNSUPPORTED, "peer-halo strips: no variant with the 3x3 re-check is compiled");
+    const int64_t row_bytes = (int64_t)W * (int64_t)elem_in(c);
+    if (!top && (!d_above || above_pitch < row_bytes || above_pitch % (int64_t)elem_in(c)))
+        return fail(LFE_EINVAL, "d_above / above_pitch invalid for an inner top side");
+    if (!bot && (!d_below || below_pitch < row_bytes || below_pitch % (int64_t)elem_in(c)))
+        return fail(LFE_EINVAL, "d_below / below_pitch invalid for an inner bottom side");
+    if (overlap(d_in_row0, (size_t)(rows - 1) * in_pitch + row_bytes, d_out_row0,
+                (size_t)(rows - 1) * out_pitch + W * elem_out(c)))
+        return fail(LFE_EINVAL, "input and output overlap");
+    Geometry g;
+    g.in = d_in_row0;
+    g.in_pitch = in_pitch;
+    g.out = d_out_row0;
+    g.out_pitch = out_pitch;
+    g.width = W;
+    g.ha_peer = top ? 0 : h;
+    g.hb_peer = bot ? 0 : h;
+    g.Hv = rows + g.ha_peer + g.hb_peer;
+    g.o0 = g.ha_peer;
+    g.o1 = g.ha_peer + rows;
+    g.above = top ? nullptr : d_above;
+    g.above_pitch = top ? 0 : above_pitch;
+    g.below = bot ? nullptr : d_below;
+    g.below_pitch = bot ? 0 : below_pitch;
+    g.wait_flag[0] = top ? nullptr : reinterpret_cast<const unsigned long long *>(wait_above);
+    g.wait_flag[1] = bot ? nullptr : reinterpret_cast<const unsigned long long *>(wait_below);
+    g.wait_value = wait_value;
+    if (!g.peer()) {  // both sides are image edges: a plain whole-strip call
+        g.Hv = rows;
+        g.o0 = 0;
+        g.o1 = rows;
+    }
+    return run(c, c->kp, g, (cudaStream_t)stream);
+}
+
+lfe_status lfe_signal(uint64_t *d_flag, uint64_t value, void *stream)
+{
+    if (!d_flag || (reinterpret_cast<uintptr_t>(d_flag) & 7u)) return fail(LFE_EINVAL, "flag pointer NULL or misaligned");
+    cudaError_t e = launch_signal(reinterpret_cast<unsigned long long *>(d_flag), value, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "signal launch: %s", cudaGetErrorString(e));
+    return LFE_OK;
+}
+
+lfe_status lfe_ipc_export(const void *d_ptr, unsigned char handle[64], int64_t *offset)
+{
+    if (!d_ptr || !handle || !offset) return fail(LFE_EINVAL, "NULL argument");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    typedef CUresult (*RangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static const RangeFn range = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<RangeFn>(p);
+        return (RangeFn) nullptr;
+    }();
+    if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+        return fail(LFE_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return LFE_OK;
+}
+
+lfe_status lfe_ipc_open(const unsigned char handle[64], int64_t offset, void **d_ptr)
+{
+    if (!handle || !d_ptr || offset < 0) return fail(LFE_EINVAL, "bad argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    *d_ptr = static_cast<char *>(base) + offset;
+    return LFE_OK;
+}
+
+lfe_status lfe_ipc_close(void *d_ptr, int64_t offset)
+{
+    if (!d_ptr || offset < 0) return fail(LFE_EINVAL, "bad argument");
+    cudaError_t e = cudaIpcCloseMemHandle(static_cast<char *>(d_ptr) - offset);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return LFE_OK;
 }
 
 lfe_status lfe_last_async_error(lfe_ctx *c, void *stream)

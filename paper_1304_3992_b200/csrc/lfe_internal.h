@@ -61,6 +61,19 @@ struct Geometry {
     int32_t bands = 1;
     int64_t in_band_stride = 0;
     int64_t out_band_stride = 0;
+    // Peer-halo strip (lfe_extract_rows_peer; fused kernel only): virtual rows
+    // [0, ha_peer) are `above` (pitch above_pitch), [Hv - hb_peer, Hv) are `below`,
+    // and `in` points at virtual row ha_peer (the strip's own row 0).  The kernel
+    // waits for *wait_flag[j] >= wait_value before reading a peer row (NULL: no wait).
+    const void *above = nullptr;
+    int64_t above_pitch = 0;
+    int32_t ha_peer = 0;
+    const void *below = nullptr;
+    int64_t below_pitch = 0;
+    int32_t hb_peer = 0;
+    const unsigned long long *wait_flag[2] = {nullptr, nullptr};
+    unsigned long long wait_value = 0;
+    bool peer() const { return ha_peer > 0 || hb_peer > 0; }
 };
 
 struct LaunchCfg {
@@ -76,6 +89,8 @@ cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int t
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
                          int *err_flag, cudaStream_t s);
 bool fused_supports(const KParams &kp, int bit_depth);
+// lfe_signal: one thread stores `value` to *flag (st.release.sys)
+cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cudaStream_t s);
 // test entry: branch j's response for every pixel of a whole image (int32 or float bits)
 cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int branch, void *d_r, cudaStream_t s);
 // adds the exact global sums of output rows [o0, o1) to *d_stats (NEXT-2)

@@ -20,12 +20,12 @@ namespace {
 cudaError_t launch_test_variant(lfe_ctx *c, const Geometry &g, int tv, cudaStream_t s)
 {
     fz::FusedArgs fa;
-    CUtensorMap map;
+    fz::Maps map;
     cudaError_t e;
     if (!prepare_fused(c->kp, g, true, c->cfg.tile_h, fa, map, &e)) return e;
-    if (tv == fz::kTvInjectR) return launch_t<true, 0, true, true, false, fz::kTvInjectR>(fa, map, c->d_err, s);
-    if (c->kp.m2) return launch_t<true, 2, false, true, false, fz::kTvInjectE>(fa, map, c->d_err, s);
-    return launch_t<true, 1, false, true, false, fz::kTvInjectE>(fa, map, c->d_err, s);
+    if (tv == fz::kTvInjectR) return launch_t<true, 0, true, true, false, false, fz::kTvInjectR>(fa, map, c->d_err, s);
+    if (c->kp.m2) return launch_t<true, 2, false, true, false, false, fz::kTvInjectE>(fa, map, c->d_err, s);
+    return launch_t<true, 1, false, true, false, false, fz::kTvInjectE>(fa, map, c->d_err, s);
 }
 
 }  // namespace

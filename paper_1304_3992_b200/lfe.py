@@ -84,7 +84,8 @@ _lib = None
 EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows", "lfe_extract_host",
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
            "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
-           "lfe_set_stats", "lfe_get_thresholds", "lfe_extract_bands"]
+           "lfe_set_stats", "lfe_get_thresholds", "lfe_extract_bands", "lfe_extract_rows_peer", "lfe_signal",
+           "lfe_ipc_export", "lfe_ipc_open", "lfe_ipc_close"]
 # include/lfe_test.h, exported by the separate liblfe_test.so
 TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response", "lfe_test_extract_r", "lfe_test_extract_e"]
 _test_lib = None
@@ -136,6 +137,18 @@ def load():
     L.lfe_set_stats.restype = st
     L.lfe_get_thresholds.argtypes = [P, P, P, P]
     L.lfe_get_thresholds.restype = st
+    if hasattr(L, "lfe_extract_rows_peer"):  # (absent only in older builds loaded for A/B timing)
+        L.lfe_extract_rows_peer.argtypes = [P, P, I64, I32, I32, P, I64, P, I64, U32, P, P, ctypes.c_uint64, P,
+                                            I64, P]
+        L.lfe_extract_rows_peer.restype = st
+        L.lfe_signal.argtypes = [P, ctypes.c_uint64, P]
+        L.lfe_signal.restype = st
+        L.lfe_ipc_export.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(I64)]
+        L.lfe_ipc_export.restype = st
+        L.lfe_ipc_open.argtypes = [ctypes.c_char_p, I64, ctypes.POINTER(P)]
+        L.lfe_ipc_open.restype = st
+        L.lfe_ipc_close.argtypes = [P, I64]
+        L.lfe_ipc_close.restype = st
     _lib = L
     return L
 
@@ -193,6 +206,37 @@ def lfe_extract_rows(ctx, d_in_row0: int, in_pitch: int, width: int, rows: int, 
                      halo_below: int, edge_flags: int, d_out_row0: int, out_pitch: int, stream: int = 0):
     _check(load().lfe_extract_rows(ctx, d_in_row0, in_pitch, width, rows, halo_above, halo_below,
                                    edge_flags, d_out_row0, out_pitch, stream), "lfe_extract_rows")
+
+
+def lfe_extract_rows_peer(ctx, d_in_row0: int, in_pitch: int, width: int, rows: int, d_above: int, above_pitch: int,
+                          d_below: int, below_pitch: int, edge_flags: int, wait_above: int, wait_below: int,
+                          wait_value: int, d_out_row0: int, out_pitch: int, stream: int = 0):
+    _check(load().lfe_extract_rows_peer(ctx, d_in_row0, in_pitch, width, rows, d_above or None, above_pitch,
+                                        d_below or None, below_pitch, edge_flags, wait_above or None,
+                                        wait_below or None, wait_value, d_out_row0, out_pitch, stream),
+           "lfe_extract_rows_peer")
+
+
+def lfe_signal(d_flag: int, value: int, stream: int = 0):
+    _check(load().lfe_signal(d_flag, value, stream), "lfe_signal")
+
+
+def lfe_ipc_export(d_ptr: int):
+    """-> (64-byte handle, offset of d_ptr in its allocation)"""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _check(load().lfe_ipc_export(d_ptr, h, ctypes.byref(off)), "lfe_ipc_export")
+    return h.raw, off.value
+
+
+def lfe_ipc_open(handle: bytes, offset: int) -> int:
+    p = ctypes.c_void_p()
+    _check(load().lfe_ipc_open(handle, offset, ctypes.byref(p)), "lfe_ipc_open")
+    return p.value
+
+
+def lfe_ipc_close(d_ptr: int, offset: int):
+    _check(load().lfe_ipc_close(d_ptr, offset), "lfe_ipc_close")
 
 
 def lfe_extract_host(ctx, h_in: int, in_pitch: int, width: int, height: int, h_out: int, out_pitch: int):
@@ -398,6 +442,30 @@ class Context:
         e_in, e_out = t_in.element_size(), t_out.element_size()
         lfe_extract_bands(self.handle, t_in.data_ptr(), t_in.stride(1) * e_in, t_in.stride(0) * e_in, W, H, B,
                           t_out.data_ptr(), t_out.stride(1) * e_out, t_out.stride(0) * e_out, self._stream(stream))
+        return t_out
+
+    def extract_rows_peer(self, t_own, t_out, above=None, below=None, wait_above=None, wait_below=None,
+                          wait_value: int = 0, edge_flags: int | None = None, stream=None):
+        """lfe_extract_rows_peer on torch views: t_own = the strip's owned rows,
+        above / below = views whose first row is the first halo row above / below
+        the strip (None = that side is the image edge), wait_* = int64 flag
+        tensors (or raw pointers) the kernel waits on."""
+        self._check_dtype(t_own, t_out)
+        W = t_own.shape[1]
+        e_in, e_out = t_own.element_size(), t_out.element_size()
+
+        def ptr(t):
+            return 0 if t is None else (t if isinstance(t, int) else t.data_ptr())
+
+        def pitch(t):
+            return 0 if t is None or isinstance(t, int) else t.stride(0) * e_in
+
+        if edge_flags is None:
+            edge_flags = (LFE_TOP_IS_EDGE if above is None else 0) | (LFE_BOTTOM_IS_EDGE if below is None else 0)
+        lfe_extract_rows_peer(self.handle, t_own.data_ptr(), t_own.stride(0) * e_in, W, t_own.shape[0],
+                              ptr(above), pitch(above), ptr(below), pitch(below), edge_flags, ptr(wait_above),
+                              ptr(wait_below), wait_value, t_out.data_ptr(), t_out.stride(0) * e_out,
+                              self._stream(stream))
         return t_out
 
     def extract_rows(self, t_in_full, row0: int, rows: int, halo_above: int, halo_below: int,

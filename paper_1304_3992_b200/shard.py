@@ -316,3 +316,85 @@ class BandShard:
 
     def owned_pixels(self) -> int:
         return (len(self.whole) * self.H + sum(e - a for _, a, e, _, _ in self.parts)) * self.W
+
+
+class PeerStripShard:
+    """Row strips whose halo rows stay in the neighbours' HBM (north_star's
+    multi-GPU row strips on one NVLink/NVSwitch node, with no exchange step):
+    each rank holds ONLY its owned rows; at setup the ranks swap CUDA IPC
+    handles of those buffers (one all_gather_object) and map their neighbours'
+    (lfe_ipc_open enables peer access), and every step is ONE
+    lfe_extract_rows_peer launch that TMA-loads the halo rows from the
+    neighbours' memory.  Each rank also exposes a uint64 "input ready" flag
+    (lfe_signal) that its neighbours' kernels wait on before reading its rows.
+
+    Host logic only (gloo-testable: the plan and the peer geometry); the device
+    calls go through lfe.py."""
+
+    def __init__(self, H: int, W: int, rank: int, world: int, halo: int):
+        self.H, self.W, self.rank, self.world, self.halo = H, W, rank, world, halo
+        self.plan = plan_strips(H, world, halo)
+        self.a, self.b = self.plan[rank]
+        self.rows = self.b - self.a
+        self.ha = halo if rank > 0 else 0          # halo rows a neighbour supplies above / below
+        self.hb = halo if rank < world - 1 else 0
+        self.peer = {}  # rank -> (base pointer of its buffer, pitch, rows, flag pointer)
+        self._opened = []
+
+    def edge_flags(self) -> int:
+        from .lfe import LFE_BOTTOM_IS_EDGE, LFE_TOP_IS_EDGE
+        return (LFE_TOP_IS_EDGE if self.rank == 0 else 0) | (LFE_BOTTOM_IS_EDGE if self.rank == self.world - 1 else 0)
+
+    def alloc(self, dtype, device):
+        import torch
+        self.buf = torch.zeros((self.rows, self.W), dtype=dtype, device=device)
+        self.flag = torch.zeros(1, dtype=torch.int64, device=device)
+        return self.buf
+
+    def load_owned(self, full_image_rows):
+        import torch
+        src = full_image_rows[self.a:self.b]
+        if not isinstance(src, torch.Tensor):
+            src = torch.from_numpy(src)
+        self.buf.copy_(src)
+
+    def neighbours(self):
+        return [k for k in (self.rank - 1, self.rank + 1) if 0 <= k < self.world]
+
+    def connect(self, group=None):
+        """Swap IPC handles of every rank's buffer and flag; map the neighbours'."""
+        import torch.distributed as dist
+
+        from . import lfe
+        mine = (lfe.lfe_ipc_export(self.buf.data_ptr()), lfe.lfe_ipc_export(self.flag.data_ptr()),
+                self.buf.stride(0) * self.buf.element_size(), self.rows)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        for k in self.neighbours():
+            (hb, ob), (hf, of), pitch, rows = allh[k]
+            pb = lfe.lfe_ipc_open(hb, ob)
+            self._opened.append((pb, ob))
+            pf = lfe.lfe_ipc_open(hf, of)
+            self._opened.append((pf, of))
+            self.peer[k] = (pb, pitch, rows, pf)
+
+    def call_args(self):
+        """(d_above, above_pitch, d_below, below_pitch, wait_above, wait_below) for
+        lfe_extract_rows_peer: the neighbour above's last `halo` rows, the
+        neighbour below's first rows, and their flags."""
+        h = self.halo
+        da = pa = db = pb = fa = fb = 0
+        if self.rank > 0:
+            base, pitch, rows, flag = self.peer[self.rank - 1]
+            da, pa, fa = base + (rows - h) * pitch, pitch, flag
+        if self.rank < self.world - 1:
+            base, pitch, rows, flag = self.peer[self.rank + 1]
+            db, pb, fb = base, pitch, flag
+        return da, pa, db, pb, fa, fb
+
+    def close(self):
+        from . import lfe
+        for p, off in self._opened:
+            lfe.lfe_ipc_close(p, off)
+        self._opened = []
+        self.peer = {}

@@ -842,16 +842,21 @@ def test_fused_range_check_and_rows_past_the_call(where):
         assert_same(out.cpu().numpy(), O.run(img, _oparams(p)), "rows past the call")
 
 
-@pytest.mark.parametrize("world,config,extra", [(2, "c3", ["--verify"]), (3, "c3", ["--adaptive", "0.75", "--verify"]),
-                                                (2, "c4", []), (8, "c4", [])])
+@pytest.mark.parametrize("world,config,extra", [(2, "c3", ["--verify", "--halo", "nccl"]),
+                                                (3, "c3", ["--adaptive", "0.75", "--verify"]),
+                                                (2, "c4", []), (8, "c4", []),
+                                                (2, "c3", ["--verify", "--halo", "peer"]),
+                                                (4, "c3", ["--halo", "peer"])])
 def test_bench_ranks_on_one_gpu(world, config, extra):
     """bench.py's N > 1 step run as `world` ranks sharing this GPU over gloo
-    (LFE_BENCH_SHARE_GPUS; NCCL refuses duplicate GPUs): c3 row strips (halo
-    exchange, interior band overlapped with it, boundary bands, max-over-ranks
-    timing) with --verify (every rank's owned rows equal a whole-scene
-    extraction), and c4 bands dealt to 2 ranks (whole bands, no exchange) and 8
-    ranks (every band cut between two ranks).  Every rank also checks its rows
-    against the CPU oracle: the line's parity must be bit-exact."""
+    (LFE_BENCH_SHARE_GPUS; NCCL refuses duplicate GPUs): c3 row strips with the
+    exchange schedule (halo exchange, interior band overlapped with it,
+    boundary bands, max-over-ranks timing) and with peer halos (CUDA IPC
+    between the rank processes, one lfe_extract_rows_peer launch per step),
+    --verify (every rank's owned rows equal a whole-scene extraction), and c4
+    bands dealt to 2 ranks (whole bands, no exchange) and 8 ranks (every band
+    cut between two ranks).  Every rank also checks its rows against the CPU
+    oracle: the line's parity must be bit-exact."""
     import json
     import os
     import subprocess
@@ -860,7 +865,8 @@ def test_bench_ranks_on_one_gpu(world, config, extra):
     env = dict(os.environ, LFE_BENCH_SHARE_GPUS="1")
     size = "2048" if config == "c3" else "1024"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
-           "--master-addr", "127.0.0.1", "--master-port", str(29517 + world), os.path.join(root, "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", str(29517 + world + 10 * len(extra)),
+           os.path.join(root, "bench.py"),
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--config", config, "--size", size] + extra
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -1018,3 +1024,91 @@ def test_fused_second_level_all_binary_groups():
         dy, dx = divmod(b, 3)
         E[dy::3, dx::3] = np.where((codes.reshape(96, 700) >> b) & 1, 0xFFF0, 5).astype(np.uint16)
     assert_same(_extract_e(E, 3), _hm_oracle(E, 3), "second level")
+
+
+# --------------------------- peer-halo strips (lfe_extract_rows_peer, multi-GPU) ----
+def _peer_strips(img, p, cuts, flags=False):
+    """Every strip [cuts[k], cuts[k+1]) in its OWN allocation; its halo rows read in
+    place from the neighbouring strips' allocations (what a rank reads from its
+    neighbours' HBM over NVLink).  Returns the stitched output."""
+    H, W = img.shape
+    tin = torch.uint8 if p.bit_depth <= 8 else torch.uint16
+    tout = torch.uint8 if p.out_mode == lfe.LFE_OUT_MASK else tin
+    with lfe.Context(p) as ctx:
+        h = ctx.halo
+        bufs, outs = [], []
+        for a, b in zip(cuts, cuts[1:]):
+            d = _pitched((b - a, W), tin)
+            d.copy_(torch.from_numpy(np.ascontiguousarray(img[a:b])))
+            bufs.append(d)
+            outs.append(_pitched((b - a, W), tout))
+        fl = torch.zeros((len(bufs),), dtype=torch.int64, device="cuda") if flags else None
+        if flags:  # each strip's owner signals "input ready" (a real run: from its own stream)
+            for k in range(len(bufs)):
+                lfe.lfe_signal(fl[k:k + 1].data_ptr(), 3, torch.cuda.current_stream().cuda_stream)
+        for k in range(len(bufs)):
+            above = bufs[k - 1][bufs[k - 1].shape[0] - h:] if k > 0 else None
+            below = bufs[k + 1] if k + 1 < len(bufs) else None
+            wa = fl[k - 1:k].data_ptr() if flags and k > 0 else None
+            wb = fl[k + 1:k + 2].data_ptr() if flags and below is not None else None
+            ctx.extract_rows_peer(bufs[k], outs[k], above, below, wait_above=wa, wait_below=wb,
+                                  wait_value=3 if flags else 0)
+        ctx.check()
+        return np.concatenate([o.cpu().numpy() for o in outs])
+
+
+@pytest.mark.parametrize("bd,hm,m2,mode", [(10, True, 0, lfe.LFE_OUT_EXTRACT), (8, True, 0, lfe.LFE_OUT_MASK),
+                                           (12, False, 0, lfe.LFE_OUT_EXTRACT), (10, True, 3, lfe.LFE_OUT_EXTRACT)])
+def test_peer_strips_equal_oracle(bd, hm, m2, mode):
+    """Strips of several sizes (exactly the halo, shorter than one 8-row TMA stage,
+    ragged, long) in separate allocations, halos read in place from the
+    neighbours' allocations: the stitched result equals the oracle's
+    whole-image result bit for bit."""
+    rng = np.random.default_rng(900 + bd + 7 * m2)
+    p = lfe.Params(bit_depth=bd, zc_threshold=(0.01, 0.01), hybrid_median=hm, median_window2=m2, out_mode=mode)
+    with lfe.Context(p) as ctx:
+        h = ctx.halo
+    for H, W in [(203, 150), (160, 1400), (300, 2701)]:
+        img = scenes.random_image(rng, H, W, bd, "mixed")
+        cuts = sorted({0, h, h + 9, 60, 61 + h, H - h - 3, H - h, H})
+        cuts = [c for c in cuts if 0 <= c <= H]
+        cuts = [c for i, c in enumerate(cuts) if i == 0 or c - cuts[i - 1] >= h or c == H]
+        if cuts[-1] - cuts[-2] < h:
+            cuts.pop(-2)
+        assert_same(_peer_strips(img, p, cuts), O.run(img, _oparams(p)), f"{H}x{W} cuts {cuts}")
+
+
+def test_peer_strips_c3_eight_ranks_with_flags():
+    """The c3 scene cut like an 8-GPU run (1500-row strips), every strip in its own
+    allocation, halos read in place, each neighbour's 'input ready' flag already
+    signalled: bit-exact against the whole-scene oracle."""
+    img = scenes.scene_c3()
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    cuts = [1500 * k for k in range(9)]
+    got = _peer_strips(img, p, cuts, flags=True)
+    assert_same(got, O.run(img, _oparams(p)), "c3 peer strips x8")
+
+
+def test_peer_strip_validation():
+    p = lfe.Params(bit_depth=10)
+    with lfe.Context(p) as ctx:
+        d = _pitched((64, 100), torch.uint16)
+        o = _pitched((64, 100), torch.uint16)
+        with pytest.raises(lfe.LfeError):  # inner top side without rows above
+            lfe.lfe_extract_rows_peer(ctx.handle, d.data_ptr(), d.stride(0) * 2, 100, 64, 0, 0, 0, 0,
+                                      lfe.LFE_BOTTOM_IS_EDGE, 0, 0, 0, o.data_ptr(), o.stride(0) * 2, 0)
+    p2 = lfe.Params(bit_depth=10, log_size=(7, 7))
+    with lfe.Context(p2) as ctx:  # general-kernel parameters: no peer path
+        with pytest.raises(lfe.LfeError):
+            ctx.extract_rows_peer(d[8:], o[8:], above=d[:8])
+
+
+def test_signal_and_ipc_roundtrip_in_process():
+    """lfe_signal stores the value (release, system scope); lfe_ipc_export names the
+    allocation and offset of a pointer inside a torch tensor."""
+    f = torch.zeros(4, dtype=torch.int64, device="cuda")
+    lfe.lfe_signal(f[2:3].data_ptr(), 12345, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert f.cpu().tolist() == [0, 0, 12345, 0]
+    h, off = lfe.lfe_ipc_export(f[2:3].data_ptr())
+    assert len(h) == 64 and off >= 16

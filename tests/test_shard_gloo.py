@@ -259,3 +259,29 @@ def test_gloo_band_shards_reproduce_every_band(world, staged):
     assert (cover == 1).all()
     for b in range(bands):
         np.testing.assert_array_equal(full[b], O.run(scene[b], p))
+
+
+def test_peer_strip_geometry():
+    """PeerStripShard.call_args: the neighbour above's LAST halo rows (its base +
+    (rows - halo) * pitch), the neighbour below's first row, and their flags;
+    nothing on an image edge."""
+    from paper_1304_3992_b200.shard import PeerStripShard
+    H, W, halo = 12000, 12000, 7
+    for world in (1, 2, 8):
+        plan = plan_strips(H, world, halo)
+        for r in range(world):
+            sh = PeerStripShard(H, W, r, world, halo)
+            assert (sh.a, sh.b) == plan[r]
+            for k in sh.neighbours():
+                a, b = plan[k]
+                sh.peer[k] = (1000000 * (k + 1), 24064, b - a, 7 + k)
+            da, pa, db, pb, fa, fb = sh.call_args()
+            if r == 0:
+                assert da == pa == fa == 0 and sh.ha == 0
+            else:
+                rows_above = plan[r - 1][1] - plan[r - 1][0]
+                assert da == 1000000 * r + (rows_above - halo) * 24064 and pa == 24064 and fa == 7 + r - 1
+            if r == world - 1:
+                assert db == pb == fb == 0 and sh.hb == 0
+            else:
+                assert db == 1000000 * (r + 2) and fb == 7 + r + 1

@@ -162,16 +162,21 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_
                             uint32_t edge_flags, void *d_out_row0, int64_t out_pitch_bytes,
                             void *cuda_stream);
 
+/* Rows lfe_extract_rows_peer reads from each neighbour (>= every fused-kernel
+ * halo; one 8-row TMA stage). */
+#define LFE_PEER_ROWS 8
+
 /* One row strip whose halo rows stay in the NEIGHBOURS' memory (multi-GPU
  * row strips on one NVLink/NVSwitch node, north_star; the paper's "data
  * transfer ... to be minimized"): the fused kernel TMA-loads
  * the rows above/below the strip straight from d_above / d_below (a peer
  * GPU's HBM mapped with lfe_ipc_open, or any device pointer this device can
  * read), so no exchange step runs.  d_in_row0: the strip's first owned row
- * (`rows` rows, in_pitch_bytes).  d_above: the first of the lfe_halo(c) rows
+ * (`rows` rows, in_pitch_bytes).  d_above: the first of the LFE_PEER_ROWS rows
  * immediately above the strip (pitch above_pitch_bytes); NULL and ignored
  * when edge_flags has LFE_TOP_IS_EDGE (the strip's row 0 is the image top).
- * d_below: the first row below the strip, likewise with LFE_BOTTOM_IS_EDGE.
+ * d_below: the first of the LFE_PEER_ROWS rows below the strip, likewise
+ * with LFE_BOTTOM_IS_EDGE.  (The neighbours' strips hold >= LFE_PEER_ROWS rows.)
  * wait_above / wait_below (device or mapped peer pointers to uint64, may be
  * NULL): before reading a row of that neighbour the kernel waits until the
  * flag is >= wait_value (acquire, system scope) -- the neighbour's "input

@@ -70,8 +70,8 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool pair
         const int ye_all = ys + n;
         while (ys < ye_all) {  // the kernel's split at kEdge rows from the virtual top/bottom
             int ye = ye_all;
-            if (ys < kEdge && ye > kEdge) ye = kEdge;
-            if (ys < fa.H - kEdge && ye > fa.H - kEdge) ye = fa.H - kEdge;
+            if (fa.o0 < halo && ys < kEdge && ye > kEdge) ye = kEdge;
+            if (fa.o1 + halo > fa.H && ys < fa.H - kEdge && ye > fa.H - kEdge) ye = fa.H - kEdge;
             const bool edge = ys - halo < 0 || ye + halo > fa.H;
             const int rows = paired ? (ye - ys + 1) / 2 : ye - ys;
             c += f * (rows + kPiece + (edge ? kEdgePiece : 0.0));
@@ -252,7 +252,10 @@ bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, 
     fa.seg_pitch[1] = g.in_pitch;
     fa.seg_pitch[2] = g.below_pitch;
     const int own_rows = g.Hv - g.ha_peer - g.hb_peer;
-    const bool ok = encode_map(&maps.own, in16, g.in, g.width, own_rows, g.bands, g.in_pitch, g.in_band_stride, kR);
+    bool ok = encode_map(&maps.own, in16, g.in, g.width, own_rows, g.bands, g.in_pitch, g.in_band_stride, kR);
+    maps.above = maps.below = maps.own;
+    if (ok && g.ha_peer > 0) ok = encode_map(&maps.above, in16, g.above, g.width, g.ha_peer, 1, g.above_pitch, 0, kR);
+    if (ok && g.hb_peer > 0) ok = encode_map(&maps.below, in16, g.below, g.width, g.hb_peer, 1, g.below_pitch, 0, kR);
     if (!ok) {
         *err = cudaErrorInvalidValue;
         return false;
@@ -267,8 +270,21 @@ __global__ void signal_kernel(unsigned long long *flag, unsigned long long value
 }
 }  // namespace
 
+// A stream memory operation (no SM work, no kernel launch gap) when the driver
+// offers it: cuStreamWriteValue64 with its default flag orders the write after
+// the stream's earlier work and its memory (a release); else a one-thread kernel.
 cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cudaStream_t s)
 {
+    typedef CUresult (*WriteFn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+    static const WriteFn wv = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<WriteFn>(p);
+        return (WriteFn) nullptr;
+    }();
+    if (wv && wv(s, reinterpret_cast<CUdeviceptr>(flag), value, 0) == CUDA_SUCCESS) return cudaSuccess;
     signal_kernel<<<1, 1, 0, s>>>(flag, value);
     return cudaGetLastError();
 }

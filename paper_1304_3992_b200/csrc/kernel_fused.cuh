@@ -116,11 +116,13 @@ struct FusedArgs {
     unsigned long long wait_value;
 };
 
-// The launch's input tensor map(s): `own`, 8-row boxes over the whole virtual image
-// (or over the own rows of a peer-halo strip).
+// The launch's input tensor maps, 8-row boxes: `own` over the whole virtual image
+// (or over the own rows of a peer-halo strip); `above` / `below` over the
+// kPeerRows rows of the neighbours of a peer-halo strip (copies of `own` otherwise).
 struct alignas(64) Maps {
-    CUtensorMap own;
+    CUtensorMap own, above, below;
 };
+
 
 // rows of input needed beyond the output rows: LoG 2 + ZC 1 + std 2 (+ HM 2) (+ second level 1)
 __host__ __device__ constexpr int halo_of(int hml) { return hml == 2 ? 8 : hml == 1 ? 7 : 5; }
@@ -407,7 +409,7 @@ struct Pieces {
         u = U * blockIdx.x / gridDim.x;
         u1 = U * (blockIdx.x + 1) / gridDim.x;
     }
-    template <int kHalo>
+    template <int kHalo, bool PEER = false>
     __device__ __forceinline__ bool next(const FusedArgs &a, Item &it)
     {
         const int R = a.o1 - a.o0;
@@ -416,10 +418,12 @@ struct Pieces {
             const int r0 = (int)(u - (u / R) * R);
             int n = (int)min((long long)(R - r0), u1 - u);
             // keep the rows within kEdge of the virtual top/bottom in segments of their
-            // own, so that only those short pieces take the row-clamping path
+            // own, so that only those short pieces take the row-clamping path (only
+            // where it can be needed: a strip with a full halo of real rows above /
+            // below never clamps there)
             const int ys = a.o0 + r0;
-            if (ys < kEdge && ys + n > kEdge) n = kEdge - ys;
-            if (ys < a.H - kEdge && ys + n > a.H - kEdge) n = a.H - kEdge - ys;
+            if (a.o0 < kHalo && ys < kEdge && ys + n > kEdge) n = kEdge - ys;
+            if (a.o1 + kHalo > a.H && ys < a.H - kEdge && ys + n > a.H - kEdge) n = a.H - kEdge - ys;
             if (half < 0) {
                 pu = u;
                 pu1 = u + n;
@@ -441,6 +445,17 @@ struct Pieces {
         it.band = band;
         it.plo = max(0, it.ys - kHalo);
         it.phi = min(a.H, it.ye + kHalo);
+        if constexpr (PEER) {
+            // peer-halo strip: align the stage grid to the one peer-segment boundary
+            // the item's rows cross (walking at most kR - 1 extra rows), so that the
+            // neighbour's kPeerRows rows are exactly one stage, one box from its map
+            const bool ta = it.plo < a.seg_a, tb = it.phi > a.seg_b;
+            if (ta != tb) {
+                const int sb = ta ? a.seg_a : a.seg_b;
+                const int p = sb - kR * ((sb - it.plo + kR - 1) / kR);
+                if (p >= 0) it.plo = p;
+            }
+        }
         it.nst = (it.phi - it.plo + kR - 1) / kR;
         return true;
     }
@@ -479,12 +494,8 @@ struct Producer {
         }
     }
 
-    // a stage touching the neighbours' rows (peer-halo strips): row by row from the
-    // segment holding it (rows past the image end are never read: any valid row), each
-    // box row by one 1-D bulk copy of its in-image part (16-byte granules; the columns
-    // outside [0, W) are never read as image values).  Returns the bytes it requested.
-    // Out of line: only the first/last stages of a strip's edge pieces take it.
-    __device__ __forceinline__ uint32_t load_peer_rows(unsigned char *dst, int y, uint64_t *bar)
+    // before the first read of a neighbour's rows: its "input ready" flag
+    __device__ __forceinline__ void wait_peers()
     {
         if (!peers_ready) {
             for (int j = 0; j < 2; ++j)
@@ -492,6 +503,17 @@ struct Producer {
                     while (ld_acquire_sys(a->wait_flag[j]) < a->wait_value) __nanosleep(64);
             peers_ready = true;
         }
+    }
+
+    // a stage straddling a peer segment boundary (an item crossing both, or a stage
+    // grid that could not be aligned): row by row from the
+    // segment holding it (rows past the image end are never read: any valid row), each
+    // box row by one 1-D bulk copy of its in-image part (16-byte granules; the columns
+    // outside [0, W) are never read as image values).  Returns the bytes it requested.
+    // Out of line: only the first/last stages of a strip's edge pieces take it.
+    __device__ __forceinline__ uint32_t load_peer_rows(unsigned char *dst, int y, uint64_t *bar)
+    {
+        wait_peers();
         constexpr int kE = IN16 ? 2 : 1;                      // bytes per pixel
         const int wr = ((a->W * kE + 15) & ~15) / kE;          // row length rounded to 16 bytes
         const int x0 = it.xo - (IN16 ? kHaloX : 2 * kHaloX);  // first column of box 0
@@ -524,7 +546,7 @@ struct Producer {
     {
         while (!done && g < released + kS) {
             if (!have) {
-                if (!pcs.template next<kHalo>(*a, it)) {
+                if (!pcs.template next<kHalo, PEER>(*a, it)) {
                     done = true;
                     return;
                 }
@@ -536,9 +558,14 @@ struct Producer {
             if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
             unsigned char *dst = ring + slot * kStageBytes;
             const int y = it.plo + k * kR;
-            if (!PEER || (y >= a->seg_a && y + kR <= a->seg_b)) {
+            if (!PEER || (y >= a->seg_a && (y + kR <= a->seg_b || a->seg_b == a->H))) {
                 mbar_expect_tx(&full[slot], kStageBytes);
                 load(dst, &maps->own, PEER ? y - a->seg_a : y, &full[slot]);
+            } else if (y + kR <= a->seg_a || y >= a->seg_b) {
+                // exactly the neighbour's kPeerRows rows (an aligned stage grid)
+                wait_peers();
+                mbar_expect_tx(&full[slot], kStageBytes);
+                load(dst, y < a->seg_a ? &maps->above : &maps->below, y < a->seg_a ? y : y - a->seg_b, &full[slot]);
             } else {
                 // the bytes are known only after the copies are issued: count them, then
                 // arrive with that transaction count (the phase cannot complete before
@@ -1151,8 +1178,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 4; ++i) rX[j][i] = rY[j][i] = 0.0f;
 
         const int rho_end = it.ye + kLag;
-        optr = obase - (long long)(kHalo + kLag) * a.out_pitch;  // output row of step rho = rho - kLag
-        for (int rho = it.ys - kHalo; rho < rho_end; rho += kR) {
+        // interior walks start at the first staged row (= ys - kHalo, or up to kR - 1
+        // rows earlier on a peer-aligned stage grid); output row of step rho = rho - kLag
+        const int rho0 = YF ? it.ys - kHalo : it.plo;
+        optr = obase + (long long)(rho0 - kLag - it.ys) * a.out_pitch;
+        for (int rho = rho0; rho < rho_end; rho += kR) {
             // wait for the ring stages holding this chunk's input rows
             const int st = (prow(rho + kR - 1) - it.plo) >> 3;
             while (waited < st) {
@@ -1193,7 +1223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     // ---- item loop -------------------------------------------------------------
-    while (pcs.next<kHalo>(a, it)) {
+    while (pcs.template next<kHalo, PEER>(a, it)) {
         mbar_wait(&full[g_base % kS], (g_base / kS) & 1);  // first stage of this piece
         ++c_idx;
         waited = 0;

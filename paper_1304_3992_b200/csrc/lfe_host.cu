@@ -645,8 +645,10 @@ lfe_status lfe_extract_rows_peer(lfe_ctx *c, const void *d_in_row0, int64_t in_p
     g.out = d_out_row0;
     g.out_pitch = out_pitch;
     g.width = W;
-    g.ha_peer = top ? 0 : h;
-    g.hb_peer = bot ? 0 : h;
+    static_assert(LFE_PEER_ROWS == kPeerRows, "lfe.h and the kernel agree on the peer rows");
+    if (h > LFE_PEER_ROWS) return fail(LFE_EUNSUPPORTED, "halo %d > LFE_PEER_ROWS", h);
+    g.ha_peer = top ? 0 : LFE_PEER_ROWS;
+    g.hb_peer = bot ? 0 : LFE_PEER_ROWS;
     g.Hv = rows + g.ha_peer + g.hb_peer;
     g.o0 = g.ha_peer;
     g.o1 = g.ha_peer + rows;

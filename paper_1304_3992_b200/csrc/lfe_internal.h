@@ -13,6 +13,7 @@ constexpr int kMaxMask = 9;                 // largest compiled LoG side (NEXT-4
 constexpr int kMaxMaskCoeffs = kMaxMask * kMaxMask;
 constexpr int kMaxStdWindow = 7;
 constexpr int kMaxMedianWindow = 7;
+constexpr int kPeerRows = 8;                // rows a peer-halo strip reads from each neighbour (LFE_PEER_ROWS)
 
 // Everything a kernel needs, passed by value as a __grid_constant__ parameter.
 struct KParams {

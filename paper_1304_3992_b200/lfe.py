@@ -25,6 +25,7 @@ LFE_STD_ZC, LFE_STD_INTENSITY, LFE_STD_RESPONSE, LFE_STD_RESPONSE_AT_ZC = 0, 1, 
 LFE_MASK_INT, LFE_MASK_F32 = 0, 1
 LFE_OUT_EXTRACT, LFE_OUT_MASK = 0, 1
 LFE_TOP_IS_EDGE, LFE_BOTTOM_IS_EDGE = 1, 2
+LFE_PEER_ROWS = 8  # rows lfe_extract_rows_peer reads from each neighbour
 LFE_OPT_KERNEL, LFE_OPT_TILE_W, LFE_OPT_TILE_H, LFE_OPT_HOST_STRIP_ROWS = 1, 2, 3, 4
 LFE_KERNEL_AUTO, LFE_KERNEL_STAGED, LFE_KERNEL_FUSED = 0, 1, 2
 LFE_ADAPT_ZC, LFE_ADAPT_STD = 1, 2

@@ -332,8 +332,10 @@ class PeerStripShard:
     calls go through lfe.py."""
 
     def __init__(self, H: int, W: int, rank: int, world: int, halo: int):
+        from .lfe import LFE_PEER_ROWS
         self.H, self.W, self.rank, self.world, self.halo = H, W, rank, world, halo
-        self.plan = plan_strips(H, world, halo)
+        self.peer_rows = max(halo, LFE_PEER_ROWS)  # rows read from each neighbour (lfe.h)
+        self.plan = plan_strips(H, world, self.peer_rows)
         self.a, self.b = self.plan[rank]
         self.rows = self.b - self.a
         self.ha = halo if rank > 0 else 0          # halo rows a neighbour supplies above / below
@@ -380,9 +382,9 @@ class PeerStripShard:
 
     def call_args(self):
         """(d_above, above_pitch, d_below, below_pitch, wait_above, wait_below) for
-        lfe_extract_rows_peer: the neighbour above's last `halo` rows, the
+        lfe_extract_rows_peer: the neighbour above's last LFE_PEER_ROWS rows, the
         neighbour below's first rows, and their flags."""
-        h = self.halo
+        h = self.peer_rows
         da = pa = db = pb = fa = fb = 0
         if self.rank > 0:
             base, pitch, rows, flag = self.peer[self.rank - 1]

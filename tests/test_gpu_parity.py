@@ -1047,7 +1047,7 @@ def _peer_strips(img, p, cuts, flags=False):
             for k in range(len(bufs)):
                 lfe.lfe_signal(fl[k:k + 1].data_ptr(), 3, torch.cuda.current_stream().cuda_stream)
         for k in range(len(bufs)):
-            above = bufs[k - 1][bufs[k - 1].shape[0] - h:] if k > 0 else None
+            above = bufs[k - 1][bufs[k - 1].shape[0] - lfe.LFE_PEER_ROWS:] if k > 0 else None
             below = bufs[k + 1] if k + 1 < len(bufs) else None
             wa = fl[k - 1:k].data_ptr() if flags and k > 0 else None
             wb = fl[k + 1:k + 2].data_ptr() if flags and below is not None else None
@@ -1066,11 +1066,11 @@ def test_peer_strips_equal_oracle(bd, hm, m2, mode):
     whole-image result bit for bit."""
     rng = np.random.default_rng(900 + bd + 7 * m2)
     p = lfe.Params(bit_depth=bd, zc_threshold=(0.01, 0.01), hybrid_median=hm, median_window2=m2, out_mode=mode)
-    with lfe.Context(p) as ctx:
-        h = ctx.halo
+    h = lfe.LFE_PEER_ROWS  # every strip holds >= the rows its neighbours read from it
     for H, W in [(203, 150), (160, 1400), (300, 2701)]:
         img = scenes.random_image(rng, H, W, bd, "mixed")
-        cuts = sorted({0, h, h + 9, 60, 61 + h, H - h - 3, H - h, H})
+        # strips of exactly 8 rows, 17 (crossing both neighbours' rows in one item), ragged, long
+        cuts = sorted({0, h, 2 * h + 9, 60, 61 + h, 100, 117, H - h - 3, H - h, H})
         cuts = [c for c in cuts if 0 <= c <= H]
         cuts = [c for i, c in enumerate(cuts) if i == 0 or c - cuts[i - 1] >= h or c == H]
         if cuts[-1] - cuts[-2] < h:

@@ -262,8 +262,8 @@ def test_gloo_band_shards_reproduce_every_band(world, staged):
 
 
 def test_peer_strip_geometry():
-    """PeerStripShard.call_args: the neighbour above's LAST halo rows (its base +
-    (rows - halo) * pitch), the neighbour below's first row, and their flags;
+    """PeerStripShard.call_args: the neighbour above's LAST LFE_PEER_ROWS = 8 rows
+    (its base + (rows - 8) * pitch), the neighbour below's first row, and their flags;
     nothing on an image edge."""
     from paper_1304_3992_b200.shard import PeerStripShard
     H, W, halo = 12000, 12000, 7
@@ -280,7 +280,7 @@ def test_peer_strip_geometry():
                 assert da == pa == fa == 0 and sh.ha == 0
             else:
                 rows_above = plan[r - 1][1] - plan[r - 1][0]
-                assert da == 1000000 * r + (rows_above - halo) * 24064 and pa == 24064 and fa == 7 + r - 1
+                assert da == 1000000 * r + (rows_above - 8) * 24064 and pa == 24064 and fa == 7 + r - 1
             if r == world - 1:
                 assert db == pb == fb == 0 and sh.hb == 0
             else:

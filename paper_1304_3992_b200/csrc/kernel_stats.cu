@@ -15,6 +15,7 @@
 // so the result is independent of the order (deterministic).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lfe_internal.h"
 
@@ -158,6 +159,174 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// ---- 5x5 masks (the paper's, R = 2): orbit sums shared by both branches -------------
+// A 66 x 256 tile per step of a persistent CTA of 128 threads, 2 adjacent columns
+// per thread.  Staging: interior tiles with 16-byte vector copies (cp.async for
+// uint16, widened loads for uint8) of the rows y0-2 .. y0+67 and columns x0-8 ..
+// x0+263; tiles touching an image border element by element with clamped
+// (edge-replicated, R5) coordinates.  Per input row a thread reads its 6 values
+// with three 4-byte loads, keeps I, h1 = I(x-1) + I(x+1), h2 = I(x-2) + I(x+2) of
+// the last 5 rows in registers (the row loop is unrolled by 5: no moves), forms the
+// six orbit sums of the centre row once -- S00 = I, S10 = h1 + I(y-1) + I(y+1),
+// S20 = h2 + I(y-2) + I(y+2), S11 = h1(y-1) + h1(y+1), S21 = h2(y-1) + h2(y+1) +
+// h1(y-2) + h1(y+2), S22 = h2(y-2) + h2(y+2) -- and both responses from them,
+// r_j = sum_k c_jk S_k (6 IMAD each; every value an exact int32, R3).
+constexpr int k5Rows = 66;                 // output rows per tile (+4 staged: 70 = 14 x 5)
+constexpr int k5Cols = 256;                // output columns per tile (2 per thread)
+constexpr int k5SRows = k5Rows + 4;
+constexpr int k5Stride = k5Cols + 16;      // staged columns x0-8 .. x0+263 (16-byte rows)
+
+// Tiles are handed out dynamically: counter[0] is the next tile, counter[1] counts
+// finished CTAs; the last CTA resets both to 0 for the next launch (launches that
+// share a counter are stream-ordered: one ctx, one stream at a time).
+template <typename Tin>
+__global__ void __launch_bounds__(kThreads)
+    stats5_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, lfe_stats *out,
+                  unsigned int *counter)
+{
+    __shared__ __align__(16) uint16_t sI[k5SRows * k5Stride];
+    __shared__ unsigned long long red[kThreads / 32][9];
+    __shared__ long long s_tile;
+    const int W = g.width, Hv = g.Hv;
+    const int tiles_x = (W + k5Cols - 1) / k5Cols;
+    const int rows = g.o1 - g.o0;
+    const long long ntiles = (long long)tiles_x * ((rows + k5Rows - 1) / k5Rows);
+    int32_t c[2][6];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) c[j][k] = kp.orb[j][k];
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(g.in) | (uintptr_t)g.in_pitch) & 15u) == 0;
+
+    long long n = 0, rs0 = 0, rs1 = 0, is = 0;
+    unsigned long long hi0 = 0, lo0 = 0, hi1 = 0, lo1 = 0, iq = 0;
+    const int t = threadIdx.x;
+    for (;;) {
+        __syncthreads();  // the previous tile's readers are done (and s_tile is free)
+        if (t == 0) s_tile = counter ? (long long)atomicAdd(counter, 1u) : -1;
+        __syncthreads();
+        const long long tile = s_tile;
+        if (tile >= ntiles) break;
+        const int tx = (int)(tile % tiles_x), ty = (int)(tile / tiles_x);
+        const int x0 = tx * k5Cols, y0 = g.o0 + ty * k5Rows;
+        if (vec_ok && x0 - 8 >= 0 && x0 + k5Cols + 8 <= W && y0 - 2 >= 0 && y0 + k5Rows + 2 <= Hv) {
+            // interior: 16-byte chunks (8 pixels) of whole staged rows
+            constexpr int kChunks = k5Stride / 8;  // 34 per row
+            for (int q = t; q < k5SRows * kChunks; q += kThreads) {
+                const int r = q / kChunks, ck = q - r * kChunks;
+                const char *src = reinterpret_cast<const char *>(g.in) + (int64_t)(y0 - 2 + r) * g.in_pitch +
+                                  (int64_t)(x0 - 8 + 8 * ck) * sizeof(Tin);
+                uint16_t *dst = sI + r * k5Stride + 8 * ck;
+                if constexpr (sizeof(Tin) == 2) {
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                                 "l"(src)
+                                 : "memory");
+                } else {
+                    const uint2 v = *reinterpret_cast<const uint2 *>(src);  // 8 x u8 -> 8 x u16
+                    uint4 w;
+                    w.x = __byte_perm(v.x, 0, 0x4140);
+                    w.y = __byte_perm(v.x, 0, 0x4342);
+                    w.z = __byte_perm(v.y, 0, 0x4140);
+                    w.w = __byte_perm(v.y, 0, 0x4342);
+                    *reinterpret_cast<uint4 *>(dst) = w;
+                }
+            }
+            if constexpr (sizeof(Tin) == 2) asm volatile("cp.async.wait_all;" ::: "memory");
+        } else {
+            for (int q = t; q < k5SRows * k5Stride; q += kThreads) {
+                const int r = q / k5Stride, cc = q - r * k5Stride;
+                const int vy = clampi(y0 - 2 + r, 0, Hv - 1), vx = clampi(x0 - 8 + cc, 0, W - 1);
+                const Tin *row = reinterpret_cast<const Tin *>(reinterpret_cast<const char *>(g.in) + (int64_t)vy * g.in_pitch);
+                sI[q] = (uint16_t)row[vx];
+            }
+        }
+        __syncthreads();
+        const int xa = x0 + 2 * t;  // this thread's columns xa, xa + 1
+        const bool ok0 = xa < W, ok1 = xa + 1 < W;
+        // per tile column pair: |sum r| < 66 * 2^23 < 2^30, sum r^2 < 66 * 2^46 < 2^53
+        int32_t t0 = 0, t1 = 0;
+        unsigned long long u0 = 0, u1 = 0, uq = 0;
+        uint32_t ti = 0;
+        int tn = 0;
+        // history of the last 5 rows (slot = row index mod 5), per column p = 0, 1
+        int32_t hI[5][2], h1[5][2], h2[5][2];
+        const uint16_t *base = sI + 2 * t + 6;  // column xa - 2 in the staged row
+        for (int m = 0; m < k5SRows; m += 5)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {  // staged row i = image row y0 - 2 + i; slot i % 5 = k
+            const int i = m + k, sl = k;
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(base + i * k5Stride);
+            const uint32_t wa = w[0], wb = w[1], wc = w[2];  // (x-2, x-1) (x, x+1) (x+2, x+3)
+            const int32_t vm2 = wa & 0xFFFF, vm1 = wa >> 16, v0 = wb & 0xFFFF, v1 = wb >> 16;
+            const int32_t v2 = wc & 0xFFFF, v3 = wc >> 16;
+            hI[sl][0] = v0;
+            hI[sl][1] = v1;
+            h1[sl][0] = vm1 + v1;
+            h1[sl][1] = v0 + v2;
+            h2[sl][0] = vm2 + v2;
+            h2[sl][1] = vm1 + v3;
+            if (i >= 4) {  // centre row y = y0 - 4 + i (slot (i - 2) % 5) is complete
+                const int y = y0 - 4 + i;
+                const int sm2 = (k + 1) % 5, sm1 = (k + 2) % 5, s0 = (k + 3) % 5, sp1 = (k + 4) % 5, sp2 = k;
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const int32_t S00 = hI[s0][p];
+                    const int32_t S10 = h1[s0][p] + hI[sm1][p] + hI[sp1][p];
+                    const int32_t S20 = h2[s0][p] + hI[sm2][p] + hI[sp2][p];
+                    const int32_t S11 = h1[sm1][p] + h1[sp1][p];
+                    const int32_t S21 = h2[sm1][p] + h2[sp1][p] + h1[sm2][p] + h1[sp2][p];
+                    const int32_t S22 = h2[sm2][p] + h2[sp2][p];
+                    const int32_t r0 = c[0][0] * S00 + c[0][1] * S10 + c[0][2] * S20 + c[0][3] * S11 +
+                                       c[0][4] * S21 + c[0][5] * S22;
+                    const int32_t r1 = c[1][0] * S00 + c[1][1] * S10 + c[1][2] * S20 + c[1][3] * S11 +
+                                       c[1][4] * S21 + c[1][5] * S22;
+                    if ((p == 0 ? ok0 : ok1) && y < g.o1) {
+                        ++tn;
+                        t0 += r0;
+                        t1 += r1;
+                        u0 += (unsigned long long)((long long)r0 * r0);
+                        u1 += (unsigned long long)((long long)r1 * r1);
+                        ti += (uint32_t)S00;
+                        uq += (unsigned long long)((uint32_t)S00 * (uint32_t)S00);
+                    }
+                }
+            }
+        }
+        n += tn;
+        rs0 += t0;
+        rs1 += t1;
+        hi0 += u0 >> 24;
+        lo0 += u0 & 0xFFFFFFull;
+        hi1 += u1 >> 24;
+        lo1 += u1 & 0xFFFFFFull;
+        is += ti;
+        iq += uq;
+    }
+    unsigned long long sv[9] = {(unsigned long long)n,  (unsigned long long)rs0, (unsigned long long)rs1,
+                                hi0, hi1, lo0, lo1, (unsigned long long)is, iq};
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        sv[k] = warp_sum(sv[k]);
+        if (lane == 0) red[warp][k] = sv[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        unsigned long long v = 0;
+        for (int w = 0; w < kThreads / 32; ++w) v += red[w][threadIdx.x];
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(out);
+        atomicAdd(dst + threadIdx.x, v);
+    }
+    if (threadIdx.x == 0) {  // every CTA has taken its last tile: the last one out resets the counter
+        __threadfence();
+        if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) {
+            atomicExch(counter, 0u);
+            atomicExch(counter + 1, 0u);
+        }
+    }
+}
+
 template <typename Tin>
 cudaError_t launch_stats_t(const KParams &kp, const Geometry &g, lfe_stats *d_stats, int grid, cudaStream_t s)
 {
@@ -172,10 +341,30 @@ cudaError_t launch_stats_t(const KParams &kp, const Geometry &g, lfe_stats *d_st
 
 }  // namespace
 
-cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, cudaStream_t s)
+cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, unsigned int *d_counter,
+                         cudaStream_t s)
 {
     const int rows = g.o1 - g.o0;
     if (rows <= 0 || g.width <= 0) return cudaSuccess;
+    if (kp.n[0] == 5 && kp.n[1] == 5 && !kp.f32 && d_counter && !getenv("LFE_STATS_GENERIC")) {
+        // the orbit-sum kernel (5x5 masks); LFE_STATS_GENERIC: the general one (A/B, tests)
+        const long long nt = (long long)((g.width + k5Cols - 1) / k5Cols) * ((rows + k5Rows - 1) / k5Rows);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+        if (in16)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint16_t>, kThreads, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint8_t>, kThreads, 0);
+        const long long cap = (long long)sms * (per_sm > 0 ? per_sm : 4);
+        const int grid = (int)(nt < cap ? nt : cap);
+        if (in16)
+            stats5_kernel<uint16_t><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
+        else
+            stats5_kernel<uint8_t><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
+        return cudaGetLastError();
+    }
     const long long ntiles = (long long)((g.width + kTileW - 1) / kTileW) * ((rows + kTileH - 1) / kTileH);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);

@@ -494,6 +494,8 @@ static lfe_status strip_geometry(lfe_ctx *c, const void *d_in_row0, int64_t in_p
     return LFE_OK;
 }
 
+static lfe_status stats_buffers(lfe_ctx *c);
+
 lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, int32_t W, int32_t rows,
                           int32_t halo_above, int32_t halo_below, uint32_t edge_flags, lfe_stats *d_stats,
                           void *stream)
@@ -507,7 +509,9 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, i
     Geometry g;
     st = strip_geometry(c, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, c->kp.RL, &g);
     if (st != LFE_OK) return st;
-    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, (cudaStream_t)stream);
+    st = stats_buffers(c);
+    if (st != LFE_OK) return st;
+    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, c->d_tile_counter, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
     ++c->launches;
     return LFE_OK;
@@ -517,7 +521,9 @@ static lfe_status stats_buffers(lfe_ctx *c)
 {
     if (c->d_stats) return LFE_OK;
     if (cudaMalloc(&c->d_stats, sizeof(lfe_stats)) != cudaSuccess ||
-        cudaMallocHost(&c->h_stats, sizeof(lfe_stats)) != cudaSuccess) {
+        cudaMallocHost(&c->h_stats, sizeof(lfe_stats)) != cudaSuccess ||
+        cudaMalloc(&c->d_tile_counter, 2 * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemset(c->d_tile_counter, 0, 2 * sizeof(unsigned int)) != cudaSuccess) {
         cudaGetLastError();
         return fail(LFE_ENOMEM, "statistics buffers");
     }
@@ -558,7 +564,7 @@ lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), s) != cudaSuccess)
         return fail(LFE_ECUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
-    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, s);
+    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, c->d_tile_counter, s);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
     ++c->launches;
     KParams kp = c->kp;
@@ -920,6 +926,7 @@ void lfe_destroy(lfe_ctx *c)
     cudaFree(c->d_err);
     cudaFree(c->d_stats);
     cudaFreeHost(c->h_stats);
+    cudaFree(c->d_tile_counter);
     delete c;
 }
 

@@ -95,7 +95,9 @@ cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cu
 // test entry: branch j's response for every pixel of a whole image (int32 or float bits)
 cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int branch, void *d_r, cudaStream_t s);
 // adds the exact global sums of output rows [o0, o1) to *d_stats (NEXT-2)
-cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, cudaStream_t s);
+// d_counter: 2 zeroed uints of tile scheduling state the kernel leaves zeroed (ctx-owned)
+cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, unsigned int *d_counter,
+                         cudaStream_t s);
 
 // ---- host core (lfe_host.cu), shared with the test-only library (csrc/test/) ----
 namespace host {
@@ -130,6 +132,7 @@ struct lfe_ctx {
     double std_T[2] = {0, 0}, std3_T[2] = {-1, -1};
     // adaptive pre-pass (NEXT-2): device accumulator + pinned host copy
     lfe_stats *d_stats = nullptr, *h_stats = nullptr;
+    unsigned int *d_tile_counter = nullptr;  // statistics-kernel tile scheduler state (2 uints)
 };
 
 namespace lfe {

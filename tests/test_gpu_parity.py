@@ -1112,3 +1112,53 @@ def test_signal_and_ipc_roundtrip_in_process():
     assert f.cpu().tolist() == [0, 0, 12345, 0]
     h, off = lfe.lfe_ipc_export(f[2:3].data_ptr())
     assert len(h) == 64 and off >= 16
+
+
+def _stats_oracle(img, p, a=0, b=None):
+    """The 9 lfe_stats sums of rows [a, b) from the oracle's whole-image responses."""
+    b = img.shape[0] if b is None else b
+    I = img.astype(np.int64)[a:b]
+    v = [I.size]
+    hi, lo, rs = [], [], []
+    for j in range(2):
+        q, _ = O.mask_int(p.sigma[j], p.log_size[j], p.bit_depth)
+        r = O.log_response(img, q)[a:b].astype(np.int64)
+        rs.append(int(r.sum()))
+        sq = sum(int(x) * int(x) for x in r.ravel().tolist())
+        hi.append(sq)
+    return v + rs, hi, [int(I.sum()), int((I * I).sum())]
+
+
+@pytest.mark.parametrize("bd", [8, 10, 12, 16])
+def test_stats_orbit_kernel_sums_exact(bd):
+    """The 5x5 statistics kernel (orbit sums shared by both branches, vector-staged
+    interior tiles, clamped border tiles) against exact numpy sums of the oracle's
+    responses, whole images and strips with halos, and against the general
+    kernel (LFE_STATS_GENERIC)."""
+    import os
+    rng = np.random.default_rng(1200 + bd)
+    p = lfe.Params(bit_depth=bd, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+    for H, W, a, b in [(70, 300, 0, 70), (300, 1030, 0, 300), (400, 777, 133, 331), (133, 2048, 5, 128)]:
+        img = scenes.random_image(rng, H, W, bd, "mixed")
+        want_head, want_sq, want_i = _stats_oracle(img, p, a, b)
+        tin = torch.uint8 if bd <= 8 else torch.uint16
+        d = _pitched((H, W), tin)
+        d.copy_(torch.from_numpy(img))
+        got = {}
+        for mode in ("orbit", "generic"):
+            if mode == "generic":
+                os.environ["LFE_STATS_GENERIC"] = "1"
+            try:
+                with lfe.Context(p) as ctx:
+                    st = torch.zeros(9, dtype=torch.int64, device="cuda")
+                    # a side within 8 rows of the image edge reads down to it (edge flag)
+                    flags = (lfe.LFE_TOP_IS_EDGE if a < 8 else 0) | (lfe.LFE_BOTTOM_IS_EDGE if H - b < 8 else 0)
+                    ctx.stats_rows(d, a, b - a, a, H - b, flags, st)
+                    got[mode] = [int(x) for x in st.cpu()]
+            finally:
+                os.environ.pop("LFE_STATS_GENERIC", None)
+        v = got["orbit"]
+        assert v[:3] == want_head, (H, W, a, b)
+        assert [v[3] * 2**24 + v[5], v[4] * 2**24 + v[6]] == want_sq
+        assert v[7:] == want_i
+        assert got["generic"][:3] == v[:3] and got["generic"][7:] == v[7:]

@@ -19,7 +19,7 @@ nvcc $FLAGS -I "$src/include" -I "$src/paper_1304_3992_b200/csrc" -o "abtest/lib
   "$src"/paper_1304_3992_b200/csrc/*.cu
 if [ -z "$2" ]; then
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -cubin -I include \
-    -I paper_1304_3992_b200/csrc -o abtest/kernel_fused.sm_100a.cubin paper_1304_3992_b200/csrc/kernel_fused.cu
+    -I paper_1304_3992_b200/csrc -o abtest/kernel_fused.sm_100a.cubin paper_1304_3992_b200/csrc/kernel_fused_v0.cu
   nvdisasm -c -g abtest/kernel_fused.sm_100a.cubin > abtest/kf.sass
 fi
 echo "built abtest/liblfe_$tag.so from ${2:-the working tree}"

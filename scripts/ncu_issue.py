@@ -32,6 +32,18 @@ out = {
     "dram_bytes": int(f("dram__bytes_read.sum") * 1e6 + f("dram__bytes_write.sum") * 1e6),
     "source": f"{label}: ncu --set full (sm__inst_executed.sum = per_cycle_elapsed x sm__cycles_elapsed.avg)",
 }
+# the sources the capture was built from (bench.py flags a mismatch with the running tree)
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from bench import fused_source_hash  # noqa: E402
+
+out["source_sha"] = fused_source_hash()
 print(json.dumps(out, indent=1))
-with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "issue.json"), "w") as fo:
+with open(os.path.join(ROOT, "profiles", "issue.json"), "w") as fo:
     json.dump(out, fo, indent=1)
+traffic = {"bytes_per_launch": out["dram_bytes"], "algorithmic_bytes": 576000000,
+           "source": f"{label}: ncu --set full of {out['kernel']} at the bench config "
+                     "(dram__bytes_read.sum + dram__bytes_write.sum)",
+           "source_sha": out["source_sha"]}
+with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fo:
+    json.dump(traffic, fo, indent=1)

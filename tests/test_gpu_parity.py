@@ -583,8 +583,10 @@ def test_f32_tolerance_contract(ci):
         print(f"F32 case {ci} {name}: exempt {ex.mean():.4f}, mismatching {mism.mean():.5f}")
         if natural:
             # the exemption set is conservative (every near tie, dilated by the 9x9-11x11
-            # dependency box); what actually differs is tiny
-            assert mism.mean() < 0.002 and ex.mean() < 0.75, (name, mism.mean(), ex.mean())
+            # dependency box); what actually differs is tiny.  Bounds: the measured
+            # exempt fractions of DESIGN.md R23 (0.093 / 0.481 / 0.295 / 0.090) + 25%
+            assert mism.mean() < 0.002, (name, mism.mean())
+            assert ex.mean() < (0.12, 0.60, 0.37, 0.12)[ci], (name, ex.mean())
 
 
 def test_int_response_is_exact():

@@ -740,3 +740,55 @@ def test_pipeline_response_std_source_matches_stagewise_composition():
             unit = 2.0**F * 1023
             k = O.std_gate_response(res.r[j], res.z[j], 5, p.std_threshold[j] * unit, -1.0, src == 3)
             np.testing.assert_array_equal(k, res.keep[j])
+
+
+# ------------------------------------- pins added in round 2 ----
+@pytest.mark.parametrize("w", [3, 5, 7])
+def test_std_gate_windows_3_5_7_vs_statistics_stdev(w):
+    """lfo_std_gate at every window side against Eq. 2 evaluated by
+    statistics.stdev on the replicate-padded w x w window of each crossing pixel
+    (intensity source and binary source; with and without the 3x3 re-check of
+    PAPER.md:94).  Thresholds are drawn away from the deviations' values so the
+    strict '>' is decided the same way by the exact and the float route."""
+    import statistics
+    rng = np.random.default_rng(700 + w)
+    for binary in (False, True):
+        H, W = 19, 23
+        src = (rng.integers(0, 2, (H, W)) if binary else rng.integers(0, 1024, (H, W))).astype(np.uint16)
+        Z = (rng.random((H, W)) < 0.5).astype(np.uint8)
+        P = np.pad(src.astype(float), w // 2, mode="edge")
+        P3 = np.pad(src.astype(float), 1, mode="edge")
+        s_all = [statistics.stdev(P[y:y + w, x:x + w].ravel().tolist()) for y in range(H) for x in range(W)]
+        s3_all = [statistics.stdev(P3[y:y + 3, x:x + 3].ravel().tolist()) for y in range(H) for x in range(W)]
+        vals = sorted(set(round(v, 9) for v in s_all))
+        T = (vals[len(vals) // 3] + vals[len(vals) // 3 + 1]) / 2  # between two attained values
+        v3 = sorted(set(round(v, 9) for v in s3_all))
+        T3 = (v3[len(v3) // 4] + v3[len(v3) // 4 + 1]) / 2
+        for t3 in (-1.0, T3):
+            keep = O.std_gate(src, Z, w, T, t3)
+            for y in range(H):
+                for x in range(W):
+                    k = y * W + x
+                    want = bool(Z[y, x]) and s_all[k] > T and (t3 < 0 or s3_all[k] > t3)
+                    assert bool(keep[y, x]) == want, (w, binary, t3, y, x, s_all[k], T)
+
+
+def test_zc_threshold_int_exact_product():
+    """R9: t = ceil(thr * 2^F * (2^b - 1)), pinned to an exact rational
+    evaluation (fractions.Fraction of the double thr: no rounding anywhere),
+    for thresholds whose exact product is not within 1e-6 of an integer (there
+    the double evaluation is the definition and both must agree)."""
+    from fractions import Fraction
+    rng = np.random.default_rng(77)
+    checked = 0
+    for b in (1, 8, 10, 12, 16):
+        for s in (0.5, 20.0):
+            _, F = O.mask_int(s, 5, b)
+            for thr in list(rng.random(200) * 0.2) + [0.0, 0.01, 0.02, 0.05, 0.3]:
+                exact = Fraction(float(thr)) * (2 ** F) * (2 ** b - 1)
+                if thr > 0 and abs(exact - round(exact)) < Fraction(1, 10**6):
+                    continue
+                want = math.ceil(exact)
+                assert O.zc_threshold_int(float(thr), F, b) == want, (b, s, thr)
+                checked += 1
+    assert checked > 1500

@@ -589,7 +589,7 @@ def main():
                 lfe.lfe_stats_rows(ctx.handle, buf.data_ptr() + shard.ha * bpitch, bpitch, W, shard.rows, shard.ha,
                                    shard.hb, shard.edge_flags(), stats.data_ptr(), cur_stream().cuda_stream)
                 shard.allreduce_stats(stats)
-                ctx.set_stats(stats.cpu().tolist())
+                ctx.set_stats_device(stats)  # resolved on the device: no host round trip
             for b in bands:
                 if not b[5]:
                     launch(b, record)

@@ -120,8 +120,10 @@ lfe_status lfe_create(const lfe_params *p, lfe_ctx **out);
 
 /* Whole-image extraction on the device (the Fig. 1 / Fig. 2 pipeline).
  * With adaptive thresholds it first runs the statistics pass over THIS image,
- * synchronises cuda_stream once to resolve the thresholds on the host (by the
- * lfe_set_stats formulas), then enqueues the extraction with them.  Those
+ * then resolves the thresholds -- on the device when only the ZC gap adapts and
+ * the fused kernel applies (no synchronisation: see lfe_set_stats_device), else
+ * by synchronising cuda_stream once and resolving on the host (by the
+ * lfe_set_stats formulas) -- then enqueues the extraction with them.  Those
  * thresholds apply to this call only: thresholds installed with lfe_set_stats
  * are neither used nor changed.
  * d_in/d_out: device pointers to W x H pitched images; pitches must be >= the
@@ -254,6 +256,21 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch_by
  * Gap thresholds above 2^26 integer units act alike (no gap reaches 2^25, R3)
  * and are clamped there.  Errors: EINVAL (n < 1, or the ctx is not adaptive). */
 lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h_stats);
+
+/* lfe_set_stats without the host round trip: enqueues on cuda_stream the
+ * resolution of the statistics at d_stats (DEVICE memory, e.g. the SUM
+ * all-reduce of every rank's lfe_stats_rows) into the ctx's device-side gap
+ * thresholds, by the same arithmetic as lfe_set_stats bit for bit (R21: the
+ * 128-bit numerator rounded once to double, IEEE sqrt and division).  Later
+ * lfe_extract_rows / lfe_extract_rows_peer / lfe_extract_host calls ordered
+ * after it on the device read them there (the fused kernel only: EUNSUPPORTED
+ * at launch for parameters that need the general kernel).  lfe_get_thresholds
+ * then returns EINVAL (the values are on the device); lfe_set_stats replaces
+ * them.  Only for adaptive == LFE_ADAPT_ZC (EUNSUPPORTED otherwise).  An
+ * adaptive lfe_extract with such parameters takes the same device route by
+ * itself (no stream synchronisation).  Errors: EINVAL, EUNSUPPORTED, ENOMEM,
+ * ECUDA. */
+lfe_status lfe_set_stats_device(lfe_ctx *c, const lfe_stats *d_stats, void *cuda_stream);
 
 /* The ctx's thresholds (fixed ones, or those installed with lfe_set_stats):
  * zc_t[j] in integer response units, std_T[j] and std3_T[j] in Eq. 2 units

@@ -53,6 +53,12 @@ lfe_status lfe_test_extract_r(lfe_ctx *c, const void *d_in, int64_t in_pitch_byt
 lfe_status lfe_test_extract_e(lfe_ctx *c, const void *d_in, int64_t in_pitch_bytes, int32_t width,
                               int32_t height, void *d_out, int64_t out_pitch_bytes, void *cuda_stream);
 
+/* The device-side threshold resolution of lfe_set_stats_device on HOST
+ * statistics: zc_t[2] = the gap thresholds it computes (integer response units,
+ * before the kernel's 2^24 clamp), for comparison with lfe_set_stats +
+ * lfe_get_thresholds (R21).  Synchronous.  Errors: EINVAL, ECUDA. */
+lfe_status lfe_test_resolve(lfe_ctx *c, const lfe_stats *h_stats, int64_t *zc_t);
+
 #ifdef __cplusplus
 }
 #endif

@@ -243,6 +243,7 @@ bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, 
     fa.wait_flag[0] = g.wait_flag[0];
     fa.wait_flag[1] = g.wait_flag[1];
     fa.wait_value = g.wait_value;
+    fa.tg_dev = g.tg_dev;
     if (g.o1 <= g.o0 || g.width <= 0) return false;
 
     fa.seg_base[0] = static_cast<const unsigned char *>(g.above);
@@ -305,9 +306,10 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     // the GAP variant is exact for t = 0 as well; the two-level filter and the 3x3
     // re-check only have that one
     v.peer = g.peer();
-    v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer;
+    v.devt = g.tg_dev != nullptr;
+    v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt;
     for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
-                       fz::launch_group4, fz::launch_group5}) {
+                       fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7}) {
         e = group(v, fa, maps, err_flag, s);
         if (e != cudaErrorNotSupported) return e;
     }

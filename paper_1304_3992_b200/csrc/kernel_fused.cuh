@@ -114,6 +114,9 @@ struct FusedArgs {
     long long seg_pitch[3];
     const unsigned long long *wait_flag[2];
     unsigned long long wait_value;
+    // device-resolved ZC gap thresholds (adaptive, no host round trip): the kernel
+    // reads tg from here instead of `tg` (DEVT instantiations only)
+    const float *tg_dev;
 };
 
 // The launch's input tensor maps, 8-row boxes: `own` over the whole virtual image
@@ -149,6 +152,7 @@ struct Variant {
     bool gap;   // ZC gap test compiled in
     bool rc;    // 3x3 re-check compiled in
     bool peer;  // peer-halo strip (halo rows in the neighbours' memory)
+    bool devt;  // gap thresholds read from device memory (resolved on the device)
 };
 using GroupFn = cudaError_t (*)(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group0(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
@@ -157,6 +161,8 @@ cudaError_t launch_group2(const Variant &, const FusedArgs &, const Maps &, int 
 cudaError_t launch_group3(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group4(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group5(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group6(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group7(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -292,13 +298,17 @@ __device__ __forceinline__ float hi16f(uint32_t w) { return __uint_as_float(prmt
 __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uint_as_float(prmt(w, 0x4B00u, sel)) - 8388608.0f; }
 
 #define LFE_FUSED_VARIANT(A, B, C, D, E)                                                   \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt) \
         return launch_t<A, B, C, D, E>(fa, maps, err_flag, s);
 // peer-halo strips (lfe_extract_rows_peer): a separate instantiation, so that the
 // producer of every other launch is exactly the plain one
 #define LFE_FUSED_PEER_VARIANT(A, B, C)                                                    \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt) \
         return launch_t<A, B, C, true, false, true>(fa, maps, err_flag, s);
+// device-resolved gap thresholds (adaptive lfe_extract, lfe_set_stats_device)
+#define LFE_FUSED_DEVT_VARIANT(A, B, C)                                                    \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt) \
+        return launch_t<A, B, C, true, false, false, kTvNone, true>(fa, maps, err_flag, s);
 
 // ---- left/right image-edge fix-ups (border warps only) ----------------------
 struct Fix {
@@ -588,7 +598,7 @@ struct Producer {
 //     injected responses;
 //   kTvInjectE (lfe_test_extract_e): the merged image is replaced by the input itself,
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ Maps maps, const __grid_constant__ FusedArgs a, int *err_flag)
 {
@@ -617,6 +627,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 *rRing = reinterpret_cast<float4 *>(eRing + kEBytes + kZBytes);  // [2 rows][32 lanes][2 float4]
     unsigned char *hRing = eRing + kEBytes + kZBytes + kRBytes;              // (HM2) rows like the E ring
     const int W = a.W, H = a.H;
+    float tgd[2] = {0.0f, 0.0f};  // DEVT: the gap thresholds resolved on the device
+    if constexpr (DEVT) {
+        tgd[0] = a.tg_dev[0];
+        tgd[1] = a.tg_dev[1];
+    }
+    auto tgv = [&](int j) -> float {
+        if constexpr (DEVT) return tgd[j];
+        else return a.tg[j];
+    };
+    // "no gap" flags of an edge between equal values (as prepare_fused's ung_top)
+    auto ung_top = [&]() -> uint32_t {
+        if constexpr (DEVT) return (tgd[0] > 0.0f ? 0x08080808u : 0u) | (tgd[1] > 0.0f ? 0x80808080u : 0u);
+        else return a.ung_top;
+    };
 
     const unsigned long long t_start = gtime();
     if (threadIdx.x == 0) {
@@ -1008,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) uB[j][i] = fabsf(rB[j][i]) - a.tg[j];
+                for (int i = 0; i < 4; ++i) uB[j][i] = fabsf(rB[j][i]) - tgv(j);
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -1048,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t XG, YG;
         if constexpr (GAP) {
             uint32_t Rngl = __shfl_up_sync(0xffffffffu, Rng, 1);
-            if constexpr (XQ) Rngl = isL ? a.ung_top : Rngl;
+            if constexpr (XQ) Rngl = isL ? ung_top() : Rngl;
             const uint32_t Lng = prmt(Rng, Rngl, 0x2107);
             XG = (NA & ~Ung) | (NC & ~Dng) | (NR & ~Rng) | (NL & ~Lng);
             YG = (PA & ~Ung) | (PC & ~Dng) | (PR & ~Rng) | (PL & ~Lng);
@@ -1079,7 +1103,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float left = i == 0 ? (j == 0 ? l0 : l1) : rB[j][i > 0 ? i - 1 : 0];
                             const float mx = fmaxf(fmaxf(rU[j][i], rC[j][i]), fmaxf(left, rn[j][i]));
                             const float mn = fminf(fminf(rU[j][i], rC[j][i]), fminf(left, rn[j][i]));
-                            if (mx - mn >= a.tg[j]) Z |= 1u << (8 * i + 3 + 4 * j);
+                            if (mx - mn >= tgv(j)) Z |= 1u << (8 * i + 3 + 4 * j);
                         }
                 }
             }
@@ -1111,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 NA = NB;
                 Um = NB;
                 Up = PB;
-                Ung = a.ung_top;
+                Ung = ung_top();
             }
         }
 
@@ -1298,10 +1322,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.dbg[6 * blockIdx.x + 5] = pr.u1;
     }
 }
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false>
 cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV>;
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT>;
     constexpr size_t smem = fused_smem<IN16, HML>();
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)

@@ -176,6 +176,70 @@ constexpr int k5Cols = 256;                // output columns per tile (2 per thr
 constexpr int k5SRows = k5Rows + 4;
 constexpr int k5Stride = k5Cols + 16;      // staged columns x0-8 .. x0+263 (16-byte rows)
 
+// per thread and tile: exact sums over its two columns of the tile's output rows
+// (|sum r| < 66 * 2^23 < 2^30, sum r^2 < 66 * 2^46 < 2^53)
+struct TileSums {
+    int32_t r[2];
+    unsigned long long q[2], iq;
+    uint32_t i;
+    int n;
+};
+
+// one thread's two columns down a staged tile (base = its column x - 2 in staged row 0).
+// FULL: every column and row of the tile is an output (no per-pixel conditions).
+template <bool FULL>
+__device__ __forceinline__ void tile_sums(const uint16_t *base, const int32_t (&c)[2][6], bool ok0, bool ok1,
+                                          int rows_left, TileSums &ts)
+{
+    ts.r[0] = ts.r[1] = 0;
+    ts.q[0] = ts.q[1] = ts.iq = 0;
+    ts.i = 0;
+    ts.n = FULL ? 2 * k5Rows : 0;
+    // history of the last 5 rows (slot = row index mod 5), per column p = 0, 1
+    int32_t hI[5][2], h1[5][2], h2[5][2];
+    for (int m = 0; m < k5SRows; m += 5)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {  // staged row i = image row y0 - 2 + i; slot i % 5 = k
+            const int i = m + k;
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(base + i * k5Stride);
+            const uint32_t wa = w[0], wb = w[1], wc = w[2];  // (x-2, x-1) (x, x+1) (x+2, x+3)
+            const int32_t vm2 = wa & 0xFFFF, vm1 = wa >> 16, v0 = wb & 0xFFFF, v1 = wb >> 16;
+            const int32_t v2 = wc & 0xFFFF, v3 = wc >> 16;
+            hI[k][0] = v0;
+            hI[k][1] = v1;
+            h1[k][0] = vm1 + v1;
+            h1[k][1] = v0 + v2;
+            h2[k][0] = vm2 + v2;
+            h2[k][1] = vm1 + v3;
+            if (m > 0 || k == 4) {  // centre row i - 2 (output row i - 4 of the tile) is complete
+                const int sm2 = (k + 1) % 5, sm1 = (k + 2) % 5, s0 = (k + 3) % 5, sp1 = (k + 4) % 5, sp2 = k;
+                const bool row_ok = FULL || i - 4 < rows_left;
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const int32_t S00 = hI[s0][p];
+                    const int32_t S10 = h1[s0][p] + hI[sm1][p] + hI[sp1][p];
+                    const int32_t S20 = h2[s0][p] + hI[sm2][p] + hI[sp2][p];
+                    const int32_t S11 = h1[sm1][p] + h1[sp1][p];
+                    const int32_t S21 = h2[sm1][p] + h2[sp1][p] + h1[sm2][p] + h1[sp2][p];
+                    const int32_t S22 = h2[sm2][p] + h2[sp2][p];
+                    const int32_t r0 = c[0][0] * S00 + c[0][1] * S10 + c[0][2] * S20 + c[0][3] * S11 +
+                                       c[0][4] * S21 + c[0][5] * S22;
+                    const int32_t r1 = c[1][0] * S00 + c[1][1] * S10 + c[1][2] * S20 + c[1][3] * S11 +
+                                       c[1][4] * S21 + c[1][5] * S22;
+                    if (FULL || ((p == 0 ? ok0 : ok1) && row_ok)) {
+                        if (!FULL) ++ts.n;
+                        ts.r[0] += r0;
+                        ts.r[1] += r1;
+                        ts.q[0] += (unsigned long long)((long long)r0 * r0);
+                        ts.q[1] += (unsigned long long)((long long)r1 * r1);
+                        ts.i += (uint32_t)S00;
+                        ts.iq += (unsigned long long)(uint32_t)S00 * (uint32_t)S00;
+                    }
+                }
+            }
+        }
+}
+
 // Tiles are handed out dynamically: counter[0] is the next tile, counter[1] counts
 // finished CTAs; the last CTA resets both to 0 for the next launch (launches that
 // share a counter are stream-ordered: one ctx, one stream at a time).
@@ -243,56 +307,15 @@ __global__ void __launch_bounds__(kThreads)
         }
         __syncthreads();
         const int xa = x0 + 2 * t;  // this thread's columns xa, xa + 1
-        const bool ok0 = xa < W, ok1 = xa + 1 < W;
-        // per tile column pair: |sum r| < 66 * 2^23 < 2^30, sum r^2 < 66 * 2^46 < 2^53
-        int32_t t0 = 0, t1 = 0;
-        unsigned long long u0 = 0, u1 = 0, uq = 0;
-        uint32_t ti = 0;
-        int tn = 0;
-        // history of the last 5 rows (slot = row index mod 5), per column p = 0, 1
-        int32_t hI[5][2], h1[5][2], h2[5][2];
-        const uint16_t *base = sI + 2 * t + 6;  // column xa - 2 in the staged row
-        for (int m = 0; m < k5SRows; m += 5)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {  // staged row i = image row y0 - 2 + i; slot i % 5 = k
-            const int i = m + k, sl = k;
-            const uint32_t *w = reinterpret_cast<const uint32_t *>(base + i * k5Stride);
-            const uint32_t wa = w[0], wb = w[1], wc = w[2];  // (x-2, x-1) (x, x+1) (x+2, x+3)
-            const int32_t vm2 = wa & 0xFFFF, vm1 = wa >> 16, v0 = wb & 0xFFFF, v1 = wb >> 16;
-            const int32_t v2 = wc & 0xFFFF, v3 = wc >> 16;
-            hI[sl][0] = v0;
-            hI[sl][1] = v1;
-            h1[sl][0] = vm1 + v1;
-            h1[sl][1] = v0 + v2;
-            h2[sl][0] = vm2 + v2;
-            h2[sl][1] = vm1 + v3;
-            if (i >= 4) {  // centre row y = y0 - 4 + i (slot (i - 2) % 5) is complete
-                const int y = y0 - 4 + i;
-                const int sm2 = (k + 1) % 5, sm1 = (k + 2) % 5, s0 = (k + 3) % 5, sp1 = (k + 4) % 5, sp2 = k;
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    const int32_t S00 = hI[s0][p];
-                    const int32_t S10 = h1[s0][p] + hI[sm1][p] + hI[sp1][p];
-                    const int32_t S20 = h2[s0][p] + hI[sm2][p] + hI[sp2][p];
-                    const int32_t S11 = h1[sm1][p] + h1[sp1][p];
-                    const int32_t S21 = h2[sm1][p] + h2[sp1][p] + h1[sm2][p] + h1[sp2][p];
-                    const int32_t S22 = h2[sm2][p] + h2[sp2][p];
-                    const int32_t r0 = c[0][0] * S00 + c[0][1] * S10 + c[0][2] * S20 + c[0][3] * S11 +
-                                       c[0][4] * S21 + c[0][5] * S22;
-                    const int32_t r1 = c[1][0] * S00 + c[1][1] * S10 + c[1][2] * S20 + c[1][3] * S11 +
-                                       c[1][4] * S21 + c[1][5] * S22;
-                    if ((p == 0 ? ok0 : ok1) && y < g.o1) {
-                        ++tn;
-                        t0 += r0;
-                        t1 += r1;
-                        u0 += (unsigned long long)((long long)r0 * r0);
-                        u1 += (unsigned long long)((long long)r1 * r1);
-                        ti += (uint32_t)S00;
-                        uq += (unsigned long long)((uint32_t)S00 * (uint32_t)S00);
-                    }
-                }
-            }
-        }
+        TileSums ts;
+        if (x0 + k5Cols <= W && y0 + k5Rows <= g.o1)
+            tile_sums<true>(sI + 2 * t + 6, c, 0, 0, 0, ts);
+        else
+            tile_sums<false>(sI + 2 * t + 6, c, xa < W, xa + 1 < W, g.o1 - y0, ts);
+        const int32_t t0 = ts.r[0], t1 = ts.r[1];
+        const unsigned long long u0 = ts.q[0], u1 = ts.q[1], uq = ts.iq;
+        const uint32_t ti = ts.i;
+        const int tn = ts.n;
         n += tn;
         rs0 += t0;
         rs1 += t1;
@@ -372,6 +395,62 @@ cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_st
     if (sms <= 0) sms = 148;
     const int grid = (int)(ntiles < 16LL * sms ? ntiles : 16LL * sms);
     return in16 ? launch_stats_t<uint16_t>(kp, g, d_stats, grid, s) : launch_stats_t<uint8_t>(kp, g, d_stats, grid, s);
+}
+
+}  // namespace lfe
+
+// ---- adaptive gap thresholds resolved on the device (R21) ------------------------
+namespace lfe {
+namespace {
+
+// (double) of an unsigned 128-bit integer, rounded to nearest-even exactly once
+// (what the host's conversion does; plain 64-bit halves would round twice)
+__device__ double u128_to_double_rn(unsigned __int128 v)
+{
+    const unsigned long long hi = (unsigned long long)(v >> 64);
+    if (hi == 0) return __ull2double_rn((unsigned long long)v);
+    const int msb = 127 - __clzll((long long)hi);  // >= 64
+    int shift = msb - 52;                           // >= 12: keep bits msb .. msb-52
+    unsigned long long m = (unsigned long long)(v >> shift);
+    const unsigned __int128 rem = v - ((unsigned __int128)m << shift);
+    const unsigned __int128 half = (unsigned __int128)1 << (shift - 1);
+    if (rem > half || (rem == half && (m & 1ull))) {
+        ++m;
+        if (m == (1ull << 53)) {
+            m >>= 1;
+            ++shift;
+        }
+    }
+    return ldexp((double)m, shift);  // m < 2^53: exact
+}
+
+// sigma = sqrt(n S2 - S1^2) / n, the numerator exact (128-bit) and rounded once
+__device__ double global_std_dev(long long n, __int128 S1, unsigned __int128 S2)
+{
+    const __int128 D = (__int128)n * (__int128)S2 - S1 * S1;
+    return __dsqrt_rn(u128_to_double_rn((unsigned __int128)D)) / (double)n;
+}
+
+__global__ void resolve_kernel(const lfe_stats *st, double k0, double k1, DevThresholds *out)
+{
+    const double k[2] = {k0, k1};
+    for (int j = 0; j < 2; ++j) {
+        const unsigned __int128 S2 = ((unsigned __int128)(unsigned long long)st->r_sq_hi[j] << 24) +
+                                     (unsigned __int128)(unsigned long long)st->r_sq_lo[j];
+        const double sigma = global_std_dev(st->n, (__int128)st->r_sum[j], S2);
+        const double x = __dmul_rn(k[j], sigma);
+        const long long t = (long long)ceil(fmin(x, 0x1p26));  // the host's gap_units
+        out->zc_t[j] = t;
+        out->tg[j] = (float)(t < (1LL << 24) ? t : (1LL << 24));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_resolve(const lfe_stats *d_stats, double k0, double k1, DevThresholds *d_thr, cudaStream_t s)
+{
+    resolve_kernel<<<1, 1, 0, s>>>(d_stats, k0, k1, d_thr);
+    return cudaGetLastError();
 }
 
 }  // namespace lfe

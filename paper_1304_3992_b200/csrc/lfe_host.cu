@@ -237,6 +237,8 @@ lfe_status run(lfe_ctx *c, const KParams &kp, const Geometry &g, cudaStream_t s)
         return fail(LFE_EUNSUPPORTED, "peer-halo strips need the fused kernel (5x5 masks, std on the ZC image, "
                                       "16-byte aligned bases and pitches)");
     if (g.peer() && k == LFE_KERNEL_STAGED) return fail(LFE_EUNSUPPORTED, "peer-halo strips need the fused kernel");
+    if (g.tg_dev && (k == LFE_KERNEL_STAGED || (k == LFE_KERNEL_AUTO && !fused_ok)))
+        return fail(LFE_EUNSUPPORTED, "device-resolved thresholds (lfe_set_stats_device) need the fused kernel");
     if (k == LFE_KERNEL_AUTO) k = fused_ok ? LFE_KERNEL_FUSED : LFE_KERNEL_STAGED;
     if (k == LFE_KERNEL_FUSED && !fused_ok)
         return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
@@ -454,6 +456,7 @@ lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h)
 {
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
     if (!c->p.adaptive) return fail(LFE_EINVAL, "ctx has no adaptive thresholds");
+    c->dev_thresholds = false;
     if (!h) {
         c->have_thresholds = false;
         return LFE_OK;
@@ -466,9 +469,32 @@ lfe_status lfe_set_stats(lfe_ctx *c, const lfe_stats *h)
     return LFE_OK;
 }
 
+static lfe_status stats_buffers(lfe_ctx *c);
+
+lfe_status lfe_set_stats_device(lfe_ctx *c, const lfe_stats *d_stats, void *stream)
+{
+    if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (c->p.adaptive != LFE_ADAPT_ZC)
+        return fail(LFE_EUNSUPPORTED, "device-resolved thresholds: only the adaptive ZC gap (LFE_ADAPT_ZC alone)");
+    if (!d_stats || reinterpret_cast<uintptr_t>(d_stats) % 8) return fail(LFE_EINVAL, "d_stats NULL or misaligned");
+    lfe_status st = check_bound_device(c);
+    if (st != LFE_OK) return st;
+    st = stats_buffers(c);
+    if (st != LFE_OK) return st;
+    cudaError_t e = launch_resolve(d_stats, c->p.zc_threshold[0], c->p.zc_threshold[1], c->d_thr, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "resolve launch: %s", cudaGetErrorString(e));
+    // the std thresholds are the fixed parameters (only the gap adapts); the gap entries
+    // are unused (the fused kernel reads the device values)
+    const int64_t zt0[2] = {0, 0};
+    install_thresholds(c, zt0, c->p.std_threshold, c->p.std3_threshold);
+    c->dev_thresholds = true;
+    return LFE_OK;
+}
+
 lfe_status lfe_get_thresholds(const lfe_ctx *c, int64_t *zc_t, double *std_T, double *std3_T)
 {
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
+    if (c->dev_thresholds) return fail(LFE_EINVAL, "thresholds resolved on the device (lfe_set_stats_device)");
     if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx without statistics (lfe_set_stats)");
     for (int j = 0; j < 2; ++j) {
         if (zc_t) zc_t[j] = c->zc_t[j];
@@ -523,7 +549,8 @@ static lfe_status stats_buffers(lfe_ctx *c)
     if (cudaMalloc(&c->d_stats, sizeof(lfe_stats)) != cudaSuccess ||
         cudaMallocHost(&c->h_stats, sizeof(lfe_stats)) != cudaSuccess ||
         cudaMalloc(&c->d_tile_counter, 2 * sizeof(unsigned int)) != cudaSuccess ||
-        cudaMemset(c->d_tile_counter, 0, 2 * sizeof(unsigned int)) != cudaSuccess) {
+        cudaMemset(c->d_tile_counter, 0, 2 * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&c->d_thr, sizeof(DevThresholds)) != cudaSuccess) {
         cudaGetLastError();
         return fail(LFE_ENOMEM, "statistics buffers");
     }
@@ -543,6 +570,19 @@ static lfe_status resolve_from_device(lfe_ctx *c, cudaStream_t s, KParams &kp)
     thresholds_from_stats(c, *c->h_stats, zt, T, T3);
     write_thresholds(c, kp, zt, T, T3);
     return LFE_OK;
+}
+
+// the fused kernel can take this ctx's adaptive thresholds from device memory:
+// only the ZC gap adapts (the std thresholds stay fixed) and the parameters and
+// the geometry's alignment are the fused kernel's
+static bool device_resolvable(const lfe_ctx *c, const Geometry &g)
+{
+    if (c->p.adaptive != LFE_ADAPT_ZC || c->cfg.kernel == LFE_KERNEL_STAGED) return false;
+    KParams kp = c->kp;
+    kp.zc_t[0] = kp.zc_t[1] = 0;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(g.in) | reinterpret_cast<uintptr_t>(g.out) |
+                           (uintptr_t)g.in_pitch | (uintptr_t)g.out_pitch) & 15u) == 0;
+    return aligned && fused_supports(kp, c->p.bit_depth);
 }
 
 lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
@@ -567,6 +607,20 @@ lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W
     cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, c->d_tile_counter, s);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
     ++c->launches;
+    if (device_resolvable(c, g)) {
+        // only the ZC gap adapts and the fused kernel runs: resolve the thresholds on
+        // the device and let the kernel read them -- no host round trip, stream-ordered
+        e = launch_resolve(c->d_stats, c->p.zc_threshold[0], c->p.zc_threshold[1], c->d_thr, s);
+        if (e != cudaSuccess) return fail(LFE_ECUDA, "resolve launch: %s", cudaGetErrorString(e));
+        Geometry gd = g;
+        gd.tg_dev = c->d_thr->tg;
+        // the std thresholds are the fixed parameters (only the gap adapts); the gap
+        // entries are unused (the kernel reads the device values)
+        KParams kp = c->kp;
+        const int64_t zt0[2] = {0, 0};
+        write_thresholds(c, kp, zt0, c->p.std_threshold, c->p.std3_threshold);
+        return run(c, kp, gd, s);
+    }
     KParams kp = c->kp;
     st = resolve_from_device(c, s, kp);
     if (st != LFE_OK) return st;
@@ -610,6 +664,7 @@ static lfe_status extract_rows(lfe_ctx *c, const KParams &kp, const void *d_in_r
         return fail(LFE_EINVAL, "input and output overlap");
     g.out = d_out_row0;
     g.out_pitch = out_pitch;
+    if (c->dev_thresholds) g.tg_dev = c->d_thr->tg;
     return run(c, kp, g, stream);
 }
 
@@ -670,6 +725,7 @@ lfe_status lfe_extract_rows_peer(lfe_ctx *c, const void *d_in_row0, int64_t in_p
         g.o0 = 0;
         g.o1 = rows;
     }
+    if (c->dev_thresholds) g.tg_dev = c->d_thr->tg;
     return run(c, c->kp, g, (cudaStream_t)stream);
 }
 
@@ -927,6 +983,7 @@ void lfe_destroy(lfe_ctx *c)
     cudaFree(c->d_stats);
     cudaFreeHost(c->h_stats);
     cudaFree(c->d_tile_counter);
+    cudaFree(c->d_thr);
     delete c;
 }
 

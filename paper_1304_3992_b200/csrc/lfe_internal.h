@@ -75,7 +75,20 @@ struct Geometry {
     const unsigned long long *wait_flag[2] = {nullptr, nullptr};
     unsigned long long wait_value = 0;
     bool peer() const { return ha_peer > 0 || hb_peer > 0; }
+    // fused kernel only: the ZC gap thresholds (float, integer response units) in
+    // device memory, resolved there (DevThresholds::tg); NULL = the KParams ones
+    const float *tg_dev = nullptr;
 };
+
+// Adaptive ZC gap thresholds resolved on the device from an lfe_stats (R21): the
+// same arithmetic as the host's lfe_set_stats, bit for bit.
+struct DevThresholds {
+    float tg[2];        // min(t_j, 2^24) as fp32 (gaps are < 2^24: larger t act alike)
+    int32_t pad[2];
+    long long zc_t[2];  // t_j = ceil(k_j * sigma(r_j)), clamped at 2^26 like the host
+};
+// enqueues the resolution of *d_stats into *d_thr (k_j = zc_threshold[j])
+cudaError_t launch_resolve(const lfe_stats *d_stats, double k0, double k1, DevThresholds *d_thr, cudaStream_t s);
 
 struct LaunchCfg {
     int kernel;   // LFE_KERNEL_*
@@ -133,6 +146,8 @@ struct lfe_ctx {
     // adaptive pre-pass (NEXT-2): device accumulator + pinned host copy
     lfe_stats *d_stats = nullptr, *h_stats = nullptr;
     unsigned int *d_tile_counter = nullptr;  // statistics-kernel tile scheduler state (2 uints)
+    lfe::DevThresholds *d_thr = nullptr;     // device-resolved gap thresholds (adaptive, no host sync)
+    bool dev_thresholds = false;             // lfe_set_stats_device installed them (lfe_extract_rows*)
 };
 
 namespace lfe {

@@ -102,4 +102,23 @@ lfe_status lfe_test_extract_e(lfe_ctx *c, const void *d_in, int64_t in_pitch, in
 }
 
 
+lfe_status lfe_test_resolve(lfe_ctx *c, const lfe_stats *h_stats, int64_t *zc_t)
+{
+    if (!c || !h_stats || !zc_t) return fail(LFE_EINVAL, "NULL argument");
+    lfe_stats *d = nullptr;
+    DevThresholds *t = nullptr;
+    DevThresholds h{};
+    cudaError_t e = cudaMalloc(&d, sizeof *d);
+    if (e == cudaSuccess) e = cudaMalloc(&t, sizeof *t);
+    if (e == cudaSuccess) e = cudaMemcpy(d, h_stats, sizeof *d, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_resolve(d, c->p.zc_threshold[0], c->p.zc_threshold[1], t, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(&h, t, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(t);
+    if (e != cudaSuccess) return fail(LFE_ECUDA, "resolve: %s", cudaGetErrorString(e));
+    zc_t[0] = h.zc_t[0];
+    zc_t[1] = h.zc_t[1];
+    return LFE_OK;
+}
+
 }  // extern "C"

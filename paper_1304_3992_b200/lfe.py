@@ -86,9 +86,10 @@ EXPORTS = ["lfe_params_default", "lfe_create", "lfe_extract", "lfe_extract_rows"
            "lfe_halo", "lfe_get_mask", "lfe_last_async_error", "lfe_set_option", "lfe_launch_count",
            "lfe_destroy", "lfe_strerror", "lfe_last_message", "lfe_abi_version", "lfe_stats_rows",
            "lfe_set_stats", "lfe_get_thresholds", "lfe_extract_bands", "lfe_extract_rows_peer", "lfe_signal",
-           "lfe_ipc_export", "lfe_ipc_open", "lfe_ipc_close"]
+           "lfe_ipc_export", "lfe_ipc_open", "lfe_ipc_close", "lfe_set_stats_device"]
 # include/lfe_test.h, exported by the separate liblfe_test.so
-TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response", "lfe_test_extract_r", "lfe_test_extract_e"]
+TEST_EXPORTS = ["lfe_test_mask", "lfe_test_validate", "lfe_test_response", "lfe_test_extract_r", "lfe_test_extract_e",
+                "lfe_test_resolve"]
 _test_lib = None
 
 
@@ -150,6 +151,9 @@ def load():
         L.lfe_ipc_open.restype = st
         L.lfe_ipc_close.argtypes = [P, I64]
         L.lfe_ipc_close.restype = st
+    if hasattr(L, "lfe_set_stats_device"):
+        L.lfe_set_stats_device.argtypes = [P, P, P]
+        L.lfe_set_stats_device.restype = st
     _lib = L
     return L
 
@@ -176,6 +180,8 @@ def load_test():
     T.lfe_test_extract_r.restype = st
     T.lfe_test_extract_e.argtypes = [P, P, I64, I32, I32, P, I64, P]
     T.lfe_test_extract_e.restype = st
+    T.lfe_test_resolve.argtypes = [P, ctypes.POINTER(lfe_stats), P]
+    T.lfe_test_resolve.restype = st
     _test_lib = T
     return T
 
@@ -512,6 +518,19 @@ class Context:
 
     def thresholds(self):
         return lfe_get_thresholds(self.handle)
+
+    def set_stats_device(self, t_stats, stream=None):
+        """lfe_set_stats_device: resolve the thresholds on the device from a CUDA
+        int64 tensor of the 9 lfe_stats values (no host round trip)."""
+        _check(load().lfe_set_stats_device(self.handle, t_stats.data_ptr(), self._stream(stream)),
+               "lfe_set_stats_device")
+
+    def test_resolve(self, values):
+        """lfe_test_resolve: the device resolution of host statistics -> (t_0, t_1)."""
+        z = (ctypes.c_int64 * 2)()
+        s = values if isinstance(values, lfe_stats) else self.stats_from(values)
+        _check(load_test().lfe_test_resolve(self.handle, ctypes.byref(s), z), "lfe_test_resolve")
+        return z[0], z[1]
 
     def test_response(self, t_in, branch: int, stream=None):
         """lfe_test_response: branch's LoG response of a whole device image as the

@@ -459,11 +459,13 @@ def test_adaptive_thresholds_and_sums_equal_oracle():
     assert v[7:] == [int(I.sum()), int((I * I).sum())]
 
 
+@pytest.mark.parametrize("device", [False, True])
 @pytest.mark.parametrize("cuts", [[0, 50, 200, 512], [0, 7, 300, 505, 512]])
-def test_adaptive_strips_with_summed_statistics(cuts):
+def test_adaptive_strips_with_summed_statistics(cuts, device):
     """The multi-GPU recipe: per-strip lfe_stats_rows into one accumulator (what
-    an int64 all-reduce does across ranks), lfe_set_stats, then lfe_extract_rows
-    per strip == the oracle on the whole image."""
+    an int64 all-reduce does across ranks), lfe_set_stats (or, device=True,
+    lfe_set_stats_device: resolved on the device, no host round trip), then
+    lfe_extract_rows per strip == the oracle on the whole image."""
     img = scenes.scene_c1(clean=False)
     p = lfe.Params(bit_depth=8, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.6, 0.8), median_window2=3)
     want = O.run(img, _oparams(p))
@@ -480,7 +482,13 @@ def test_adaptive_strips_with_summed_statistics(cuts):
             st = torch.zeros(9, dtype=torch.int64, device="cuda")
             ctx.stats_rows(d[a - ha:b + hb].clone(), ha, b - a, ha, hb, flags, st)
             parts.append(st)
-        ctx.set_stats(torch.stack(parts).sum(0).cpu().tolist())
+        total = torch.stack(parts).sum(0)
+        if device:
+            ctx.set_stats_device(total)
+            with pytest.raises(lfe.LfeError):  # the values live on the device
+                ctx.thresholds()
+        else:
+            ctx.set_stats(total.cpu().tolist())
         out = torch.zeros_like(d)
         for a, b in zip(cuts[:-1], cuts[1:]):
             ha, hb = min(h, a), min(h, H - b)
@@ -1164,3 +1172,38 @@ def test_stats_orbit_kernel_sums_exact(bd):
         assert [v[3] * 2**24 + v[5], v[4] * 2**24 + v[6]] == want_sq
         assert v[7:] == want_i
         assert got["generic"][:3] == v[:3] and got["generic"][7:] == v[7:]
+
+
+def test_device_resolved_thresholds_equal_host():
+    """lfe_set_stats_device's arithmetic (R21 on the device: the 128-bit numerator
+    rounded once to double by hand, IEEE sqrt / division / product, ceil, the
+    2^26 clamp) equals the host's lfe_set_stats bit for bit: random statistics,
+    numerators far beyond 2^64 and 2^53, exact squares, ties at .5 ulp, and the
+    statistics of real images."""
+    rng = np.random.default_rng(31)
+    p = lfe.Params(bit_depth=16, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 1.37))
+    cases = []
+    for _ in range(400):
+        n = int(rng.integers(1, 2**31))
+        vmax = int(rng.integers(1, 2**23))
+        S1 = [int(rng.integers(-vmax, vmax)) * int(rng.integers(0, n)) // 3 for _ in range(2)]
+        S2 = [n * vmax * vmax - int(rng.integers(0, 2**20)) for _ in range(2)]
+        cases.append((n, S1, S2))
+    cases += [(1, [0, 0], [0, 0]), (4, [2, -2], [2, 2]), (2**31 - 1, [0, 0], [(2**31 - 1) * 2**46] * 2),
+              (3, [1, 1], [1, 1]), (10**9, [12345678901, -98765432109], [10**9 * 2**40 + 1, 10**9 * 2**44 + 7])]
+    with lfe.Context(p) as ctx:
+        for n, S1, S2 in cases:
+            if any(n * s2 - s1 * s1 < 0 for s1, s2 in zip(S1, S2)):
+                continue
+            v = [n, S1[0], S1[1], S2[0] >> 24, S2[1] >> 24, S2[0] & 0xFFFFFF, S2[1] & 0xFFFFFF, 0, 0]
+            ctx.set_stats(v)
+            z, _, _ = ctx.thresholds()
+            assert tuple(ctx.test_resolve(v)) == tuple(z), (n, S1, S2)
+        for seed in range(3):
+            img = scenes.random_image(np.random.default_rng(seed), 300, 500, 16, "mixed")
+            st = torch.zeros(9, dtype=torch.int64, device="cuda")
+            ctx.stats_rows(torch.from_numpy(img).cuda(), 0, 300, 0, 0,
+                           lfe.LFE_TOP_IS_EDGE | lfe.LFE_BOTTOM_IS_EDGE, st)
+            v = [int(x) for x in st.cpu()]
+            ctx.set_stats(v)
+            assert tuple(ctx.test_resolve(v)) == tuple(ctx.thresholds()[0])

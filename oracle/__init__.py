@@ -59,8 +59,13 @@ class _Params(ctypes.Structure):
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB)
+        # LFE_ORACLE_LIB: an instrumented build of the same source (ASan/UBSan runs,
+        # tests/test_sanitizers.py) instead of the default one
+        path = os.environ.get("LFE_ORACLE_LIB")
+        if not path:
+            build()
+            path = _LIB
+        L = ctypes.CDLL(path)
         P = ctypes.c_void_p
         L.lfo_set_threads.argtypes = [ctypes.c_int]
         L.lfo_get_threads.restype = ctypes.c_int

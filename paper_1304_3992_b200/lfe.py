@@ -18,7 +18,8 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LFE_LIB") or os.path.join(_PKG, "liblfe.so")  # LFE_LIB: A/B experiments only
-TEST_LIB_PATH = os.path.join(_PKG, "liblfe_test.so")  # include/lfe_test.h: test-only entry points
+# include/lfe_test.h: test-only entry points (LFE_TEST_LIB: an instrumented build, sanitizer runs only)
+TEST_LIB_PATH = os.environ.get("LFE_TEST_LIB") or os.path.join(_PKG, "liblfe_test.so")
 
 LFE_OK, LFE_EINVAL, LFE_EUNSUPPORTED, LFE_ENOMEM, LFE_ENODEV, LFE_ECUDA, LFE_ERANGE = range(7)
 LFE_STD_ZC, LFE_STD_INTENSITY, LFE_STD_RESPONSE, LFE_STD_RESPONSE_AT_ZC = 0, 1, 2, 3

@@ -48,3 +48,44 @@ with lfe.Context(lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), std3_thresh
     ctx.extract(torch.from_numpy(img).cuda())
     ctx.check()
     print('ok recheck')
+
+# round 2: peer-halo strips (3 strips in separate allocations, flags signalled), the
+# device-resolved adaptive path (DEVT kernel + resolve kernel), lfe_set_stats_device
+# on strips, and the orbit-sum statistics kernel on u8 / u16 odd shapes
+p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+with lfe.Context(p) as ctx:
+    H, W = img.shape
+    cuts = [0, 90, 180, H]
+    bufs = [torch.from_numpy(np.ascontiguousarray(img[a:b])).cuda() for a, b in zip(cuts, cuts[1:])]
+    outs = [torch.empty_like(x) for x in bufs]
+    fl = torch.zeros(3, dtype=torch.int64, device='cuda')
+    for k in range(3):
+        lfe.lfe_signal(fl[k:k + 1].data_ptr(), 1, torch.cuda.current_stream().cuda_stream)
+    for k in range(3):
+        above = bufs[k - 1][bufs[k - 1].shape[0] - lfe.LFE_PEER_ROWS:] if k > 0 else None
+        below = bufs[k + 1] if k < 2 else None
+        ctx.extract_rows_peer(bufs[k], outs[k], above, below,
+                              wait_above=fl[k - 1:k].data_ptr() if k > 0 else None,
+                              wait_below=fl[k + 1:k + 2].data_ptr() if k < 2 else None, wait_value=1)
+    ctx.check()
+    print('ok peer strips')
+pa = lfe.Params(bit_depth=10, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+with lfe.Context(pa) as ctx:
+    d = torch.from_numpy(img).cuda()
+    ctx.extract(d)  # device-resolved thresholds, no host sync
+    st = torch.zeros(9, dtype=torch.int64, device='cuda')
+    ctx.stats_rows(d, 0, 150, 0, 7, lfe.LFE_TOP_IS_EDGE, st)
+    ctx.stats_rows(d, 150, 150, 7, 0, lfe.LFE_BOTTOM_IS_EDGE, st)
+    ctx.set_stats_device(st)
+    out = torch.empty_like(d)
+    ctx.extract_rows(d, 0, 300, 0, 0, lfe.LFE_TOP_IS_EDGE | lfe.LFE_BOTTOM_IS_EDGE, out)
+    ctx.check()
+    print('ok device thresholds')
+for bd, shape in [(8, (70, 300)), (16, (133, 1030))]:
+    pi = lfe.Params(bit_depth=bd, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+    x = scenes.random_image(np.random.default_rng(bd), *shape, bd, 'mixed')
+    with lfe.Context(pi) as ctx:
+        st = torch.zeros(9, dtype=torch.int64, device='cuda')
+        ctx.stats_rows(torch.from_numpy(x).cuda(), 0, shape[0], 0, 0, 3, st)
+        ctx.check()
+    print('ok stats5', bd, shape)

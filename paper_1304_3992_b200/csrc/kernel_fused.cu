@@ -2,6 +2,8 @@
 // map, cost-weighted partition, parameter packing and variant dispatch.
 #include "kernel_fused.cuh"
 
+#include <cmath>
+
 namespace lfe {
 namespace fz {
 
@@ -171,9 +173,12 @@ void cached_partition(FusedArgs &fa, int grid, int halo)
 bool fused_supports(const KParams &kp, int bit_depth)
 {
     using namespace fz;
-    (void)bit_depth;
     if (kp.n[0] != 5 || kp.n[1] != 5) return false;
-    if (kp.std_source != LFE_STD_ZC || kp.w != 5) return false;
+    if (kp.w != 5) return false;
+    // std on the ZC image; or on the intensity image (exact int32 window sums for
+    // b <= 10, 5x5 only: no 3x3 re-check variant, no peer / device-threshold one)
+    const bool stdi = kp.std_source == LFE_STD_INTENSITY && bit_depth <= 10 && !kp.recheck[0] && !kp.recheck[1];
+    if (kp.std_source != LFE_STD_ZC && !stdi) return false;
     if (kp.f32) return false;  // float masks (R23): general kernel only
     if (kp.hm && kp.m != 5) return false;
     if (kp.m2 && !(kp.hm && kp.m == 5 && kp.m2 == 3)) return false;
@@ -181,7 +186,7 @@ bool fused_supports(const KParams &kp, int bit_depth)
     for (int j = 0; j < 2; ++j) {
         if (kp.zc_t[j] > (1 << 24)) return false;  // t <= 2^24: every gap test is exact in fp32
         int lo, hi;
-        if (!interval_of(kp.pass_lut[j], 25, &lo, &hi)) return false;
+        if (!stdi && !interval_of(kp.pass_lut[j], 25, &lo, &hi)) return false;
     }
     return encode_fn() != nullptr;
 }
@@ -244,6 +249,12 @@ bool prepare_fused(const KParams &kp, const Geometry &g, bool in16, int tile_h, 
     fa.wait_flag[1] = g.wait_flag[1];
     fa.wait_value = g.wait_value;
     fa.tg_dev = g.tg_dev;
+    // intensity std gate (R11): (double)LHS > rhs  <=>  LHS >= floor(rhs) + 1 for an integer
+    // LHS (< 2^30 for b <= 10)
+    for (int j = 0; j < 2; ++j) {
+        const double r = kp.rhs[j];
+        fa.stdi_L[j] = !(r < 1073741824.0) ? 1073741824 : r < 0.0 ? 0 : (int)std::floor(r) + 1;
+    }
     if (g.o1 <= g.o0 || g.width <= 0) return false;
 
     fa.seg_base[0] = static_cast<const unsigned char *>(g.above);
@@ -307,9 +318,12 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     // re-check only have that one
     v.peer = g.peer();
     v.devt = g.tg_dev != nullptr;
-    v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt;
+    v.stdi = kp.std_source == LFE_STD_INTENSITY;
+    if (v.stdi && (v.peer || v.devt)) return cudaErrorNotSupported;
+    v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt || v.stdi;
     for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
-                       fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7}) {
+                       fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7,
+                       fz::launch_group8, fz::launch_group9}) {
         e = group(v, fa, maps, err_flag, s);
         if (e != cudaErrorNotSupported) return e;
     }

@@ -75,6 +75,7 @@ constexpr int kEBytes = 16 * kERow;         // 8-row E ring per warp, mirrored
 constexpr int kZBytes = 16 * 32 * 4;        // 8-row Z ring per warp, mirrored
 constexpr int kRBytes = 2 * 32 * 32;        // 2-row r ring per warp (zero-pixel slow path)
 constexpr int kHBytes = 4 * kERow;          // 4-row ring of first-median-level rows (second level only)
+constexpr int kPBytes = 8 * 32 * 4;         // 8-row ring of intensity-std pass words per warp (STDI only)
 constexpr int kHdr = 128;                   // mbarriers
 constexpr int kEdge = 16;                   // rows near the image top/bottom walked separately
 constexpr int kMaxGrid = 192;               // largest grid the weighted partition table serves
@@ -117,6 +118,9 @@ struct FusedArgs {
     // device-resolved ZC gap thresholds (adaptive, no host round trip): the kernel
     // reads tg from here instead of `tg` (DEVT instantiations only)
     const float *tg_dev;
+    // std gate on the INTENSITY image (R10's alternative, STDI instantiations, b <= 10):
+    // pass_j <=> 25 S2 - S1^2 >= stdi_L[j] over the 5x5 window (= "> rhs_j" of R11)
+    int stdi_L[2];
 };
 
 // The launch's input tensor maps, 8-row boxes: `own` over the whole virtual image
@@ -153,6 +157,7 @@ struct Variant {
     bool rc;    // 3x3 re-check compiled in
     bool peer;  // peer-halo strip (halo rows in the neighbours' memory)
     bool devt;  // gap thresholds read from device memory (resolved on the device)
+    bool stdi;  // std gate on the intensity image (b <= 10)
 };
 using GroupFn = cudaError_t (*)(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group0(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
@@ -163,6 +168,8 @@ cudaError_t launch_group4(const Variant &, const FusedArgs &, const Maps &, int 
 cudaError_t launch_group5(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group6(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group7(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group8(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group9(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -298,17 +305,21 @@ __device__ __forceinline__ float hi16f(uint32_t w) { return __uint_as_float(prmt
 __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uint_as_float(prmt(w, 0x4B00u, sel)) - 8388608.0f; }
 
 #define LFE_FUSED_VARIANT(A, B, C, D, E)                                                   \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi) \
         return launch_t<A, B, C, D, E>(fa, maps, err_flag, s);
 // peer-halo strips (lfe_extract_rows_peer): a separate instantiation, so that the
 // producer of every other launch is exactly the plain one
 #define LFE_FUSED_PEER_VARIANT(A, B, C)                                                    \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt && !v.stdi) \
         return launch_t<A, B, C, true, false, true>(fa, maps, err_flag, s);
 // device-resolved gap thresholds (adaptive lfe_extract, lfe_set_stats_device)
 #define LFE_FUSED_DEVT_VARIANT(A, B, C)                                                    \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi) \
         return launch_t<A, B, C, true, false, false, kTvNone, true>(fa, maps, err_flag, s);
+// std gate on the intensity image (b <= 10; gap test compiled in)
+#define LFE_FUSED_STDI_VARIANT(A, B, C)                                                    \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && !v.devt && v.stdi) \
+        return launch_t<A, B, C, true, false, false, kTvNone, false, true>(fa, maps, err_flag, s);
 
 // ---- left/right image-edge fix-ups (border warps only) ----------------------
 struct Fix {
@@ -598,7 +609,8 @@ struct Producer {
 //     injected responses;
 //   kTvInjectE (lfe_test_extract_e): the merged image is replaced by the input itself,
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
+          bool STDI = false>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ Maps maps, const __grid_constant__ FusedArgs a, int *err_flag)
 {
@@ -626,6 +638,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *zRing = reinterpret_cast<uint32_t *>(eRing + kEBytes);
     float4 *rRing = reinterpret_cast<float4 *>(eRing + kEBytes + kZBytes);  // [2 rows][32 lanes][2 float4]
     unsigned char *hRing = eRing + kEBytes + kZBytes + kRBytes;              // (HM2) rows like the E ring
+    // (STDI) pass words of the intensity std gate, slot = row & 7: [8][32 lanes]
+    uint32_t *pRing = reinterpret_cast<uint32_t *>(ring + kS * kStageBytes + kWarps * warp_bytes(HML)) + warp * 8 * 32;
     const int W = a.W, H = a.H;
     float tgd[2] = {0.0f, 0.0f};  // DEVT: the gap thresholds resolved on the device
     if constexpr (DEVT) {
@@ -696,6 +710,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t chk_lo = 0, chk_hi = 0;  // the range-check masks of the current chunk
     float acc[2][4][4];
     uint32_t PA, NA, PB, NB, Um, Up, Ung, V;
+    // (STDI) running 5-row window sums of the per-row 5-sums of I (exact fp32) and of
+    // I^2 (int32), window rows rho-4 .. rho, this lane's 4 pixels; first row of the walk
+    float S1w[4];
+    int32_t S2w[4];
+    int rho_first = 0;
 
     auto row_ptr = [&](int p) -> const unsigned char * {
         const int d = p - it.plo;
@@ -761,6 +780,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- std gate + merge for row rho-6 (Z rows rho-8 .. rho-4) ----------------
         uint32_t Zc;
         const uint32_t *zk = zRing + k * 32 + lane;
+        uint32_t M7;
+        if constexpr (STDI) {
+            // std gate on the intensity image (R10's alternative): the pass word of row
+            // rho-6 was formed 4 steps ago (bit 7: branch 0, bit 6: branch 1)
+            if constexpr (!YF)
+                Zc = zk[2 * 32];  // row rho-6
+            else
+                Zc = row_e >= 0 ? zRing[(min(row_e, H - 1) & 7) * 32 + lane] : 0u;
+            const uint32_t P6 = pRing[(row_e & 7) * 32 + lane];
+            M7 = (P6 & (Zc << 7)) | ((P6 << 1) & (Zc << 3));
+        } else {
         if constexpr (!YF) {
             const uint32_t z_new = zk[4 * 32];  // row rho-4
             const uint32_t z_old = zk[7 * 32];  // row rho-9
@@ -807,7 +837,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             pass0 &= (K30 + a.add_lo3[0]) & ~(K30 + a.add_hi3[0]);
             pass1 &= (K31 + a.add_lo3[1]) & ~(K31 + a.add_hi3[1]);
         }
-        const uint32_t M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
+        M7 = (pass0 & (Zc << 7)) | (pass1 & (Zc << 3));  // merged flag at bit 7 of each byte
+        }  // !STDI
         uint32_t e0, e1;                                              // E pairs of row rho-6
         {
             uint32_t i0, i1;
@@ -947,6 +978,99 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (XQ) I[1] = isL ? I[2] : I[1];
         if constexpr (XQ) I[6] = isR ? I[5] : I[6];
         if constexpr (XQ) I[7] = isR ? I[5] : I[7];
+
+        // ---------------- intensity std window (STDI): rows rho-4 .. rho -> pass of row rho-2 ----------------
+        if constexpr (STDI) {
+            // 5-sums of I and of I^2 around this lane's 4 pixels in one row (replicate-
+            // padded columns, like the LoG's input): every value an exact fp32 integer
+            // (b <= 10: 5 * 1023^2 < 2^23)
+            auto row_sums = [&](const float (&v)[8], float (&h1)[4], int32_t (&h2)[4]) {
+                float q[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) q[m] = v[m] * v[m];
+                float s1 = (v[0] + v[1]) + (v[2] + v[3]) + v[4];
+                float s2 = (q[0] + q[1]) + (q[2] + q[3]) + q[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (i > 0) {
+                        s1 = (s1 - v[i - 1]) + v[i + 4];
+                        s2 = (s2 - q[i - 1]) + q[i + 4];
+                    }
+                    h1[i] = s1;
+                    h2[i] = __float_as_int(s2 + 8388608.0f) - 0x4B000000;  // exact: 0 <= s2 < 2^23
+                }
+            };
+            float h1n[4];
+            int32_t h2n[4];
+            row_sums(I, h1n, h2n);
+            if (rho - 5 >= rho_first) {  // the row leaving the window, rho-5, was added this walk
+                const unsigned char *op = YF ? row_ptr(prow(rho - 5)) + off_own
+                                             : (k >= 5 ? cb + (k - 5) * kRowBytes : pb + (k + 3) * kRowBytes);
+                float J[8];
+                if constexpr (IN16) {
+                    const uint2 own = *reinterpret_cast<const uint2 *>(op);
+                    J[2] = lo16f(own.x);
+                    J[3] = hi16f(own.x);
+                    J[4] = lo16f(own.y);
+                    J[5] = hi16f(own.y);
+                } else {
+                    const uint32_t own = *reinterpret_cast<const uint32_t *>(op);
+                    J[2] = byte_f(own, 0x5440);
+                    J[3] = byte_f(own, 0x5441);
+                    J[4] = byte_f(own, 0x5442);
+                    J[5] = byte_f(own, 0x5443);
+                }
+                if constexpr (XF) {
+                    float own4[4] = {J[2], J[3], J[4], J[5]};
+                    fix_floats(fx, own4);
+                    J[2] = own4[0];
+                    J[3] = own4[1];
+                    J[4] = own4[2];
+                    J[5] = own4[3];
+                }
+                J[0] = __shfl_up_sync(0xffffffffu, J[4], 1);
+                J[1] = __shfl_up_sync(0xffffffffu, J[5], 1);
+                J[6] = __shfl_down_sync(0xffffffffu, J[2], 1);
+                J[7] = __shfl_down_sync(0xffffffffu, J[3], 1);
+                if constexpr (XQ) J[0] = isL ? J[2] : J[0];
+                if constexpr (XQ) J[1] = isL ? J[2] : J[1];
+                if constexpr (XQ) J[6] = isR ? J[5] : J[6];
+                if constexpr (XQ) J[7] = isR ? J[5] : J[7];
+                float h1o[4];
+                int32_t h2o[4];
+                row_sums(J, h1o, h2o);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    S1w[i] += h1n[i] - h1o[i];
+                    S2w[i] += h2n[i] - h2o[i];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    S1w[i] += h1n[i];
+                    S2w[i] += h2n[i];
+                }
+            }
+            // Eq. 2 over the 5x5 window (R11): pass_j <=> 25 S2 - S1^2 >= stdi_L[j], exact in
+            // int32 (b <= 10); the sign of the difference, gathered by PRMT sign replication
+            int32_t dd[2][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int32_t s1 = __float_as_int(S1w[i] + 8388608.0f) - 0x4B000000;  // exact: 0 <= S1 < 2^23
+                const int32_t lhs = 25 * S2w[i] - s1 * s1;
+                dd[0][i] = lhs - a.stdi_L[0];
+                dd[1][i] = lhs - a.stdi_L[1];
+            }
+            uint32_t fail[2];  // 0xFF bytes where the pixel fails
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t lo = prmt((uint32_t)dd[j][0], (uint32_t)dd[j][1], 0x00FB);
+                const uint32_t hi = prmt((uint32_t)dd[j][2], (uint32_t)dd[j][3], 0xFB00);
+                fail[j] = (lo & 0x0000FFFFu) | (hi & 0xFFFF0000u);
+            }
+            const uint32_t P = (~fail[0] & 0x80808080u) | (~fail[1] & 0x40404040u);
+            pRing[((rho - 2) & 7) * 32 + lane] = P;
+        }
 
         // ---------------- LoG x 2, streaming over rows ----------------
         if constexpr (TV == kTvInjectR) {
@@ -1190,6 +1314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 4; ++i) acc[j][0][i] = acc[j][1][i] = acc[j][2][i] = acc[j][3][i] = 0.0f;
         PA = NA = PB = NB = Um = Up = Ung = 0;
         V = 0;
+        if constexpr (STDI) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                S1w[i] = 0.0f;
+                S2w[i] = 0;
+            }
+        }
         if constexpr (!YF) {
 #pragma unroll
             for (int k = 0; k < 16; ++k) zRing[k * 32 + lane] = 0;
@@ -1205,6 +1336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // interior walks start at the first staged row (= ys - kHalo, or up to kR - 1
         // rows earlier on a peer-aligned stage grid); output row of step rho = rho - kLag
         const int rho0 = YF ? it.ys - kHalo : it.plo;
+        rho_first = rho0;
         optr = obase + (long long)(rho0 - kLag - it.ys) * a.out_pitch;
         for (int rho = rho0; rho < rho_end; rho += kR) {
             // wait for the ring stages holding this chunk's input rows
@@ -1322,11 +1454,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.dbg[6 * blockIdx.x + 5] = pr.u1;
     }
 }
-template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false>
+template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
+          bool STDI = false>
 cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT>;
-    constexpr size_t smem = fused_smem<IN16, HML>();
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI>;
+    constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0);
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)
     // (std::call_once: distinct ctxs on distinct host threads may launch concurrently)

@@ -15,8 +15,12 @@ want = sys.argv[1] if len(sys.argv) > 1 else "fused_kernelILb1ELi1ELb0ELb1E"
 with tempfile.TemporaryDirectory() as d:
     subprocess.check_call(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_1304_3992_b200", "liblfe.so")],
                           cwd=d, stdout=subprocess.DEVNULL)
-    cub = next(f for f in sorted(os.listdir(d)) if "kernel_fused_v0" in f and f.endswith(".cubin"))
-    txt = subprocess.check_output(["nvdisasm", "-c", os.path.join(d, cub)], text=True)
+    txt = ""
+    for cub in sorted(f for f in os.listdir(d) if "kernel_fused_v" in f and f.endswith(".cubin")):
+        t = subprocess.check_output(["nvdisasm", "-c", os.path.join(d, cub)], text=True)
+        if want in t:
+            txt = t
+            break
 sec = None
 lines = []
 for ln in txt.splitlines():

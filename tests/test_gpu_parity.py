@@ -1207,3 +1207,32 @@ def test_device_resolved_thresholds_equal_host():
             v = [int(x) for x in st.cpu()]
             ctx.set_stats(v)
             assert tuple(ctx.test_resolve(v)) == tuple(ctx.thresholds()[0])
+
+
+# ------------------ std gate on the intensity image in the fused kernel (R10 alternative) ----
+@pytest.mark.parametrize("bd,hm,m2,mode,T", [(8, True, 0, lfe.LFE_OUT_EXTRACT, 12.0),
+                                             (10, True, 0, lfe.LFE_OUT_MASK, 30.0),
+                                             (10, False, 0, lfe.LFE_OUT_EXTRACT, 8.5),
+                                             (8, True, 3, lfe.LFE_OUT_EXTRACT, 20.0),
+                                             (10, True, 3, lfe.LFE_OUT_MASK, 0.0)])
+def test_fused_intensity_std(bd, hm, m2, mode, T):
+    """LFE_STD_INTENSITY (Eq. 2 over the 5x5 window of I; R10's
+    alternative reading) on the fused kernel (forced: LFE_KERNEL_FUSED): running
+    5-row sums of per-row 5-sums of I and I^2, exact int32 test 25 S2 - S1^2 >=
+    floor(rhs) + 1.  Random images with edge-row pieces, ragged and multiple-of-4
+    widths, several column groups; the two branches get different thresholds."""
+    rng = np.random.default_rng(1500 + bd + int(T))
+    p = lfe.Params(bit_depth=bd, zc_threshold=(0.01, 0.02), std_source=lfe.LFE_STD_INTENSITY,
+                   std_threshold=(T, 1.5 * T + 1.0), hybrid_median=hm, median_window2=m2, out_mode=mode)
+    for (H, W), kind in itertools.product([(37, 150), (203, 1400), (130, 2701), (64, 2688), (5, 33)],
+                                          ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, bd, kind)
+        assert_same(run_gpu(img, p, lfe.LFE_KERNEL_FUSED), O.run(img, _oparams(p)), f"{H}x{W} {kind}")
+
+
+def test_fused_intensity_std_c3_full_size():
+    """c3 at full size with the intensity std source (T = 20 DN at 10 bit), every
+    pixel; AUTO picks the fused kernel."""
+    img = scenes.scene_c3()
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02), std_source=lfe.LFE_STD_INTENSITY, std_threshold=(20.0, 20.0))
+    assert_same(run_gpu(img, p), O.run(img, _oparams(p)), "c3 intensity std")

@@ -93,6 +93,9 @@ def parse():
     ap.add_argument("--tile", type=str, default="", help="TWxTH override (tuning only)")
     ap.add_argument("--median2", type=int, default=0, choices=[0, 3, 5, 7],
                     help="second hybrid-median level (the water pipeline, PAPER.md:102); 0 = the metric config")
+    ap.add_argument("--std", choices=["zc", "intensity"], default="zc",
+                    help="image the Eq. 2 deviation is computed on (reading R10): the ZC image (the metric config) "
+                         "or the intensity image (R10's alternative; T = 20 DN x 2^(b-10))")
     ap.add_argument("--adaptive", type=float, default=0.0,
                     help="k > 0: adaptive ZC gap t = ceil(k * sigma(r)) (SPEC.md:233, NEXT-2), with its "
                          "statistics pre-pass and all-reduce inside every step; 0 = the metric config")
@@ -111,13 +114,15 @@ def geometry(args):
     return c
 
 
-def workload_params(cfg, median2=0, adaptive=0.0):
+def workload_params(cfg, median2=0, adaptive=0.0, std="zc"):
     from paper_1304_3992_b200 import lfe
     # SURVEY.md 8(c) defaults for benchmark scenes: ZC gap 0.02 (normalised; 0.01 for the
     # 12-bit c4), std source = ZC image, 5x5 window, T = 0.3, hybrid median on, extract.
     zc = (adaptive, adaptive) if adaptive > 0 else (cfg["zc"], cfg["zc"])
+    T = 0.3 if std == "zc" else 20.0 * 2.0 ** (cfg["bit_depth"] - 10)
     return lfe.Params(bit_depth=cfg["bit_depth"], sigma=(0.5, 20.0), log_size=(5, 5), zc_threshold=zc,
-                      std_source=lfe.LFE_STD_ZC, std_window=5, std_threshold=(0.3, 0.3),
+                      std_source=lfe.LFE_STD_ZC if std == "zc" else lfe.LFE_STD_INTENSITY, std_window=5,
+                      std_threshold=(T, T),
                       std3_threshold=(-1.0, -1.0), hybrid_median=True, median_window=5,
                       out_mode=lfe.LFE_OUT_EXTRACT, median_window2=median2,
                       adaptive=lfe.LFE_ADAPT_ZC if adaptive > 0 else 0)
@@ -176,11 +181,14 @@ def config_dict(name, cfg, world, p, graph=False, halo_mode=None):
           f"scene ({2 * in_bytes / 1e6:.1f} MB in + out) is L2-resident across steps: no flush, "
           "a latency/launch-bound config")
     return {
-        "workload": f"{cfg['desc']}; dual LoG (sigma 0.5, 20; 5x5) + {zc} + 5x5 std gate (T=0.3) + OR + {hm}, extract",
+        "workload": f"{cfg['desc']}; dual LoG (sigma 0.5, 20; 5x5) + {zc} + 5x5 std gate "
+                    f"({'on the ZC image' if p.std_source == 0 else 'on the intensity image'}, T={p.std_threshold[0]:g})"
+                    f" + OR + {hm}, extract",
         "name": name, "width": W, "height": H, "bit_depth": cfg["bit_depth"], "bands": B,
         "parallelism": par, "l2": l2,
         "params": {"sigma": list(p.sigma), "log_size": list(p.log_size), "zc_threshold": list(p.zc_threshold),
-                   "std_source": "zc", "std_window": p.std_window, "std_threshold": list(p.std_threshold),
+                   "std_source": "zc" if p.std_source == 0 else "intensity", "std_window": p.std_window,
+                   "std_threshold": list(p.std_threshold),
                    "hybrid_median": bool(p.hybrid_median), "median_window": p.median_window,
                    "median_window2": p.median_window2, "adaptive": p.adaptive, "out_mode": "extract"},
     }
@@ -404,7 +412,7 @@ def run_reference(args, world, rank):
     import oracle
     from paper_1304_3992_b200 import scenes
     cfg = geometry(args)
-    p = workload_params(cfg, args.median2, args.adaptive)
+    p = workload_params(cfg, args.median2, args.adaptive, args.std)
     H, W, h = cfg["H"], cfg["W"], halo_rows(p)
     rows = min(512, H)
     if args.config == "c4":
@@ -462,7 +470,7 @@ def main():
     dev = torch.device("cuda", local)
     cfg = geometry(args)
     name = args.config
-    p = workload_params(cfg, args.median2, args.adaptive)
+    p = workload_params(cfg, args.median2, args.adaptive, args.std)
     H, W, NB = cfg["H"], cfg["W"], cfg["bands"]
     tdt = torch.uint8 if elem(cfg) == 1 else torch.uint16
     esz = elem(cfg)
@@ -801,7 +809,7 @@ def main():
             line["verify"] = verify
         src = fused_source_hash()
         headline = name == "c3" and cfg["W"] == 12000 and not p.adaptive and not p.median_window2 \
-            and args.kernel != "staged"
+            and args.kernel != "staged" and args.std == "zc"
         iss = _profile_json("issue.json")
         if iss and headline:
             # the binding resource: instruction issue, 4 warp-instructions

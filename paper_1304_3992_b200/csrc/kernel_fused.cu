@@ -56,6 +56,18 @@ constexpr double kPiece = 19.5;      // row-equivalents per piece (pipeline warm
 constexpr double kEdgePiece = 2.7;    // extra for an edge-row piece (general path)
 constexpr double kEdgeCol = 1.048;   // column-edge group, cheap path (W % 4 == 0)
 constexpr double kEdgeColGen = 1.40; // column-edge group, general path
+constexpr double kPartialFloor = 0.55; // a column group with few working warps (see partial_floor; 0.45 / 0.6 / 1.0 measured)
+
+// per-row cost of a column group whose warps mostly idle, relative to a full one
+// (LFE_DEBUG_PARTIAL overrides it: tuning only)
+double partial_floor()
+{
+    static const double v = [] {
+        const char *e = getenv("LFE_DEBUG_PARTIAL");
+        return e ? atof(e) : kPartialFloor;
+    }();
+    return v;
+}
 
 // per-CTA cost of units [u0, u1); `paired`: the cost of one CTA of a pair
 // sharing the range (half of every segment, every piece)
@@ -67,7 +79,11 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool pair
     while (u < u1) {
         const int bg = (int)(u / R), r0 = (int)(u - (long long)bg * R), g = bg % G;
         const int n = (int)std::min<long long>(R - r0, u1 - u);
-        const double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kEdgeCol) : 1.0;
+        double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kEdgeCol) : 1.0;
+        // a last column group with fewer warps holding output columns (the others only
+        // follow the ring): per-row cost falls with them, to a single-warp latency floor
+        const int nw = (fa.W - g * kCtaOut + kWarpOut - 1) / kWarpOut;
+        if (nw < kWarps) f *= std::max(partial_floor(), (double)nw / kWarps);
         int ys = fa.o0 + r0;
         const int ye_all = ys + n;
         while (ys < ye_all) {  // the kernel's split at kEdge rows from the virtual top/bottom

@@ -1419,7 +1419,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the instruction cache): 0 interior; 4 cheap column edges (W % 4 == 0); 3 general
         // fix-ups (edge rows, or column edges of other widths)
         const bool xedge_cta = (it.xo - kHaloX < 0 || it.xo - kHaloX + (kWarps - 1) * kWarpOut + 128 > W) && !a.dbg_nofix;
-        if (it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge_cta && (W & 3))) {
+        if (xw + kHaloX >= W) {
+            // no output column of this warp is in the image (the last column group of a
+            // width that is not a multiple of 1344): follow the ring without computing --
+            // wait for each stage, then release it, in order (an early release would count
+            // towards the slot's previous use)
+            for (int j = 0; j < it.nst; ++j) {
+                if (threadIdx.x == kProdThread) prod.run(rel_w);
+                __syncwarp();
+                const uint32_t g = g_base + j;
+                if (j > 0) mbar_wait(&full[g % kS], (g / kS) & 1);
+                if (lane == 0) mbar_arrive(&empty[g % kS]);
+                ++rel_w;
+            }
+            released = it.nst;
+        } else if (it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge_cta && (W & 3))) {
             isL = isR = false;
             walk(std::integral_constant<int, 3>{});
         } else if (xedge_cta) {

@@ -56,7 +56,7 @@ constexpr double kPiece = 19.5;      // row-equivalents per piece (pipeline warm
 constexpr double kEdgePiece = 2.7;    // extra for an edge-row piece (general path)
 constexpr double kEdgeCol = 1.048;   // column-edge group, cheap path (W % 4 == 0)
 constexpr double kEdgeColGen = 1.40; // column-edge group, general path
-constexpr double kPartialFloor = 0.55; // a column group with few working warps (see partial_floor; 0.45 / 0.6 / 1.0 measured)
+constexpr double kPartialFloor = 0.55; // a column group with 1-2 working warps (see partial_floor; 0.45 / 0.6 / 1.0 measured)
 
 // per-row cost of a column group whose warps mostly idle, relative to a full one
 // (LFE_DEBUG_PARTIAL overrides it: tuning only)
@@ -80,10 +80,12 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool pair
         const int bg = (int)(u / R), r0 = (int)(u - (long long)bg * R), g = bg % G;
         const int n = (int)std::min<long long>(R - r0, u1 - u);
         double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kEdgeCol) : 1.0;
-        // a last column group with fewer warps holding output columns (the others only
-        // follow the ring): per-row cost falls with them, to a single-warp latency floor
+        // a last column group where only one or two warps hold output columns (the
+        // others only follow the ring) costs about a single warp's latency per row; with
+        // more working warps the per-row time stays near a full group's (10 warps: 0.97,
+        // DESIGN.md 12), so those keep weight 1 (c5's 9-warp group at 0.75 cost +26%)
         const int nw = (fa.W - g * kCtaOut + kWarpOut - 1) / kWarpOut;
-        if (nw < kWarps) f *= std::max(partial_floor(), (double)nw / kWarps);
+        if (nw <= 2) f *= partial_floor();
         int ys = fa.o0 + r0;
         const int ye_all = ys + n;
         while (ys < ye_all) {  // the kernel's split at kEdge rows from the virtual top/bottom

@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--impl", choices=["lfe", "reference"], default="lfe")
     ap.add_argument("--config", choices=sorted(CFG), default="c3")
     ap.add_argument("--kernel", choices=["auto", "staged", "fused"], default="auto")
+    ap.add_argument("--log-unit", choices=["auto", "cuda"], default="auto",
+                    help="fused kernel LoG: tensor cores where exact (auto) or forced CUDA cores (A/B)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="do not report the oracle timing")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check of the last step")
@@ -476,6 +478,7 @@ def main():
     esz = elem(cfg)
     ctx = lfe.Context(p)
     ctx.set_option(lfe.LFE_OPT_KERNEL, {"auto": 0, "staged": 1, "fused": 2}[args.kernel])
+    ctx.set_option(lfe.LFE_OPT_LOG_UNIT, {"auto": lfe.LFE_LOG_AUTO, "cuda": lfe.LFE_LOG_CUDA_CORES}[args.log_unit])
     if args.tile:
         tw, th = (int(v) for v in args.tile.split("x"))
         ctx.set_option(lfe.LFE_OPT_TILE_W, tw)

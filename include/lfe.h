@@ -63,7 +63,13 @@ enum { LFE_OUT_EXTRACT = 0, LFE_OUT_MASK = 1 };
 /* lfe_extract_rows: which strip sides are true image edges (clamped). */
 enum { LFE_TOP_IS_EDGE = 1u, LFE_BOTTOM_IS_EDGE = 2u };
 /* lfe_set_option keys (test/tuning only; results never depend on them). */
-enum { LFE_OPT_KERNEL = 1, LFE_OPT_TILE_W = 2, LFE_OPT_TILE_H = 3, LFE_OPT_HOST_STRIP_ROWS = 4 };
+enum { LFE_OPT_KERNEL = 1, LFE_OPT_TILE_W = 2, LFE_OPT_TILE_H = 3, LFE_OPT_HOST_STRIP_ROWS = 4, LFE_OPT_LOG_UNIT = 5 };
+/* LFE_OPT_LOG_UNIT values: where the fused kernel computes the two LoG responses.
+ * AUTO: on the tensor cores (tcgen05) when exact there -- uint16 input with
+ * b <= 11 and every mask coefficient an fp16 value -- else on the CUDA cores
+ * (exact-integer fp32 FFMA); CUDA_CORES forces the latter (A/B and tests).
+ * Results are identical either way. */
+enum { LFE_LOG_AUTO = 0, LFE_LOG_CUDA_CORES = 1 };
 /* LFE_OPT_KERNEL values. */
 enum { LFE_KERNEL_AUTO = 0, LFE_KERNEL_STAGED = 1, LFE_KERNEL_FUSED = 2 };
 /* lfe_params.adaptive flags (NEXT-2, readings R21/R22). */

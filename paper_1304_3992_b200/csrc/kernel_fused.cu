@@ -4,6 +4,8 @@
 
 #include <cmath>
 
+#include <cuda_fp16.h>
+
 namespace lfe {
 namespace fz {
 
@@ -319,10 +321,23 @@ cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cu
     return cudaGetLastError();
 }
 
-cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h, int *err_flag,
+// The LoG on the tensor cores is exact when the u16 input bits read as fp16 are the
+// values themselves times 2^-24 (v < 2048: subnormals and the first binade) and every
+// mask coefficient is an fp16 value (scripts/tc_probe.cu).
+static bool tc_exact(const KParams &kp, bool in16)
+{
+    if (!in16 || kp.maxv > 2047) return false;
+    for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 6; ++k) {
+            const float c = (float)kp.orb[j][k];
+            if (std::fabs(c) > 65504.0f || __half2float(__float2half_rn(c)) != c) return false;
+        }
+    return true;
+}
+
+cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int log_unit, int tile_h, int *err_flag,
                          cudaStream_t s)
 {
-    (void)tile_w;
     fz::FusedArgs fa;
     fz::Maps maps;
     cudaError_t e;
@@ -339,11 +354,16 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int ti
     v.stdi = kp.std_source == LFE_STD_INTENSITY;
     if (v.stdi && (v.peer || v.devt)) return cudaErrorNotSupported;
     v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt || v.stdi;
-    for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
-                       fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7,
-                       fz::launch_group8, fz::launch_group9}) {
-        e = group(v, fa, maps, err_flag, s);
-        if (e != cudaErrorNotSupported) return e;
+    // the tensor-core LoG where it is exact and compiled (else the CUDA-core one)
+    v.tc = log_unit != LFE_LOG_CUDA_CORES && !v.peer && !v.stdi && tc_exact(kp, in16);
+    for (int pass = v.tc ? 0 : 1; pass < 2; ++pass) {
+        v.tc = pass == 0;
+        for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
+                           fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7,
+                           fz::launch_group8, fz::launch_group9, fz::launch_group10}) {
+            e = group(v, fa, maps, err_flag, s);
+            if (e != cudaErrorNotSupported) return e;
+        }
     }
     return cudaErrorNotSupported;
 }

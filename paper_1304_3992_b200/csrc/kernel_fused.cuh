@@ -44,6 +44,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -158,6 +159,7 @@ struct Variant {
     bool peer;  // peer-halo strip (halo rows in the neighbours' memory)
     bool devt;  // gap thresholds read from device memory (resolved on the device)
     bool stdi;  // std gate on the intensity image (b <= 10)
+    bool tc;    // LoG on the tensor cores (u16, b <= 11, fp16-exact masks)
 };
 using GroupFn = cudaError_t (*)(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group0(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
@@ -170,6 +172,7 @@ cudaError_t launch_group6(const Variant &, const FusedArgs &, const Maps &, int 
 cudaError_t launch_group7(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group8(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group9(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group10(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -233,6 +236,78 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
             smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
+}
+
+// ---- tcgen05 (TC variants: the LoG on the tensor cores) ---------------------------
+// The 5x5 LoG of both branches as one small MMA per 4 rows and group of 4 warps:
+// D[m][n] = sum_k A[m][k] B[k][n] with m = the TMEM lane = (warp % 4, lane) = this
+// lane's 4-column group, k = (patch row ky, patch column kx) of the 8 x 8 input
+// patch (columns x-2 .. x+5, rows of the half-chunk), n = (r row, branch, pixel).
+// A is the lane's own patch (tcgen05.st into its TMEM lane), B the constant banded
+// mask matrix in shared memory, D lands in TMEM where tcgen05.ld hands every lane
+// exactly its 4 pixels x 2 branches of one r row: the layout the rest of the row
+// step uses, no transposition.  Exactness (scripts/tc_probe.cu):
+// the u16 input bits read as fp16 are the subnormals v * 2^-24 (exact for v < 2048),
+// the integer mask coefficients are exact fp16 values (checked on the host), every
+// product is an exact multiple of 2^-24 and every partial sum stays below 2^24 units
+// (R3), which the fp32 accumulation keeps: D = r * 2^-24 exactly.
+constexpr int kTcB = 64 * 32 * 2;  // B: K = 64 (8 patch rows x 8 columns) x N = 32 (4 r rows x 2 branches x 4 pixels), fp16
+constexpr int kTcCols = 160;       // TMEM columns per group of 4 warps: A x2 (48 each) + D (2 halves x 32)
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 4 patch rows (16 columns) of this lane's A row
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+// one r row of this lane: 2 branches x 4 pixels (fp32 bits, scaled by 2^-24)
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+// the registers of a tcgen05.ld are valid only after this wait: they are in/out
+// operands here so that no use can be scheduled above it
+__device__ __forceinline__ void tc_wait_ld(uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+                 :
+                 : "memory");
+}
+
+// D[dcol .. +32) (= 4 r rows) from A columns [acol, acol + 32) (= 8 patch rows) and B:
+// four K = 16 steps, then a commit to `bar` (one elected thread)
+__device__ __forceinline__ void tc_mma_half(uint32_t dcol, uint32_t acol, uint32_t b_saddr, uint64_t *bar)
+{
+    // kind::f16: A = B = F16, D = F32, both K-major, N = 32 (>> 3), M = 128 (>> 4)
+    constexpr uint32_t idesc = (1u << 4) | (4u << 17) | (8u << 24);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        // canonical K-major layout without swizzle: core matrices of 8 rows x 16 B,
+        // 128 B apart along K (LBO), 1024 B apart along N (SBO); version 1
+        const uint32_t sa = b_saddr + kk * 256;
+        const uint64_t desc = (uint64_t)((sa >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+                              (1ull << 46);
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
+            "r"(acol + kk * 8), "l"(desc), "r"(idesc), "r"((uint32_t)kk)
+            : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
@@ -305,21 +380,28 @@ __device__ __forceinline__ float hi16f(uint32_t w) { return __uint_as_float(prmt
 __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uint_as_float(prmt(w, 0x4B00u, sel)) - 8388608.0f; }
 
 #define LFE_FUSED_VARIANT(A, B, C, D, E)                                                   \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && !v.tc) \
         return launch_t<A, B, C, D, E>(fa, maps, err_flag, s);
 // peer-halo strips (lfe_extract_rows_peer): a separate instantiation, so that the
 // producer of every other launch is exactly the plain one
 #define LFE_FUSED_PEER_VARIANT(A, B, C)                                                    \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt && !v.stdi) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt && !v.stdi && !v.tc) \
         return launch_t<A, B, C, true, false, true>(fa, maps, err_flag, s);
 // device-resolved gap thresholds (adaptive lfe_extract, lfe_set_stats_device)
 #define LFE_FUSED_DEVT_VARIANT(A, B, C)                                                    \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi && !v.tc) \
         return launch_t<A, B, C, true, false, false, kTvNone, true>(fa, maps, err_flag, s);
 // std gate on the intensity image (b <= 10; gap test compiled in)
 #define LFE_FUSED_STDI_VARIANT(A, B, C)                                                    \
-    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && !v.devt && v.stdi) \
+    if (v.in16 == A && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && !v.devt && v.stdi && !v.tc) \
         return launch_t<A, B, C, true, false, false, kTvNone, false, true>(fa, maps, err_flag, s);
+// the LoG on the tensor cores (u16, b <= 11, fp16-exact masks; plain and DEVT)
+#define LFE_FUSED_TC_VARIANT(B, C, D, E)                                                       \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && v.tc) \
+        return launch_t<true, B, C, D, E, false, kTvNone, false, false, true>(fa, maps, err_flag, s);
+#define LFE_FUSED_TC_DEVT_VARIANT(B, C)                                                        \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi && v.tc) \
+        return launch_t<true, B, C, true, false, false, kTvNone, true, false, true>(fa, maps, err_flag, s);
 
 // ---- left/right image-edge fix-ups (border warps only) ----------------------
 struct Fix {
@@ -610,7 +692,7 @@ struct Producer {
 //   kTvInjectE (lfe_test_extract_e): the merged image is replaced by the input itself,
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
 template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
-          bool STDI = false>
+          bool STDI = false, bool TC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const __grid_constant__ Maps maps, const __grid_constant__ FusedArgs a, int *err_flag)
 {
@@ -656,16 +738,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         else return a.ung_top;
     };
 
+    // (TC) per group of 4 warps Q = warp / 4: "D half h of the next chunk ready" at
+    // tcbar[2Q + h]; the TMEM base address at byte 112 of the header; B after the rings
+    uint64_t *tcbar = full + 2 * kS;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 112);
+    unsigned char *tcB = ring + kS * kStageBytes + kWarps * warp_bytes(HML);
     const unsigned long long t_start = gtime();
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kWarps);
         }
+        if constexpr (TC)
+            for (int s = 0; s < 2 * (kWarps / 4); ++s) mbar_init(&tcbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.own)) : "memory");
     }
+    if constexpr (TC) {
+        if (warp == 0) {  // one CTA per SM: the whole TMEM
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        // B[n][k], n = (r row 0..3, branch, pixel), k = (patch row 0..7, patch column 0..7):
+        // q_branch(dy, dx) with dy = patch row - r row - 2, dx = patch column - pixel - 2
+        for (int e = threadIdx.x; e < 64 * 32; e += kThreads) {
+            const int n = e >> 6, k = e & 63;
+            const int dy = (k >> 3) - (n >> 3) - 2, dx = (k & 7) - (n & 3) - 2, br = (n >> 2) & 1;
+            const int ay = dy < 0 ? -dy : dy, ax = dx < 0 ? -dx : dx;
+            const int hi = ay > ax ? ay : ax, lo = ay > ax ? ax : ay;
+            float c = 0.0f;
+            if (hi <= 2) c = a.c[br][hi == 0 ? 0 : hi == 1 ? (lo == 0 ? 1 : 3) : (lo == 0 ? 2 : lo == 1 ? 4 : 5)];
+            *reinterpret_cast<__half *>(tcB + (n >> 3) * 1024 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) =
+                __float2half_rn(c);
+        }
+        // the ring starts zeroed: a slot no TMA has filled yet never holds fp16 NaN patterns
+        for (int o = threadIdx.x * 16; o < kS * kStageBytes; o += kThreads * 16)
+            *reinterpret_cast<uint4 *>(ring + o) = make_uint4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+    }
     __syncthreads();
+    uint32_t tl = 0, ta0 = 0, td0 = 0, tcc = 0;
+    if constexpr (TC) {
+        tc_fence_after();
+        // this warp's TMEM lanes (32 (warp % 4)) and its group's columns
+        tl = *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kTcCols);
+        ta0 = 0;   // A buffers at +0 / +48
+        td0 = 96;  // D at +96 (half h at +32 h)
+    }
 
     Producer<IN16, PEER, kHalo, kStageBytes, kBoxBytes, kBoxCols, kNBox> prod;
     prod.a = &a;
@@ -767,10 +887,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     // chunk, cb / pb = this lane's pixel 0 in the chunk's / the previous chunk's stage.
     // A row rho - c then sits in ring slot (k - c) & 7, read from its mirror at the
     // fixed index k + ((8 - c) & 7) or one 8 above -- always inside the 16 stored slots.
-    auto step = [&](auto fix_tag, int rho, float(&rB)[2][4], float(&rC)[2][4], int k, const unsigned char *cb,
-                    const unsigned char *pb) {
+    auto step = [&](auto fix_tag, auto even_tag, int rho, float(&rB)[2][4], float(&rC)[2][4], int k,
+                    const unsigned char *cb, const unsigned char *pb) {
         constexpr bool XF = decltype(fix_tag)::value & 1, YF = decltype(fix_tag)::value & 2;
         constexpr bool XQ = decltype(fix_tag)::value & 4;
+        // TC walks (interior and cheap column edges): r(rho-2) comes from TMEM, D row k
+        constexpr bool TCS = TC && !XF && !YF;
+        uint32_t tv[8];
+        if constexpr (TCS) {
+            if constexpr (decltype(even_tag)::value) {
+                if (k == 0 || k == 4) {  // D half k/4 of this chunk: issued by the group's MMA thread
+                    mbar_wait(&tcbar[2 * (warp >> 2) + (k >> 2)], tcc & 1);
+                    tc_fence_after();
+                }
+            }
+            tc_ld8(tl + td0 + 8 * k, tv);
+        }
         // XQ: cheap column edges (W % 4 == 0; chosen per CTA piece, so all warps of an SM
         // run the same code).  The lane holding column 0
         // (isL) / column W-1 at its pixel 3 (isR) substitutes its own edge values for the
@@ -943,8 +1075,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         // ---------------- input row ----------------
-        const unsigned char *rowp = YF ? row_ptr(prow(rho)) + off_own : cb + k * kRowBytes;
         float I[8];  // columns x0-2 .. x0+5
+        if constexpr (!TCS) {
+        const unsigned char *rowp = YF ? row_ptr(prow(rho)) + off_own : cb + k * kRowBytes;
         if constexpr (IN16) {
             const uint2 own = *reinterpret_cast<const uint2 *>(rowp);
             range_acc |= (own.x & chk_lo) | (own.y & chk_hi);
@@ -978,6 +1111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (XQ) I[1] = isL ? I[2] : I[1];
         if constexpr (XQ) I[6] = isR ? I[5] : I[6];
         if constexpr (XQ) I[7] = isR ? I[5] : I[7];
+        }  // !TCS
 
         // ---------------- intensity std window (STDI): rows rho-4 .. rho -> pass of row rho-2 ----------------
         if constexpr (STDI) {
@@ -1073,7 +1207,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         // ---------------- LoG x 2, streaming over rows ----------------
-        if constexpr (TV == kTvInjectR) {
+        if constexpr (TCS) {
+            tc_wait_ld(tv);
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) rC[j][i] = __uint_as_float(tv[4 * j + i]) * 16777216.0f;  // exact: D = r 2^-24
+        } else if constexpr (TV == kTvInjectR) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 rC[0][i] = I[i + 2] - 32768.0f;
@@ -1305,9 +1445,51 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     };
 
+    // ---- (TC) A of one chunk: this lane's 12 x 8 input patch into its TMEM lane ----
+    // Patch row ky = input row rho0 - 4 + ky (rho0 = the chunk's first row): rows 4..7
+    // of `prev` (the previous stage), then rows 0..7 of `cur`; columns x0-2 .. x0+5 as
+    // four u16 pairs (the neighbours' pairs by shuffle; the raw bits ARE the fp16
+    // operand).  The rows of `cur` take the range check (masks clo / chi).
+    auto tc_build = [&](auto xq_tag, const unsigned char *prev, const unsigned char *cur, uint32_t acol, uint32_t clo,
+                        uint32_t chi) {
+        constexpr bool XQ = decltype(xq_tag)::value;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            uint32_t r[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int ky = 4 * q + j;
+                const unsigned char *p = ky < 4 ? prev + (4 + ky) * kRowBytes : cur + (ky - 4) * kRowBytes;
+                const uint2 own = *reinterpret_cast<const uint2 *>(p);
+                if (ky >= 4) range_acc |= (own.x & clo) | (own.y & chi);
+                uint32_t L = __shfl_up_sync(0xffffffffu, own.y, 1), R = __shfl_down_sync(0xffffffffu, own.x, 1);
+                if constexpr (XQ) L = isL ? prmt(own.x, 0, 0x1010) : L;  // columns -2, -1 := column 0 (R5)
+                if constexpr (XQ) R = isR ? prmt(own.y, 0, 0x3232) : R;  // columns W, W+1 := column W-1
+                r[4 * j] = L;
+                r[4 * j + 1] = own.x;
+                r[4 * j + 2] = own.y;
+                r[4 * j + 3] = R;
+            }
+            tc_st16(tl + acol + 16 * q, r);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    };
+    // (TC) the group's 4 warps have written their A rows / read their D rows: one thread
+    // issues the MMA of D half h (A columns 16 h .. 16 h + 31 of buffer acol)
+    auto tc_issue = [&](int h, uint32_t acol) {
+        tc_fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + (warp >> 2)) : "memory");
+        tc_fence_after();
+        if ((warp & 3) == 0 && lane == 0)
+            tc_mma_half((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + 16 * h, smem_u32(tcB),
+                        &tcbar[2 * (warp >> 2) + h]);
+    };
+
     // ---- walk every row of the current item ---------------------------------
     auto walk = [&](auto fix_tag) {
         constexpr bool YF = decltype(fix_tag)::value & 2;
+        constexpr bool TCW = TC && !YF && !(decltype(fix_tag)::value & 1);
+        constexpr bool XQW = decltype(fix_tag)::value & 4;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -1338,6 +1520,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rho0 = YF ? it.ys - kHalo : it.plo;
         rho_first = rho0;
         optr = obase + (long long)(rho0 - kLag - it.ys) * a.out_pitch;
+        if constexpr (TCW) {
+            // first chunk (stage g_base, waited for by the item loop): its patch rows
+            // above the stage are warm-up only (r rows < plo + 2 never reach an output),
+            // so the stage itself stands in for them
+            const unsigned char *c0 = ring + (g_base % kS) * kStageBytes + off_own;
+            const uint32_t acol = ta0 + 48 * (tcc & 1);
+            tc_build(std::bool_constant<XQW>{}, c0, c0, acol, in_lo, in_hi);
+            tc_issue(0, acol);
+            tc_issue(1, acol);
+        }
         for (int rho = rho0; rho < rho_end; rho += kR) {
             // wait for the ring stages holding this chunk's input rows
             const int st = (prow(rho + kR - 1) - it.plo) >> 3;
@@ -1361,9 +1553,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // check.
                 if (m >= it.nst) chk_lo = chk_hi = 0;
             }
+            const bool tc_next = TCW && rho + kR < rho_end;  // (TC) a next chunk follows in this walk
             for (int k = 0; k < n; k += 2) {  // x2: the centre / new r rows swap roles without moves
-                step(fix_tag, rho + k, rX, rY, k, cb, pb);
-                step(fix_tag, rho + k + 1, rY, rX, k + 1, cb, pb);
+                step(fix_tag, std::true_type{}, rho + k, rX, rY, k, cb, pb);
+                step(fix_tag, std::false_type{}, rho + k + 1, rY, rX, k + 1, cb, pb);
+                if constexpr (TCW) {
+                    if (k == 2 && tc_next) {
+                        // D half 0 is read: A of the next chunk (stage m + 1, once it has
+                        // landed), then the MMA of its half 0
+                        const int m1 = ((rho - it.plo) >> 3) + 1;
+                        while (waited < m1 && waited < it.nst - 1) {
+                            ++waited;
+                            const uint32_t g = g_base + waited;
+                            mbar_wait(&full[g % kS], (g / kS) & 1);
+                        }
+                        const unsigned char *nb = ring + ((g_base + m1) % kS) * kStageBytes + off_own;
+                        const uint32_t acol = ta0 + 48 * ((tcc + 1) & 1);
+                        tc_build(std::bool_constant<XQW>{}, cb, nb, acol, m1 < it.nst ? in_lo : 0u,
+                                 m1 < it.nst ? in_hi : 0u);
+                        tc_issue(0, acol);
+                    }
+                }
+            }
+            if constexpr (TCW) {
+                if (tc_next) tc_issue(1, ta0 + 48 * ((tcc + 1) & 1));  // D half 1 is read too
+                ++tcc;
             }
             // release ring stages that no later step reads (the E stage reads row rho-6)
             const int next_e = prow(rho + n - 6);
@@ -1419,7 +1633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the instruction cache): 0 interior; 4 cheap column edges (W % 4 == 0); 3 general
         // fix-ups (edge rows, or column edges of other widths)
         const bool xedge_cta = (it.xo - kHaloX < 0 || it.xo - kHaloX + (kWarps - 1) * kWarpOut + 128 > W) && !a.dbg_nofix;
-        if (xw + kHaloX >= W) {
+        if (!TC && xw + kHaloX >= W) {
             // no output column of this warp is in the image (the last column group of a
             // width that is not a multiple of 1344): follow the ring without computing --
             // wait for each stage, then release it, in order (an early release would count
@@ -1467,13 +1681,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.dbg[6 * blockIdx.x + 4] = pr.u;
         a.dbg[6 * blockIdx.x + 5] = pr.u1;
     }
+    if constexpr (TC) {  // every issued MMA was waited for by its group
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
+    }
 }
 template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
-          bool STDI = false>
+          bool STDI = false, bool TC = false>
 cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI>;
-    constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0);
+    static_assert(!TC || (IN16 && !PEER && !STDI && TV == kTvNone), "TC: u16 plain / DEVT variants only");
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI, TC>;
+    constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0) + (TC ? (size_t)kTcB : 0);
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)
     // (std::call_once: distinct ctxs on distinct host threads may launch concurrently)

@@ -243,7 +243,7 @@ lfe_status run(lfe_ctx *c, const KParams &kp, const Geometry &g, cudaStream_t s)
     if (k == LFE_KERNEL_FUSED && !fused_ok)
         return fail(LFE_EUNSUPPORTED, "fused kernel does not support these parameters/alignment");
     cudaError_t e = k == LFE_KERNEL_FUSED
-                        ? launch_fused(kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s)
+                        ? launch_fused(kp, g, in16, c->cfg.log_unit, c->cfg.tile_h, c->d_err, s)
                         : launch_staged(kp, g, in16, c->cfg.tile_w, c->cfg.tile_h, c->d_err, s);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
     ++c->launches;
@@ -447,6 +447,10 @@ lfe_status lfe_set_option(lfe_ctx *c, int32_t key, int64_t value)
     case LFE_OPT_HOST_STRIP_ROWS:
         if (value < 1 || value > (1 << 20)) return fail(LFE_EINVAL, "bad strip rows");
         c->host_strip_rows = (int)value;
+        return LFE_OK;
+    case LFE_OPT_LOG_UNIT:
+        if (value < LFE_LOG_AUTO || value > LFE_LOG_CUDA_CORES) return fail(LFE_EINVAL, "bad LoG unit");
+        c->cfg.log_unit = (int)value;
         return LFE_OK;
     }
     return fail(LFE_EINVAL, "unknown option %d", key);

@@ -94,13 +94,14 @@ struct LaunchCfg {
     int kernel;   // LFE_KERNEL_*
     int tile_w;   // 0 = default
     int tile_h;
+    int log_unit;  // LFE_LOG_* (fused kernel: which unit computes the LoG)
 };
 
 // kernel launchers (return cudaGetLastError())
 cudaError_t launch_staged(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
                           int *err_flag, cudaStream_t s);
 // err_flag[0] = sticky ERANGE flag, err_flag[1] = scratch work counter (fused kernel)
-cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int tile_w, int tile_h,
+cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int log_unit, int tile_h,
                          int *err_flag, cudaStream_t s);
 bool fused_supports(const KParams &kp, int bit_depth);
 // lfe_signal: one thread stores `value` to *flag (st.release.sys)
@@ -131,7 +132,7 @@ struct lfe_ctx {
     int F[2];
     int device;
     int *d_err = nullptr;
-    lfe::LaunchCfg cfg{LFE_KERNEL_AUTO, 0, 0};
+    lfe::LaunchCfg cfg{LFE_KERNEL_AUTO, 0, 0, LFE_LOG_AUTO};
     int64_t launches = 0;
     // lfe_extract_host staging
     int host_strip_rows = 1024;

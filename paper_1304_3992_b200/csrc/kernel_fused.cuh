@@ -251,7 +251,7 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 // the integer mask coefficients are exact fp16 values (checked on the host), every
 // product is an exact multiple of 2^-24 and every partial sum stays below 2^24 units
 // (R3), which the fp32 accumulation keeps: D = r * 2^-24 exactly.
-constexpr int kTcB = 64 * 32 * 2;  // B: K = 64 (8 patch rows x 8 columns) x N = 32 (4 r rows x 2 branches x 4 pixels), fp16
+constexpr int kTcB = 64 * 32 * 2 + 64;  // B: K = 64 (8 patch rows x 8 columns) x N = 32 (4 r rows x 2 branches x 4 pixels), fp16; 6 counters
 constexpr int kTcCols = 160;       // TMEM columns per group of 4 warps: A x2 (48 each) + D (2 halves x 32)
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -334,29 +334,43 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b)
 // median of three packed pairs: min3 / max3, then the remaining element by XOR
 // (measured: the IADD3 form a + b + c - lo - hi, which moves the two LOP3 to the
 // FMA-lite pipe, is 0.5% slower on c3)
+// ADD (the TC variants): the remaining element as a + b + c - lo - hi instead, two
+// IADD3 on the FMA-side pipe; exact in packed u16x2 for any values (linear mod 2^32,
+// both halves of the result in [0, 2^16)).  With the LoG on the tensor cores the ALU
+// pipe is the busy one (ncu: ALU 66%, FMA 22%), so the mids move off it.
+template <bool ADD = false>
+__device__ __forceinline__ uint32_t mid3(uint32_t a, uint32_t b, uint32_t c, uint32_t lo, uint32_t hi)
+{
+    if constexpr (ADD) return a + b + c - lo - hi;
+    else return a ^ b ^ c ^ lo ^ hi;
+}
+
+template <bool ADD = false>
 __device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c)
 {
     uint32_t lo = vmin2(vmin2(a, b), c), hi = vmax2(vmax2(a, b), c);
-    return a ^ b ^ c ^ lo ^ hi;
+    return mid3<ADD>(a, b, c, lo, hi);
 }
 
 // median of nine: sort three triples, then med3(max of lows, med of mids, min of highs)
+template <bool ADD = false>
 __device__ __forceinline__ uint32_t med9(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t v4, uint32_t v5,
                                          uint32_t v6, uint32_t v7, uint32_t v8)
 {
-    uint32_t l0 = vmin2(vmin2(v0, v1), v2), h0 = vmax2(vmax2(v0, v1), v2), m0 = v0 ^ v1 ^ v2 ^ l0 ^ h0;
-    uint32_t l1 = vmin2(vmin2(v3, v4), v5), h1 = vmax2(vmax2(v3, v4), v5), m1 = v3 ^ v4 ^ v5 ^ l1 ^ h1;
-    uint32_t l2 = vmin2(vmin2(v6, v7), v8), h2 = vmax2(vmax2(v6, v7), v8), m2 = v6 ^ v7 ^ v8 ^ l2 ^ h2;
+    uint32_t l0 = vmin2(vmin2(v0, v1), v2), h0 = vmax2(vmax2(v0, v1), v2), m0 = mid3<ADD>(v0, v1, v2, l0, h0);
+    uint32_t l1 = vmin2(vmin2(v3, v4), v5), h1 = vmax2(vmax2(v3, v4), v5), m1 = mid3<ADD>(v3, v4, v5, l1, h1);
+    uint32_t l2 = vmin2(vmin2(v6, v7), v8), h2 = vmax2(vmax2(v6, v7), v8), m2 = mid3<ADD>(v6, v7, v8, l2, h2);
     uint32_t L = vmax2(vmax2(l0, l1), l2), Hh = vmin2(vmin2(h0, h1), h2);
-    return med3(L, med3(m0, m1, m2), Hh);
+    return med3<ADD>(L, med3<ADD>(m0, m1, m2), Hh);
 }
 
 // median of five: med3(max(min(a,b), min(c,d)), min(max(a,b), max(c,d)), e) -- the
 // larger of the two pair minima and the smaller of the two pair maxima bracket the
 // median of {a,b,c,d} with e (checked exhaustively on 5^5 inputs)
+template <bool ADD = false>
 __device__ __forceinline__ uint32_t med5(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e)
 {
-    return med3(vmax2(vmin2(a, b), vmin2(c, d)), vmin2(vmax2(a, b), vmax2(c, d)), e);
+    return med3<ADD>(vmax2(vmin2(a, b), vmin2(c, d)), vmin2(vmax2(a, b), vmax2(c, d)), e);
 }
 
 // pixel pair shifted by one: (a.hi, b.lo)
@@ -693,10 +707,16 @@ struct Producer {
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
 template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
           bool STDI = false, bool TC = false>
-__global__ void __launch_bounds__(kThreads, 1)
+#ifndef LFE_LB
+#define LFE_LB kThreads
+#endif
+__global__ void __launch_bounds__(LFE_LB, 1)
     fused_kernel(const __grid_constant__ Maps maps, const __grid_constant__ FusedArgs a, int *err_flag)
 {
     constexpr bool HM = HML >= 1, HM2 = HML == 2;
+    // packed-median mids by XOR (ALU) -- the IADD3 form measured no faster with the LoG on
+    // the tensor cores either (c3 0.8253 vs 0.8241 ms)
+    constexpr bool kAddMids = false;
     constexpr int kElem = IN16 ? 2 : 1;
     constexpr int kHalo = halo_of(HML);
     constexpr int kLag = HM2 ? 11 : HM ? 9 : 6;  // pipeline delay: output row = input row - kLag
@@ -771,6 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<__half *>(tcB + (n >> 3) * 1024 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) =
                 __float2half_rn(c);
         }
+        if (threadIdx.x < 6) reinterpret_cast<uint32_t *>(tcB + 64 * 32 * 2)[threadIdx.x] = 0;  // group x half counters
         // the ring starts zeroed: a slot no TMA has filled yet never holds fp16 NaN patterns
         for (int o = threadIdx.x * 16; o < kS * kStageBytes; o += kThreads * 16)
             *reinterpret_cast<uint4 *>(ring + o) = make_uint4(0, 0, 0, 0);
@@ -1033,13 +1054,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t s1a = sh1(E[1][0], E[1][1]), s1b = sh1(E[1][1], E[1][2]), s1c = sh1(E[1][2], E[1][3]);
             const uint32_t s3a = sh1(E[3][0], E[3][1]), s3b = sh1(E[3][1], E[3][2]), s3c = sh1(E[3][2], E[3][3]);
             const uint32_t c0 = E[2][1];
-            const uint32_t mp0 = med9(E[2][0], s2a, c0, s2b, E[2][2], E[0][1], E[1][1], E[3][1], E[4][1]);
-            const uint32_t mx0 = med9(E[0][0], s1a, s3b, E[4][2], E[0][2], s1b, s3a, E[4][0], c0);
-            o0 = med3(mp0, mx0, c0);
+            const uint32_t mp0 = med9<kAddMids>(E[2][0], s2a, c0, s2b, E[2][2], E[0][1], E[1][1], E[3][1], E[4][1]);
+            const uint32_t mx0 = med9<kAddMids>(E[0][0], s1a, s3b, E[4][2], E[0][2], s1b, s3a, E[4][0], c0);
+            o0 = med3<kAddMids>(mp0, mx0, c0);
             const uint32_t c1 = E[2][2];
-            const uint32_t mp1 = med9(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
-            const uint32_t mx1 = med9(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
-            o1 = med3(mp1, mx1, c1);
+            const uint32_t mp1 = med9<kAddMids>(E[2][1], s2b, c1, s2c, E[2][3], E[0][2], E[1][2], E[3][2], E[4][2]);
+            const uint32_t mx1 = med9<kAddMids>(E[0][1], s1b, s3c, E[4][3], E[0][3], s1c, s3b, E[4][1], c1);
+            o1 = med3<kAddMids>(mp1, mx1, c1);
             if constexpr (XF && HM2) fix_pairs(fx, o0, o1);  // replicate-pad the first level's output too
         }
 
@@ -1070,8 +1091,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t m01 = sh1(Hq[1][0], Hq[1][1]), m12 = sh1(Hq[1][1], Hq[1][2]), m23 = sh1(Hq[1][2], Hq[1][3]);
             const uint32_t d01 = sh1(Hq[2][0], Hq[2][1]), d12 = sh1(Hq[2][1], Hq[2][2]), d23 = sh1(Hq[2][2], Hq[2][3]);
             const uint32_t c0 = Hq[1][1], c1 = Hq[1][2];
-            q0 = med3(med5(m01, m12, Hq[0][1], Hq[2][1], c0), med5(u01, u12, d01, d12, c0), c0);
-            q1 = med3(med5(m12, m23, Hq[0][2], Hq[2][2], c1), med5(u12, u23, d12, d23, c1), c1);
+            q0 = med3<kAddMids>(med5<kAddMids>(m01, m12, Hq[0][1], Hq[2][1], c0), med5<kAddMids>(u01, u12, d01, d12, c0), c0);
+            q1 = med3<kAddMids>(med5<kAddMids>(m12, m23, Hq[0][2], Hq[2][2], c1), med5<kAddMids>(u12, u23, d12, d23, c1), c1);
         }
 
         // ---------------- input row ----------------
@@ -1476,13 +1497,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // (TC) the group's 4 warps have written their A rows / read their D rows: one thread
     // issues the MMA of D half h (A columns 16 h .. 16 h + 31 of buffer acol)
+    // The last of the 4 warps to get here issues it (an acq_rel counter per group and
+    // half: the release sequence of the other 3 warps' increments orders their
+    // tcgen05.st / ld before it), so no warp waits here.  Per half, because a warp can
+    // arrive for half 1 before the others arrived for half 0 (never for the next half 0:
+    // it first waits for this one's result).
     auto tc_issue = [&](int h, uint32_t acol) {
         tc_fence_before();
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + (warp >> 2)) : "memory");
-        tc_fence_after();
-        if ((warp & 3) == 0 && lane == 0)
-            tc_mma_half((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + 16 * h, smem_u32(tcB),
-                        &tcbar[2 * (warp >> 2) + h]);
+        __syncwarp();
+        if (lane == 0) {
+            uint32_t old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old)
+                         : "r"(smem_u32(tcB + 64 * 32 * 2 + 4 * (2 * (warp >> 2) + h)))
+                         : "memory");
+            if ((old & 3) == 3) {
+                tc_fence_after();
+                tc_mma_half((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + 16 * h, smem_u32(tcB),
+                            &tcbar[2 * (warp >> 2) + h]);
+            }
+        }
+        __syncwarp();
     };
 
     // ---- walk every row of the current item ---------------------------------

@@ -355,12 +355,13 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int lo
     if (v.stdi && (v.peer || v.devt)) return cudaErrorNotSupported;
     v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt || v.stdi;
     // the tensor-core LoG where it is exact and compiled (else the CUDA-core one)
-    v.tc = log_unit != LFE_LOG_CUDA_CORES && !v.peer && !v.stdi && tc_exact(kp, in16);
+    v.tc = log_unit != LFE_LOG_CUDA_CORES && !v.stdi && tc_exact(kp, in16);
     for (int pass = v.tc ? 0 : 1; pass < 2; ++pass) {
         v.tc = pass == 0;
         for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
                            fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7,
-                           fz::launch_group8, fz::launch_group9, fz::launch_group10}) {
+                           fz::launch_group8, fz::launch_group9, fz::launch_group10, fz::launch_group11,
+                           fz::launch_group12, fz::launch_group13}) {
             e = group(v, fa, maps, err_flag, s);
             if (e != cudaErrorNotSupported) return e;
         }

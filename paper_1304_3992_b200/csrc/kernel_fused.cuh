@@ -173,6 +173,9 @@ cudaError_t launch_group7(const Variant &, const FusedArgs &, const Maps &, int 
 cudaError_t launch_group8(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group9(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group10(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group11(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group12(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group13(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -416,6 +419,9 @@ __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uin
 #define LFE_FUSED_TC_DEVT_VARIANT(B, C)                                                        \
     if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi && v.tc) \
         return launch_t<true, B, C, true, false, false, kTvNone, true, false, true>(fa, maps, err_flag, s);
+#define LFE_FUSED_TC_PEER_VARIANT(B, C)                                                        \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt && !v.stdi && v.tc) \
+        return launch_t<true, B, C, true, false, true, kTvNone, false, false, true>(fa, maps, err_flag, s);
 
 // ---- left/right image-edge fix-ups (border warps only) ----------------------
 struct Fix {
@@ -759,10 +765,11 @@ __global__ void __launch_bounds__(LFE_LB, 1)
     };
 
     // (TC) per group of 4 warps Q = warp / 4: "D half h of the next chunk ready" at
-    // tcbar[2Q + h]; the TMEM base address at byte 112 of the header; B after the rings
+    // tcbar[2Q + h]; B after the rings, then the issue counters and the TMEM base address
     uint64_t *tcbar = full + 2 * kS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 112);
+    static_assert(kHdr >= 8 * (2 * kS + 2 * (kWarps / 4)), "mbarrier header");
     unsigned char *tcB = ring + kS * kStageBytes + kWarps * warp_bytes(HML);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tcB + 64 * 32 * 2 + 32);
     const unsigned long long t_start = gtime();
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
@@ -1726,7 +1733,7 @@ template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false
           bool STDI = false, bool TC = false>
 cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
-    static_assert(!TC || (IN16 && !PEER && !STDI && TV == kTvNone), "TC: u16 plain / DEVT variants only");
+    static_assert(!TC || (IN16 && !STDI && TV == kTvNone), "TC: u16 plain / DEVT / PEER variants only");
     auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI, TC>;
     constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0) + (TC ? (size_t)kTcB : 0);
     // the shared-memory attribute is per device: one-time setup for each device this

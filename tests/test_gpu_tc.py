@@ -1,0 +1,127 @@
+"""GPU parity of the fused kernel's tensor-core LoG (tcgen05) against
+the CPU oracle and against the same kernel with the LoG forced onto the CUDA cores
+(LFE_OPT_LOG_UNIT), bit for bit.
+
+The tensor-core path is exact when the u16 input bits read as fp16 equal v * 2^-24
+(v < 2048, b <= 11) and every mask coefficient is an fp16 value; the cases below
+cover every compiled TC variant family (median levels 0/1/2, extract / mask, with /
+without the gap test, the 3x3 re-check), the walks it takes (interior, cheap column
+edges, and the CUDA-core fallbacks inside the same kernel: edge rows and widths
+that are not a multiple of 4), the largest 11-bit values (the first fp16 binade and
+the largest partial sums R3 allows) and the piece / chunk boundaries of the MMA
+pipeline (rows per piece, 8-row chunks, 4-row MMA halves).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1304_3992_b200 import lfe, scenes
+from test_gpu_parity import _oparams, _pitched, assert_same
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    lfe.load()
+
+
+def run(img, p, log_unit=lfe.LFE_LOG_AUTO, seg=0):
+    with lfe.Context(p) as ctx:
+        ctx.set_option(lfe.LFE_OPT_KERNEL, lfe.LFE_KERNEL_FUSED)
+        ctx.set_option(lfe.LFE_OPT_LOG_UNIT, log_unit)
+        if seg:
+            ctx.set_option(lfe.LFE_OPT_TILE_H, seg)
+        tout = torch.uint8 if p.out_mode == lfe.LFE_OUT_MASK else torch.uint16
+        d = _pitched(img.shape, torch.uint16)
+        d.copy_(torch.from_numpy(np.ascontiguousarray(img)))
+        out = _pitched(img.shape, tout)
+        ctx.extract(d, out)
+        ctx.check()
+        return out.cpu().numpy()
+
+
+def _variants():
+    yield lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))                        # c3's variant
+    yield lfe.Params(bit_depth=10, zc_threshold=(0.0, 0.0))                          # no gap test
+    yield lfe.Params(bit_depth=11, zc_threshold=(0.01, 0.0), out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=9, hybrid_median=False, zc_threshold=(0.02, 0.01))
+    yield lfe.Params(bit_depth=10, hybrid_median=False, out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=10, median_window2=3, zc_threshold=(0.01, 0.01))      # two median levels
+    yield lfe.Params(bit_depth=11, median_window2=3, out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=10, std3_threshold=(0.4, 0.2), zc_threshold=(0.01, 0.0))  # 3x3 re-check
+    yield lfe.Params(bit_depth=10, std3_threshold=(0.3, 0.3), hybrid_median=False, out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=10, sigma=(1.0, 2.0), zc_threshold=(0.005, 0.02))   # other masks
+
+
+VARIANTS = list(_variants())
+# W % 4 == 0 widths take the cheap column-edge walk on the tensor cores, other widths
+# the general fix-up walk on the CUDA cores; 1344 = one CTA column group, 2700 three
+SHAPES = [(40, 64), (64, 124), (33, 1344), (70, 1348), (29, 2700), (120, 517), (9, 300), (200, 96)]
+
+
+@pytest.mark.parametrize("vi", range(len(VARIANTS)))
+def test_tc_equals_cuda_cores_and_oracle(vi):
+    p = VARIANTS[vi]
+    rng = np.random.default_rng(4200 + vi)
+    for (H, W), kind in itertools.product(SHAPES, ["mixed", "blocks"]):
+        img = scenes.random_image(rng, H, W, p.bit_depth, kind)
+        want = O.run(img, _oparams(p))
+        got = run(img, p)
+        assert_same(got, want, f"TC {H}x{W} {kind} {p}")
+        assert_same(run(img, p, lfe.LFE_LOG_CUDA_CORES), got, f"CUDA cores vs TC {H}x{W} {kind}")
+
+
+@pytest.mark.parametrize("kind", ["max", "binade", "checker", "ramp"])
+def test_tc_eleven_bit_extremes(kind):
+    """b = 11: the u16 bits 1024..2047 are fp16 normals of the first binade (still
+    v * 2^-24); the largest partial sums R3 admits (M * sum|q| < 2^24) come from
+    checkerboards of 0 and 2047 under the mask's sign pattern."""
+    H, W = 96, 1348
+    rng = np.random.default_rng(11)
+    y, x = np.mgrid[0:H, 0:W]
+    if kind == "max":
+        img = np.where(rng.random((H, W)) < 0.5, 2047, 0)
+    elif kind == "binade":
+        img = rng.integers(1024, 2048, (H, W))
+    elif kind == "checker":
+        img = np.where(((y // 2) + (x // 2)) % 2 == 0, 2047, 0)
+    else:
+        img = (x * 7 + y * 13) % 2048
+    img = img.astype(np.uint16)
+    for p in (lfe.Params(bit_depth=11, zc_threshold=(0.0, 0.0)),
+              lfe.Params(bit_depth=11, zc_threshold=(0.02, 0.02), median_window2=3)):
+        want = O.run(img, _oparams(p))
+        assert_same(run(img, p), want, f"{kind} {p}")
+
+
+@pytest.mark.parametrize("seg", [1, 3, 4, 5, 8, 9, 15, 16, 17, 100])
+def test_tc_piece_and_chunk_boundaries(seg):
+    """Pieces of every length around the 8-row chunk and the 4-row MMA half: the
+    prologue (first chunk), the mid-chunk issue and the last partial chunk."""
+    img = scenes.random_image(np.random.default_rng(77), 150, 2696, 10, "mixed")
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    assert_same(run(img, p, seg=seg), O.run(img, _oparams(p)), f"seg {seg}")
+
+
+def test_tc_c3_strip_equals_cuda_cores():
+    """The bench scene's recipe: 600 rows of c3 at full width, both LoG units."""
+    img = scenes.scene_c3(height=600)
+    p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
+    got = run(img, p)
+    assert_same(got, run(img, p, lfe.LFE_LOG_CUDA_CORES), "c3 strip")
+    assert_same(got, O.run(img, _oparams(p)), "c3 strip vs oracle")
+
+
+def test_log_unit_option_validation():
+    with lfe.Context(lfe.Params(bit_depth=10)) as ctx:
+        ctx.set_option(lfe.LFE_OPT_LOG_UNIT, lfe.LFE_LOG_CUDA_CORES)
+        ctx.set_option(lfe.LFE_OPT_LOG_UNIT, lfe.LFE_LOG_AUTO)
+        with pytest.raises(lfe.LfeError):
+            ctx.set_option(lfe.LFE_OPT_LOG_UNIT, 2)

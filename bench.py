@@ -160,7 +160,19 @@ def _backend_name():
     return "NCCL" if b == "nccl" else f"{b} (host-staged; ranks sharing a GPU: test hook, not a measurement)"
 
 
-def config_dict(name, cfg, world, p, graph=False, halo_mode=None):
+def log_unit_of(ctx, p, forced_cuda: bool) -> str:
+    """Which unit the fused kernel computes the two LoG responses on (the library's
+    rule, kernel_fused.cu tc_exact): the tensor cores when exact there -- u16 input with
+    b <= 11 and every mask coefficient an fp16 value -- else the CUDA cores."""
+    import numpy as np
+    qs = [ctx.mask(j)[0] for j in (0, 1)]
+    exact = all(np.all(np.float16(q).astype(np.float64) == q) for q in qs)
+    if not forced_cuda and 8 < p.bit_depth <= 11 and exact and p.std_source == 0:
+        return "tensor cores (tcgen05.mma kind::f16 into TMEM; exact: u16 bits = fp16 v*2^-24, fp16-exact integer masks)"
+    return "CUDA cores (exact-integer fp32 FFMA)"
+
+
+def config_dict(name, cfg, world, p, graph=False, halo_mode=None, log_unit=None):
     hm = "5x5 hybrid median" + (f" + {p.median_window2}x{p.median_window2} second level" if p.median_window2 else "")
     zc = (f"ZC (adaptive gap {p.zc_threshold[0]} x global std of r, statistics pre-pass)" if p.adaptive
           else f"ZC (gap {p.zc_threshold[0]})")
@@ -188,6 +200,7 @@ def config_dict(name, cfg, world, p, graph=False, halo_mode=None):
                     f" + OR + {hm}, extract",
         "name": name, "width": W, "height": H, "bit_depth": cfg["bit_depth"], "bands": B,
         "parallelism": par, "l2": l2,
+        **({"log_unit": log_unit} if log_unit else {}),
         "params": {"sigma": list(p.sigma), "log_size": list(p.log_size), "zc_threshold": list(p.zc_threshold),
                    "std_source": "zc" if p.std_source == 0 else "intensity", "std_window": p.std_window,
                    "std_threshold": list(p.std_threshold),
@@ -788,7 +801,8 @@ def main():
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": config_dict(name, cfg, world, p, graph=graph is not None, halo_mode=halo_mode),
+            "config": config_dict(name, cfg, world, p, graph=graph is not None, halo_mode=halo_mode,
+                                  log_unit=log_unit_of(ctx, p, args.log_unit == "cuda")),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel": "lfe fused stencil kernel (dominant launch: the interior band / all whole bands)"

@@ -1619,6 +1619,10 @@ __global__ void __launch_bounds__(LFE_LB, 1)
             }
             if constexpr (TCW) {
                 if (tc_next) tc_issue(1, ta0 + 48 * ((tcc + 1) & 1));  // D half 1 is read too
+                if (n <= 4) {  // (the last chunk) its half 1 was issued but no step read it: let it land
+                    mbar_wait(&tcbar[2 * (warp >> 2) + 1], tcc & 1);
+                    tc_fence_after();
+                }
                 ++tcc;
             }
             // release ring stages that no later step reads (the E stage reads row rho-6)

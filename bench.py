@@ -163,12 +163,13 @@ def _backend_name():
 def log_unit_of(ctx, p, forced_cuda: bool) -> str:
     """Which unit the fused kernel computes the two LoG responses on (the library's
     rule, kernel_fused.cu tc_exact): the tensor cores when exact there -- u16 input with
-    b <= 11 and every mask coefficient an fp16 value -- else the CUDA cores."""
+    b <= 12 and every mask coefficient an fp16 value -- else the CUDA cores."""
     import numpy as np
     qs = [ctx.mask(j)[0] for j in (0, 1)]
     exact = all(np.all(np.float16(q).astype(np.float64) == q) for q in qs)
-    if not forced_cuda and 8 < p.bit_depth <= 11 and exact and p.std_source == 0:
-        return "tensor cores (tcgen05.mma kind::f16 into TMEM; exact: u16 bits = fp16 v*2^-24, fp16-exact integer masks)"
+    if not forced_cuda and 8 < p.bit_depth <= 12 and exact and p.std_source == 0:
+        return ("tensor cores (tcgen05.mma kind::f16 into TMEM; exact: u16 bits = fp16 v*2^-24, fp16-exact integer masks"
+                + ("; b = 12: v & 0x7FF and bit 11 as two K halves)" if p.bit_depth == 12 else ")"))
     return "CUDA cores (exact-integer fp32 FFMA)"
 
 

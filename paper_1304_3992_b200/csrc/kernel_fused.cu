@@ -87,7 +87,7 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool pair
         // more working warps the per-row time stays near a full group's (10 warps: 0.97,
         // DESIGN.md 12), so those keep weight 1 (c5's 9-warp group at 0.75 cost +26%)
         const int nw = (fa.W - g * kCtaOut + kWarpOut - 1) / kWarpOut;
-        if (nw <= 2) f *= partial_floor();
+        if (nw <= 2 && !fa.idle_walk) f *= partial_floor();
         int ys = fa.o0 + r0;
         const int ye_all = ys + n;
         while (ys < ye_all) {  // the kernel's split at kEdge rows from the virtual top/bottom
@@ -152,11 +152,11 @@ void weighted_partition(FusedArgs &fa, int grid, int halo)
 // strips of a host stream) reuse it.  A small per-thread table keyed by
 // everything the partition depends on.
 struct PartKey {
-    int W, H, o0, o1, nbands, cap, grid, halo;
+    int W, H, o0, o1, nbands, cap, grid, halo, idle_walk;
     bool operator==(const PartKey &k) const
     {
         return W == k.W && H == k.H && o0 == k.o0 && o1 == k.o1 && nbands == k.nbands && cap == k.cap &&
-               grid == k.grid && halo == k.halo;
+               grid == k.grid && halo == k.halo && idle_walk == k.idle_walk;
     }
 };
 
@@ -170,7 +170,7 @@ void cached_partition(FusedArgs &fa, int grid, int halo)
     constexpr int kEntries = 8;
     static thread_local Entry table[kEntries];
     static thread_local int used = 0, next = 0;
-    const PartKey key{fa.W, fa.H, fa.o0, fa.o1, fa.nbands, fa.cap, grid, halo};
+    const PartKey key{fa.W, fa.H, fa.o0, fa.o1, fa.nbands, fa.cap, grid, halo, fa.idle_walk};
     for (int i = 0; i < used; ++i)
         if (table[i].key == key) {
             fa.nb = table[i].nb;
@@ -323,16 +323,17 @@ cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cu
 
 // The LoG on the tensor cores is exact when the u16 input bits read as fp16 are the
 // values themselves times 2^-24 (v < 2048: subnormals and the first binade) and every
-// mask coefficient is an fp16 value (scripts/tc_probe.cu).
-static bool tc_exact(const KParams &kp, bool in16)
+// mask coefficient is an fp16 value (scripts/tc_probe.cu).  b = 12
+// splits v into v & 0x7FF and bit 11 (TC12).  0: not exact, 1: TC, 2: TC12.
+static int tc_exact(const KParams &kp, bool in16)
 {
-    if (!in16 || kp.maxv > 2047) return false;
+    if (!in16 || kp.maxv > 4095) return 0;
     for (int j = 0; j < 2; ++j)
         for (int k = 0; k < 6; ++k) {
             const float c = (float)kp.orb[j][k];
-            if (std::fabs(c) > 65504.0f || __half2float(__float2half_rn(c)) != c) return false;
+            if (std::fabs(c) > 65504.0f || __half2float(__float2half_rn(c)) != c) return 0;
         }
-    return true;
+    return kp.maxv > 2047 ? 2 : 1;
 }
 
 cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int log_unit, int tile_h, int *err_flag,
@@ -355,13 +356,14 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int lo
     if (v.stdi && (v.peer || v.devt)) return cudaErrorNotSupported;
     v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt || v.stdi;
     // the tensor-core LoG where it is exact and compiled (else the CUDA-core one)
-    v.tc = log_unit != LFE_LOG_CUDA_CORES && !v.stdi && tc_exact(kp, in16);
-    for (int pass = v.tc ? 0 : 1; pass < 2; ++pass) {
+    const int tcx = log_unit != LFE_LOG_CUDA_CORES && !v.stdi ? tc_exact(kp, in16) : 0;
+    for (int pass = tcx ? 0 : 1; pass < 2; ++pass) {
         v.tc = pass == 0;
+        v.tc12 = pass == 0 && tcx == 2;
         for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
                            fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7,
                            fz::launch_group8, fz::launch_group9, fz::launch_group10, fz::launch_group11,
-                           fz::launch_group12, fz::launch_group13}) {
+                           fz::launch_group12, fz::launch_group13, fz::launch_group14}) {
             e = group(v, fa, maps, err_flag, s);
             if (e != cudaErrorNotSupported) return e;
         }

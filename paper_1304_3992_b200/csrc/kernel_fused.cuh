@@ -103,6 +103,7 @@ struct FusedArgs {
     long long out_pitch;
     unsigned long long *dbg;  // optional per-CTA [start, end, items] globaltimer record (LFE_DEBUG_TIMING)
     int dbg_nofix;            // timing experiments only: never take the column-fix path (wrong borders)
+    int idle_walk;            // partition: warps with no output column still walk the rows (TC, not TC12)
     // Peer-halo strips (lfe_extract_rows_peer): virtual rows [0, seg_a) are the rows
     // above (seg_base[0], pitch seg_pitch[0]), [seg_a, seg_b) the own rows (the tensor
     // map; own row = virtual row - seg_a; also seg_base[1]), [seg_b, H) the rows below
@@ -159,7 +160,8 @@ struct Variant {
     bool peer;  // peer-halo strip (halo rows in the neighbours' memory)
     bool devt;  // gap thresholds read from device memory (resolved on the device)
     bool stdi;  // std gate on the intensity image (b <= 10)
-    bool tc;    // LoG on the tensor cores (u16, b <= 11, fp16-exact masks)
+    bool tc;    // LoG on the tensor cores (u16, b <= 12, fp16-exact masks)
+    bool tc12;  // ... with the input split into its low 11 bits and bit 11 (b = 12)
 };
 using GroupFn = cudaError_t (*)(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group0(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
@@ -176,6 +178,7 @@ cudaError_t launch_group10(const Variant &, const FusedArgs &, const Maps &, int
 cudaError_t launch_group11(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group12(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group13(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group14(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -254,7 +257,11 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 // the integer mask coefficients are exact fp16 values (checked on the host), every
 // product is an exact multiple of 2^-24 and every partial sum stays below 2^24 units
 // (R3), which the fp32 accumulation keeps: D = r * 2^-24 exactly.
-constexpr int kTcB = 64 * 32 * 2 + 64;  // B: K = 64 (8 patch rows x 8 columns) x N = 32 (4 r rows x 2 branches x 4 pixels), fp16; 6 counters
+// B: K = 64 (8 patch rows x 8 columns) x N = 32 (4 r rows x 2 branches x 4 pixels), fp16
+// (TC12: K = 128, every patch row twice: its low 11 bits, then its bit 11), then the
+// 6 issue counters and the TMEM base address
+template <bool TC12> __host__ __device__ constexpr int tc_b_bytes() { return (TC12 ? 128 : 64) * 32 * 2; }
+template <bool TC12> __host__ __device__ constexpr int tc_smem() { return tc_b_bytes<TC12>() + 64; }
 constexpr int kTcCols = 160;       // TMEM columns per group of 4 warps: A x2 (48 each) + D (2 halves x 32)
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -291,17 +298,21 @@ __device__ __forceinline__ void tc_wait_ld(uint32_t (&v)[8])
 }
 
 // D[dcol .. +32) (= 4 r rows) from A columns [acol, acol + 32) (= 8 patch rows) and B:
-// four K = 16 steps, then a commit to `bar` (one elected thread)
+// four K = 16 steps (TC12: eight, one patch row each, over A columns [acol, acol + 64)),
+// then a commit to `bar` (one elected thread)
+template <bool TC12>
 __device__ __forceinline__ void tc_mma_half(uint32_t dcol, uint32_t acol, uint32_t b_saddr, uint64_t *bar)
 {
     // kind::f16: A = B = F16, D = F32, both K-major, N = 32 (>> 3), M = 128 (>> 4)
     constexpr uint32_t idesc = (1u << 4) | (4u << 17) | (8u << 24);
+    constexpr int kSteps = TC12 ? 8 : 4;
+    constexpr uint32_t kSbo = 128 * 2 * kSteps;  // one 8-row group of B along N: every K core matrix
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
+    for (int kk = 0; kk < kSteps; ++kk) {
         // canonical K-major layout without swizzle: core matrices of 8 rows x 16 B,
-        // 128 B apart along K (LBO), 1024 B apart along N (SBO); version 1
+        // 128 B apart along K (LBO), kSbo apart along N (SBO); version 1
         const uint32_t sa = b_saddr + kk * 256;
-        const uint64_t desc = (uint64_t)((sa >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+        const uint64_t desc = (uint64_t)((sa >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(kSbo >> 4) << 32) |
                               (1ull << 46);
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -414,13 +425,17 @@ __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uin
         return launch_t<A, B, C, true, false, false, kTvNone, false, true>(fa, maps, err_flag, s);
 // the LoG on the tensor cores (u16, b <= 11, fp16-exact masks; plain and DEVT)
 #define LFE_FUSED_TC_VARIANT(B, C, D, E)                                                       \
-    if (v.in16 && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && v.tc) \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && v.tc && !v.tc12) \
         return launch_t<true, B, C, D, E, false, kTvNone, false, false, true>(fa, maps, err_flag, s);
 #define LFE_FUSED_TC_DEVT_VARIANT(B, C)                                                        \
-    if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi && v.tc) \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi && v.tc && !v.tc12) \
         return launch_t<true, B, C, true, false, false, kTvNone, true, false, true>(fa, maps, err_flag, s);
+// b = 12 (u16): the patch split into its low 11 bits and bit 11 (TC12)
+#define LFE_FUSED_TC12_VARIANT(B, C, D, E)                                                     \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && v.tc && v.tc12) \
+        return launch_t<true, B, C, D, E, false, kTvNone, false, false, true, true>(fa, maps, err_flag, s);
 #define LFE_FUSED_TC_PEER_VARIANT(B, C)                                                        \
-    if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt && !v.stdi && v.tc) \
+    if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && v.peer && !v.devt && !v.stdi && v.tc && !v.tc12) \
         return launch_t<true, B, C, true, false, true, kTvNone, false, false, true>(fa, maps, err_flag, s);
 
 // ---- left/right image-edge fix-ups (border warps only) ----------------------
@@ -712,7 +727,7 @@ struct Producer {
 //   kTvInjectE (lfe_test_extract_e): the merged image is replaced by the input itself,
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
 template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
-          bool STDI = false, bool TC = false>
+          bool STDI = false, bool TC = false, bool TC12 = false>
 #ifndef LFE_LB
 #define LFE_LB kThreads
 #endif
@@ -769,7 +784,8 @@ __global__ void __launch_bounds__(LFE_LB, 1)
     uint64_t *tcbar = full + 2 * kS;
     static_assert(kHdr >= 8 * (2 * kS + 2 * (kWarps / 4)), "mbarrier header");
     unsigned char *tcB = ring + kS * kStageBytes + kWarps * warp_bytes(HML);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tcB + 64 * 32 * 2 + 32);
+    constexpr int kBB = tc_b_bytes<TC12>();  // B bytes; the counters and the TMEM base follow
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tcB + kBB + 32);
     const unsigned long long t_start = gtime();
     if (threadIdx.x == 0) {
         for (int s = 0; s < kS; ++s) {
@@ -786,19 +802,22 @@ __global__ void __launch_bounds__(LFE_LB, 1)
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }
-        // B[n][k], n = (r row 0..3, branch, pixel), k = (patch row 0..7, patch column 0..7):
+        // B[n][k], n = (r row 0..3, branch, pixel), k = (patch row 0..7, patch column 0..7)
+        // (TC12: k = (patch row, part, patch column), both parts the same weights):
         // q_branch(dy, dx) with dy = patch row - r row - 2, dx = patch column - pixel - 2
-        for (int e = threadIdx.x; e < 64 * 32; e += kThreads) {
-            const int n = e >> 6, k = e & 63;
-            const int dy = (k >> 3) - (n >> 3) - 2, dx = (k & 7) - (n & 3) - 2, br = (n >> 2) & 1;
+        constexpr int kK = TC12 ? 128 : 64;
+        for (int e = threadIdx.x; e < kK * 32; e += kThreads) {
+            const int n = e / kK, k = e % kK;
+            const int prow_k = TC12 ? k >> 4 : k >> 3;
+            const int dy = prow_k - (n >> 3) - 2, dx = (k & 7) - (n & 3) - 2, br = (n >> 2) & 1;
             const int ay = dy < 0 ? -dy : dy, ax = dx < 0 ? -dx : dx;
             const int hi = ay > ax ? ay : ax, lo = ay > ax ? ax : ay;
             float c = 0.0f;
             if (hi <= 2) c = a.c[br][hi == 0 ? 0 : hi == 1 ? (lo == 0 ? 1 : 3) : (lo == 0 ? 2 : lo == 1 ? 4 : 5)];
-            *reinterpret_cast<__half *>(tcB + (n >> 3) * 1024 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) =
+            *reinterpret_cast<__half *>(tcB + (n >> 3) * (kK / 8) * 128 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) =
                 __float2half_rn(c);
         }
-        if (threadIdx.x < 6) reinterpret_cast<uint32_t *>(tcB + 64 * 32 * 2)[threadIdx.x] = 0;  // group x half counters
+        if (threadIdx.x < 6) reinterpret_cast<uint32_t *>(tcB + kBB)[threadIdx.x] = 0;  // group x half counters
         // the ring starts zeroed: a slot no TMA has filled yet never holds fp16 NaN patterns
         for (int o = threadIdx.x * 16; o < kS * kStageBytes; o += kThreads * 16)
             *reinterpret_cast<uint4 *>(ring + o) = make_uint4(0, 0, 0, 0);
@@ -811,7 +830,7 @@ __global__ void __launch_bounds__(LFE_LB, 1)
         tc_fence_after();
         // this warp's TMEM lanes (32 (warp % 4)) and its group's columns
         tl = *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kTcCols);
-        ta0 = 0;   // A buffers at +0 / +48
+        ta0 = 0;   // A buffers at +0 / +48 (TC12: one buffer of 12 patch rows x 8 columns)
         td0 = 96;  // D at +96 (half h at +32 h)
     }
 
@@ -1478,25 +1497,40 @@ __global__ void __launch_bounds__(LFE_LB, 1)
     // of `prev` (the previous stage), then rows 0..7 of `cur`; columns x0-2 .. x0+5 as
     // four u16 pairs (the neighbours' pairs by shuffle; the raw bits ARE the fp16
     // operand).  The rows of `cur` take the range check (masks clo / chi).
+    // TC12 (b = 12): every patch row as 8 columns, its low 11 bits (the exact fp16
+    // v * 2^-24 of v & 0x7FF) and its bit 11 alone (0x0800 = the fp16 2^-13 = 2048 * 2^-24):
+    // the two parts' products with the same weights sum to q * v * 2^-24 exactly.
     auto tc_build = [&](auto xq_tag, const unsigned char *prev, const unsigned char *cur, uint32_t acol, uint32_t clo,
                         uint32_t chi) {
         constexpr bool XQ = decltype(xq_tag)::value;
+        constexpr int kRowsPerSt = TC12 ? 2 : 4;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 12 / kRowsPerSt; ++q) {
             uint32_t r[16];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int ky = 4 * q + j;
+            for (int j = 0; j < kRowsPerSt; ++j) {
+                const int ky = kRowsPerSt * q + j;
                 const unsigned char *p = ky < 4 ? prev + (4 + ky) * kRowBytes : cur + (ky - 4) * kRowBytes;
                 const uint2 own = *reinterpret_cast<const uint2 *>(p);
                 if (ky >= 4) range_acc |= (own.x & clo) | (own.y & chi);
                 uint32_t L = __shfl_up_sync(0xffffffffu, own.y, 1), R = __shfl_down_sync(0xffffffffu, own.x, 1);
                 if constexpr (XQ) L = isL ? prmt(own.x, 0, 0x1010) : L;  // columns -2, -1 := column 0 (R5)
                 if constexpr (XQ) R = isR ? prmt(own.y, 0, 0x3232) : R;  // columns W, W+1 := column W-1
-                r[4 * j] = L;
-                r[4 * j + 1] = own.x;
-                r[4 * j + 2] = own.y;
-                r[4 * j + 3] = R;
+                if constexpr (TC12) {
+                    r[8 * j] = L & 0x07FF07FFu;
+                    r[8 * j + 1] = own.x & 0x07FF07FFu;
+                    r[8 * j + 2] = own.y & 0x07FF07FFu;
+                    r[8 * j + 3] = R & 0x07FF07FFu;
+                    r[8 * j + 4] = L & 0x08000800u;
+                    r[8 * j + 5] = own.x & 0x08000800u;
+                    r[8 * j + 6] = own.y & 0x08000800u;
+                    r[8 * j + 7] = R & 0x08000800u;
+                } else {
+                    r[4 * j] = L;
+                    r[4 * j + 1] = own.x;
+                    r[4 * j + 2] = own.y;
+                    r[4 * j + 3] = R;
+                }
             }
             tc_st16(tl + acol + 16 * q, r);
         }
@@ -1516,11 +1550,11 @@ __global__ void __launch_bounds__(LFE_LB, 1)
             uint32_t old;
             asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                          : "=r"(old)
-                         : "r"(smem_u32(tcB + 64 * 32 * 2 + 4 * (2 * (warp >> 2) + h)))
+                         : "r"(smem_u32(tcB + kBB + 4 * (2 * (warp >> 2) + h)))
                          : "memory");
             if ((old & 3) == 3) {
                 tc_fence_after();
-                tc_mma_half((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + 16 * h, smem_u32(tcB),
+                tc_mma_half<TC12>((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + (TC12 ? 32 : 16) * h, smem_u32(tcB),
                             &tcbar[2 * (warp >> 2) + h]);
             }
         }
@@ -1567,7 +1601,7 @@ __global__ void __launch_bounds__(LFE_LB, 1)
             // above the stage are warm-up only (r rows < plo + 2 never reach an output),
             // so the stage itself stands in for them
             const unsigned char *c0 = ring + (g_base % kS) * kStageBytes + off_own;
-            const uint32_t acol = ta0 + 48 * (tcc & 1);
+            const uint32_t acol = TC12 ? ta0 : ta0 + 48 * (tcc & 1);
             tc_build(std::bool_constant<XQW>{}, c0, c0, acol, in_lo, in_hi);
             tc_issue(0, acol);
             tc_issue(1, acol);
@@ -1610,7 +1644,11 @@ __global__ void __launch_bounds__(LFE_LB, 1)
                             mbar_wait(&full[g % kS], (g / kS) & 1);
                         }
                         const unsigned char *nb = ring + ((g_base + m1) % kS) * kStageBytes + off_own;
-                        const uint32_t acol = ta0 + 48 * ((tcc + 1) & 1);
+                        const uint32_t acol = TC12 ? ta0 : ta0 + 48 * ((tcc + 1) & 1);
+                        if constexpr (TC12) {  // one A buffer: this chunk's half-1 MMA still reads it
+                            mbar_wait(&tcbar[2 * (warp >> 2) + 1], tcc & 1);
+                            tc_fence_after();
+                        }
                         tc_build(std::bool_constant<XQW>{}, cb, nb, acol, m1 < it.nst ? in_lo : 0u,
                                  m1 < it.nst ? in_hi : 0u);
                         tc_issue(0, acol);
@@ -1618,7 +1656,7 @@ __global__ void __launch_bounds__(LFE_LB, 1)
                 }
             }
             if constexpr (TCW) {
-                if (tc_next) tc_issue(1, ta0 + 48 * ((tcc + 1) & 1));  // D half 1 is read too
+                if (tc_next) tc_issue(1, TC12 ? ta0 : ta0 + 48 * ((tcc + 1) & 1));  // D half 1 is read too
                 if (n <= 4) {  // (the last chunk) its half 1 was issued but no step read it: let it land
                     mbar_wait(&tcbar[2 * (warp >> 2) + 1], tcc & 1);
                     tc_fence_after();
@@ -1626,6 +1664,51 @@ __global__ void __launch_bounds__(LFE_LB, 1)
                 ++tcc;
             }
             // release ring stages that no later step reads (the E stage reads row rho-6)
+            const int next_e = prow(rho + n - 6);
+            __syncwarp();
+            while (released < it.nst && it.plo + (released + 1) * kR <= next_e) {
+                if (lane == 0) mbar_arrive(&empty[(g_base + released) % kS]);
+                ++released;
+                ++rel_w;
+            }
+            if (threadIdx.x == kProdThread) prod.run(rel_w);
+            __syncwarp();
+        }
+    };
+
+    // ---- (TC) a warp with no output column in the image, in a tensor-core walk ----
+    // It follows the ring (wait for each stage, release it in order) and keeps the group's
+    // MMA protocol -- its arrivals, each after the wait for that half's previous MMA, in
+    // the walk's order -- without computing anything: its TMEM lanes' A and D rows are
+    // never read (an MMA's row m depends on A row m only).
+    // (TC12 kernels only: the 11-bit TC kernels walk such warps like the others -- see
+    // launch_t -- which keeps this code out of the c3 kernel)
+    auto tc_shadow = [&]() {
+        const int rho_end = it.ye + kLag;
+        tc_issue(0, TC12 ? ta0 : ta0 + 48 * (tcc & 1));
+        tc_issue(1, TC12 ? ta0 : ta0 + 48 * (tcc & 1));
+        for (int rho = it.plo; rho < rho_end; rho += kR) {
+            const int st = (prow(rho + kR - 1) - it.plo) >> 3;
+            while (waited < st) {
+                ++waited;
+                const uint32_t g = g_base + waited;
+                mbar_wait(&full[g % kS], (g / kS) & 1);
+            }
+            const int n = min(kR, rho_end - rho);
+            const bool tc_next = rho + kR < rho_end;
+            mbar_wait(&tcbar[2 * (warp >> 2)], tcc & 1);  // as step 0
+            tc_fence_after();
+            if (n > 2) {
+                if constexpr (TC12) {  // as the midpoint's wait before its A build
+                    mbar_wait(&tcbar[2 * (warp >> 2) + 1], tcc & 1);
+                    tc_fence_after();
+                }
+                if (tc_next) tc_issue(0, TC12 ? ta0 : ta0 + 48 * ((tcc + 1) & 1));
+            }
+            mbar_wait(&tcbar[2 * (warp >> 2) + 1], tcc & 1);  // as step 4 (or the last chunk's wait)
+            tc_fence_after();
+            if (tc_next) tc_issue(1, TC12 ? ta0 : ta0 + 48 * ((tcc + 1) & 1));
+            ++tcc;
             const int next_e = prow(rho + n - 6);
             __syncwarp();
             while (released < it.nst && it.plo + (released + 1) * kR <= next_e) {
@@ -1679,7 +1762,12 @@ __global__ void __launch_bounds__(LFE_LB, 1)
         // the instruction cache): 0 interior; 4 cheap column edges (W % 4 == 0); 3 general
         // fix-ups (edge rows, or column edges of other widths)
         const bool xedge_cta = (it.xo - kHaloX < 0 || it.xo - kHaloX + (kWarps - 1) * kWarpOut + 128 > W) && !a.dbg_nofix;
-        if (!TC && xw + kHaloX >= W) {
+        const bool yf_item = it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge_cta && (W & 3));
+        bool shadow = false;
+        if constexpr (TC12) shadow = xw + kHaloX >= W && !yf_item;
+        if (shadow) {
+            tc_shadow();
+        } else if (!(TC && !TC12) && xw + kHaloX >= W) {
             // no output column of this warp is in the image (the last column group of a
             // width that is not a multiple of 1344): follow the ring without computing --
             // wait for each stage, then release it, in order (an early release would count
@@ -1693,7 +1781,7 @@ __global__ void __launch_bounds__(LFE_LB, 1)
                 ++rel_w;
             }
             released = it.nst;
-        } else if (it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge_cta && (W & 3))) {
+        } else if (yf_item) {
             isL = isR = false;
             walk(std::integral_constant<int, 3>{});
         } else if (xedge_cta) {
@@ -1734,12 +1822,13 @@ __global__ void __launch_bounds__(LFE_LB, 1)
     }
 }
 template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
-          bool STDI = false, bool TC = false>
+          bool STDI = false, bool TC = false, bool TC12 = false>
 cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
     static_assert(!TC || (IN16 && !STDI && TV == kTvNone), "TC: u16 plain / DEVT / PEER variants only");
-    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI, TC>;
-    constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0) + (TC ? (size_t)kTcB : 0);
+    static_assert(!TC12 || TC, "TC12 is a TC variant");
+    auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI, TC, TC12>;
+    constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0) + (TC ? (size_t)tc_smem<TC12>() : 0);
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)
     // (std::call_once: distinct ctxs on distinct host threads may launch concurrently)
@@ -1761,6 +1850,10 @@ cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaS
     const int grid = units < grid_cap ? (int)units : grid_cap;
     cudaError_t e = cudaSuccess;
     FusedArgs fw = fa;
+    // The 11-bit TC kernels walk warps with no output column like the others (their MMA
+    // protocol needs the group's 4 warps; a shadow walk would add ~1.4 k instructions to
+    // the c3 kernel, measured 2.6% slower); TC12 and the CUDA-core kernels shadow / skip them
+    fw.idle_walk = TC && !TC12;
     cached_partition(fw, grid, halo_of(HML));
     static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
     FusedArgs fb = fw;

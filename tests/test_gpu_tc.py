@@ -3,12 +3,13 @@ the CPU oracle and against the same kernel with the LoG forced onto the CUDA cor
 (LFE_OPT_LOG_UNIT), bit for bit.
 
 The tensor-core path is exact when the u16 input bits read as fp16 equal v * 2^-24
-(v < 2048, b <= 11) and every mask coefficient is an fp16 value; the cases below
+(v < 2048, b <= 11; b = 12 splits v into v & 0x7FF and bit 11) and every mask
+coefficient is an fp16 value; the cases below
 cover every compiled TC variant family (median levels 0/1/2, extract / mask, with /
 without the gap test, the 3x3 re-check), the walks it takes (interior, cheap column
 edges, and the CUDA-core fallbacks inside the same kernel: edge rows and widths
-that are not a multiple of 4), the largest 11-bit values (the first fp16 binade and
-the largest partial sums R3 allows) and the piece / chunk boundaries of the MMA
+that are not a multiple of 4), the largest 11- and 12-bit values (the first fp16
+binade, bit 11, and the largest partial sums R3 allows) and the piece / chunk boundaries of the MMA
 pipeline (rows per piece, 8-row chunks, 4-row MMA halves).
 """
 import itertools
@@ -58,6 +59,12 @@ def _variants():
     yield lfe.Params(bit_depth=10, std3_threshold=(0.4, 0.2), zc_threshold=(0.01, 0.0))  # 3x3 re-check
     yield lfe.Params(bit_depth=10, std3_threshold=(0.3, 0.3), hybrid_median=False, out_mode=lfe.LFE_OUT_MASK)
     yield lfe.Params(bit_depth=10, sigma=(1.0, 2.0), zc_threshold=(0.005, 0.02))   # other masks
+    # b = 12 (c4): the patch split into its low 11 bits and bit 11 (TC12)
+    yield lfe.Params(bit_depth=12, zc_threshold=(0.02, 0.02))
+    yield lfe.Params(bit_depth=12, zc_threshold=(0.0, 0.0), out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=12, median_window2=3, zc_threshold=(0.01, 0.01))
+    yield lfe.Params(bit_depth=12, std3_threshold=(0.4, 0.2), zc_threshold=(0.01, 0.0))
+    yield lfe.Params(bit_depth=12, hybrid_median=False, zc_threshold=(0.02, 0.0))
 
 
 VARIANTS = list(_variants())
@@ -78,25 +85,28 @@ def test_tc_equals_cuda_cores_and_oracle(vi):
         assert_same(run(img, p, lfe.LFE_LOG_CUDA_CORES), got, f"CUDA cores vs TC {H}x{W} {kind}")
 
 
+@pytest.mark.parametrize("bd", [11, 12])
 @pytest.mark.parametrize("kind", ["max", "binade", "checker", "ramp"])
-def test_tc_eleven_bit_extremes(kind):
+def test_tc_bit_depth_extremes(kind, bd):
     """b = 11: the u16 bits 1024..2047 are fp16 normals of the first binade (still
-    v * 2^-24); the largest partial sums R3 admits (M * sum|q| < 2^24) come from
-    checkerboards of 0 and 2047 under the mask's sign pattern."""
+    v * 2^-24); b = 12: values 2048..4095 take the bit-11 part (TC12); the largest
+    partial sums R3 admits (M * sum|q| < 2^24) come from checkerboards of 0 and the
+    maximum under the mask's sign pattern."""
     H, W = 96, 1348
     rng = np.random.default_rng(11)
     y, x = np.mgrid[0:H, 0:W]
+    M = (1 << bd) - 1
     if kind == "max":
-        img = np.where(rng.random((H, W)) < 0.5, 2047, 0)
+        img = np.where(rng.random((H, W)) < 0.5, M, 0)
     elif kind == "binade":
-        img = rng.integers(1024, 2048, (H, W))
+        img = rng.integers((M + 1) // 2, M + 1, (H, W))
     elif kind == "checker":
-        img = np.where(((y // 2) + (x // 2)) % 2 == 0, 2047, 0)
+        img = np.where(((y // 2) + (x // 2)) % 2 == 0, M, 0)
     else:
-        img = (x * 7 + y * 13) % 2048
+        img = (x * 7 + y * 13) % (M + 1)
     img = img.astype(np.uint16)
-    for p in (lfe.Params(bit_depth=11, zc_threshold=(0.0, 0.0)),
-              lfe.Params(bit_depth=11, zc_threshold=(0.02, 0.02), median_window2=3)):
+    for p in (lfe.Params(bit_depth=bd, zc_threshold=(0.0, 0.0)),
+              lfe.Params(bit_depth=bd, zc_threshold=(0.02, 0.02), median_window2=3)):
         want = O.run(img, _oparams(p))
         assert_same(run(img, p), want, f"{kind} {p}")
 
@@ -108,6 +118,25 @@ def test_tc_piece_and_chunk_boundaries(seg):
     img = scenes.random_image(np.random.default_rng(77), 150, 2696, 10, "mixed")
     p = lfe.Params(bit_depth=10, zc_threshold=(0.02, 0.02))
     assert_same(run(img, p, seg=seg), O.run(img, _oparams(p)), f"seg {seg}")
+
+
+def test_tc12_c4_bands_equal_cuda_cores():
+    """c4's recipe (b = 12 multispectral bands) at 2048^2, every band, both LoG units."""
+    img = scenes.scene_c4(size=2048)
+    p = lfe.Params(bit_depth=12, zc_threshold=(0.02, 0.02))
+    for b in range(img.shape[0]):
+        got = run(img[b], p)
+        assert_same(got, run(img[b], p, lfe.LFE_LOG_CUDA_CORES), f"c4 band {b}")
+        assert_same(got, O.run(img[b], _oparams(p)), f"c4 band {b} vs oracle")
+
+
+def test_tc12_wide_strip_equals_oracle():
+    """A 500-row strip of c4's width (8192 = 6.1 column groups) of random 12-bit data."""
+    img = scenes.random_image(np.random.default_rng(12), 500, 8192, 12, "mixed")
+    p = lfe.Params(bit_depth=12, zc_threshold=(0.02, 0.02))
+    got = run(img, p)
+    assert_same(got, run(img, p, lfe.LFE_LOG_CUDA_CORES), "b12 strip")
+    assert_same(got, O.run(img, _oparams(p)), "b12 strip vs oracle")
 
 
 def test_tc_c3_strip_equals_cuda_cores():

@@ -242,8 +242,8 @@ typedef struct lfe_stats {
     int64_t r_sum[2];    /* sum r_j                           */
     int64_t r_sq_hi[2];  /* sum of (partial sum r_j^2) >> 24  */
     int64_t r_sq_lo[2];  /* sum of (partial sum r_j^2) mod 2^24 */
-    int64_t i_sum;       /* sum I                             */
-    int64_t i_sq;        /* sum I^2                           */
+    int64_t i_sum;       /* sum I   (only for a ctx with LFE_ADAPT_STD, R22: else 0 is added) */
+    int64_t i_sq;        /* sum I^2 (ditto)                                              */
 } lfe_stats;
 
 /* Adds the statistics of the OWNED rows of a strip to *d_stats (DEVICE memory,

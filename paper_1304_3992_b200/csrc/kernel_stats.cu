@@ -44,7 +44,7 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v)
 // output rows.  Every value is an exact int32 (|r| < 2^24, R3).
 template <typename Tin, int R>
 __global__ void __launch_bounds__(kThreads)
-    stats_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, lfe_stats *out)
+    stats_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, lfe_stats *out, bool need_i)
 {
     __shared__ uint16_t sI[(kTileH + 2 * kMaxR) * (kTileW + 2 * kMaxR)];
     __shared__ unsigned long long red[kThreads / 32][9];
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kThreads)
         lo1 += u1 & 0xFFFFFFull;
         is += ti;
     }
+    if (!need_i) is = 0, iq = 0;  // the intensity sums only where a threshold is resolved from them (R22)
     unsigned long long s[9] = {(unsigned long long)n,  (unsigned long long)rs0, (unsigned long long)rs1,
                                hi0, hi1, lo0, lo1, (unsigned long long)is, iq};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -187,7 +188,9 @@ struct TileSums {
 
 // one thread's two columns down a staged tile (base = its column x - 2 in staged row 0).
 // FULL: every column and row of the tile is an output (no per-pixel conditions).
-template <bool FULL>
+// ISTATS: also the intensity sums (only LFE_ADAPT_STD reads them; the public
+// lfe_stats_rows always fills them)
+template <bool FULL, bool ISTATS>
 __device__ __forceinline__ void tile_sums(const uint16_t *base, const int32_t (&c)[2][6], bool ok0, bool ok1,
                                           int rows_left, TileSums &ts)
 {
@@ -232,8 +235,10 @@ __device__ __forceinline__ void tile_sums(const uint16_t *base, const int32_t (&
                         ts.r[1] += r1;
                         ts.q[0] += (unsigned long long)((long long)r0 * r0);
                         ts.q[1] += (unsigned long long)((long long)r1 * r1);
-                        ts.i += (uint32_t)S00;
-                        ts.iq += (unsigned long long)(uint32_t)S00 * (uint32_t)S00;
+                        if constexpr (ISTATS) {
+                            ts.i += (uint32_t)S00;
+                            ts.iq += (unsigned long long)(uint32_t)S00 * (uint32_t)S00;
+                        }
                     }
                 }
             }
@@ -243,7 +248,7 @@ __device__ __forceinline__ void tile_sums(const uint16_t *base, const int32_t (&
 // Tiles are handed out dynamically: counter[0] is the next tile, counter[1] counts
 // finished CTAs; the last CTA resets both to 0 for the next launch (launches that
 // share a counter are stream-ordered: one ctx, one stream at a time).
-template <typename Tin>
+template <typename Tin, bool ISTATS>
 __global__ void __launch_bounds__(kThreads)
     stats5_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Geometry g, lfe_stats *out,
                   unsigned int *counter)
@@ -309,9 +314,9 @@ __global__ void __launch_bounds__(kThreads)
         const int xa = x0 + 2 * t;  // this thread's columns xa, xa + 1
         TileSums ts;
         if (x0 + k5Cols <= W && y0 + k5Rows <= g.o1)
-            tile_sums<true>(sI + 2 * t + 6, c, 0, 0, 0, ts);
+            tile_sums<true, ISTATS>(sI + 2 * t + 6, c, 0, 0, 0, ts);
         else
-            tile_sums<false>(sI + 2 * t + 6, c, xa < W, xa + 1 < W, g.o1 - y0, ts);
+            tile_sums<false, ISTATS>(sI + 2 * t + 6, c, xa < W, xa + 1 < W, g.o1 - y0, ts);
         const int32_t t0 = ts.r[0], t1 = ts.r[1];
         const unsigned long long u0 = ts.q[0], u1 = ts.q[1], uq = ts.iq;
         const uint32_t ti = ts.i;
@@ -351,13 +356,14 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <typename Tin>
-cudaError_t launch_stats_t(const KParams &kp, const Geometry &g, lfe_stats *d_stats, int grid, cudaStream_t s)
+cudaError_t launch_stats_t(const KParams &kp, const Geometry &g, lfe_stats *d_stats, int grid, cudaStream_t s,
+                           bool need_i)
 {
     switch (kp.RL) {
-    case 1: stats_kernel<Tin, 1><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
-    case 2: stats_kernel<Tin, 2><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
-    case 3: stats_kernel<Tin, 3><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
-    default: stats_kernel<Tin, 4><<<grid, kThreads, 0, s>>>(kp, g, d_stats); break;
+    case 1: stats_kernel<Tin, 1><<<grid, kThreads, 0, s>>>(kp, g, d_stats, need_i); break;
+    case 2: stats_kernel<Tin, 2><<<grid, kThreads, 0, s>>>(kp, g, d_stats, need_i); break;
+    case 3: stats_kernel<Tin, 3><<<grid, kThreads, 0, s>>>(kp, g, d_stats, need_i); break;
+    default: stats_kernel<Tin, 4><<<grid, kThreads, 0, s>>>(kp, g, d_stats, need_i); break;
     }
     return cudaGetLastError();
 }
@@ -365,7 +371,7 @@ cudaError_t launch_stats_t(const KParams &kp, const Geometry &g, lfe_stats *d_st
 }  // namespace
 
 cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, unsigned int *d_counter,
-                         cudaStream_t s)
+                         cudaStream_t s, bool need_i)
 {
     const int rows = g.o1 - g.o0;
     if (rows <= 0 || g.width <= 0) return cudaSuccess;
@@ -377,15 +383,19 @@ cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_st
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
         if (in16)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint16_t>, kThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint16_t, true>, kThreads, 0);
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint8_t>, kThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint8_t, true>, kThreads, 0);
         const long long cap = (long long)sms * (per_sm > 0 ? per_sm : 4);
         const int grid = (int)(nt < cap ? nt : cap);
-        if (in16)
-            stats5_kernel<uint16_t><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
+        if (in16 && need_i)
+            stats5_kernel<uint16_t, true><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
+        else if (in16)
+            stats5_kernel<uint16_t, false><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
+        else if (need_i)
+            stats5_kernel<uint8_t, true><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
         else
-            stats5_kernel<uint8_t><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
+            stats5_kernel<uint8_t, false><<<grid, kThreads, 0, s>>>(kp, g, d_stats, d_counter);
         return cudaGetLastError();
     }
     const long long ntiles = (long long)((g.width + kTileW - 1) / kTileW) * ((rows + kTileH - 1) / kTileH);
@@ -394,7 +404,8 @@ cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_st
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
     const int grid = (int)(ntiles < 16LL * sms ? ntiles : 16LL * sms);
-    return in16 ? launch_stats_t<uint16_t>(kp, g, d_stats, grid, s) : launch_stats_t<uint8_t>(kp, g, d_stats, grid, s);
+    return in16 ? launch_stats_t<uint16_t>(kp, g, d_stats, grid, s, need_i)
+                : launch_stats_t<uint8_t>(kp, g, d_stats, grid, s, need_i);
 }
 
 }  // namespace lfe

@@ -541,7 +541,9 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, i
     if (st != LFE_OK) return st;
     st = stats_buffers(c);
     if (st != LFE_OK) return st;
-    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, c->d_tile_counter, (cudaStream_t)stream);
+    // the intensity sums only for a ctx that resolves a threshold from them (R22)
+    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, d_stats, c->d_tile_counter, (cudaStream_t)stream,
+                                 (c->p.adaptive & LFE_ADAPT_STD) != 0);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
     ++c->launches;
     return LFE_OK;
@@ -608,7 +610,9 @@ lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(c->d_stats, 0, sizeof(lfe_stats), s) != cudaSuccess)
         return fail(LFE_ECUDA, "memset: %s", cudaGetErrorString(cudaGetLastError()));
-    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, c->d_tile_counter, s);
+    // (the intensity sums only when a threshold is resolved from them, R22)
+    cudaError_t e = launch_stats(c->kp, g, c->p.bit_depth > 8, c->d_stats, c->d_tile_counter, s,
+                                 (c->p.adaptive & LFE_ADAPT_STD) != 0);
     if (e != cudaSuccess) return fail(LFE_ECUDA, "stats launch: %s", cudaGetErrorString(e));
     ++c->launches;
     if (device_resolvable(c, g)) {

@@ -111,7 +111,7 @@ cudaError_t launch_response(const KParams &kp, const Geometry &g, bool in16, int
 // adds the exact global sums of output rows [o0, o1) to *d_stats (NEXT-2)
 // d_counter: 2 zeroed uints of tile scheduling state the kernel leaves zeroed (ctx-owned)
 cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_stats *d_stats, unsigned int *d_counter,
-                         cudaStream_t s);
+                         cudaStream_t s, bool need_i = true);
 
 // ---- host core (lfe_host.cu), shared with the test-only library (csrc/test/) ----
 namespace host {

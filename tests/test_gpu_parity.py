@@ -1139,15 +1139,19 @@ def _stats_oracle(img, p, a=0, b=None):
     return v + rs, hi, [int(I.sum()), int((I * I).sum())]
 
 
+@pytest.mark.parametrize("istd", [False, True])
 @pytest.mark.parametrize("bd", [8, 10, 12, 16])
-def test_stats_orbit_kernel_sums_exact(bd):
+def test_stats_orbit_kernel_sums_exact(bd, istd):
     """The 5x5 statistics kernel (orbit sums shared by both branches, vector-staged
     interior tiles, clamped border tiles) against exact numpy sums of the oracle's
     responses, whole images and strips with halos, and against the general
     kernel (LFE_STATS_GENERIC)."""
     import os
     rng = np.random.default_rng(1200 + bd)
-    p = lfe.Params(bit_depth=bd, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75))
+    # the intensity sums only for a ctx with LFE_ADAPT_STD (their only reader, R22; lfe.h)
+    p = (lfe.Params(bit_depth=bd, adaptive=lfe.LFE_ADAPT_ZC | lfe.LFE_ADAPT_STD, zc_threshold=(0.75, 0.75),
+                    std_source=lfe.LFE_STD_INTENSITY, std_threshold=(1.0, 1.0))
+         if istd else lfe.Params(bit_depth=bd, adaptive=lfe.LFE_ADAPT_ZC, zc_threshold=(0.75, 0.75)))
     for H, W, a, b in [(70, 300, 0, 70), (300, 1030, 0, 300), (400, 777, 133, 331), (133, 2048, 5, 128)]:
         img = scenes.random_image(rng, H, W, bd, "mixed")
         want_head, want_sq, want_i = _stats_oracle(img, p, a, b)
@@ -1170,7 +1174,7 @@ def test_stats_orbit_kernel_sums_exact(bd):
         v = got["orbit"]
         assert v[:3] == want_head, (H, W, a, b)
         assert [v[3] * 2**24 + v[5], v[4] * 2**24 + v[6]] == want_sq
-        assert v[7:] == want_i
+        assert v[7:] == (want_i if istd else [0, 0])
         assert got["generic"][:3] == v[:3] and got["generic"][7:] == v[7:]
 
 

@@ -1,4 +1,4 @@
-# Round-2 measurement bundle with the tensor-core LoG (one GPU).  Outputs in gpurun_out/ (copied to profiles/ by hand).
+# Round-2 measurement bundle with the tensor-core LoG (one GPU); final state of the round.  Outputs in gpurun_out/ (copied to profiles/ by hand).
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/gpu.txt
@@ -7,7 +7,7 @@ timeout 2400 python -m pytest tests -m gpu -q -rs --durations=10 > gpurun_out/gp
 # ncu --set full of the fused kernel (+ source page) -> hash-stamped issue.json / traffic.json
 bash scripts/ncu_quick.sh
 ncu -i gpurun_out/prof_fused.ncu-rep --page source --csv --print-source sass > gpurun_out/src_sass.csv 2>&1
-python scripts/ncu_issue.py gpurun_out/prof_fused.ncu-rep "r02 final" > /dev/null
+python scripts/ncu_issue.py gpurun_out/prof_fused.ncu-rep "r02 tensor-core LoG (final)" > /dev/null
 cp profiles/issue.json profiles/traffic.json gpurun_out/
 python scripts/ncu_summary.py gpurun_out/prof_fused.ncu-rep > gpurun_out/ncu_fused_summary.txt 2>&1
 bash scripts/ncu_stats.sh

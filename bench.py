@@ -78,8 +78,9 @@ def parse():
     ap.add_argument("--impl", choices=["lfe", "reference"], default="lfe")
     ap.add_argument("--config", choices=sorted(CFG), default="c3")
     ap.add_argument("--kernel", choices=["auto", "staged", "fused"], default="auto")
-    ap.add_argument("--log-unit", choices=["auto", "cuda"], default="auto",
-                    help="fused kernel LoG: tensor cores where exact (auto) or forced CUDA cores (A/B)")
+    ap.add_argument("--log-unit", choices=["auto", "cuda", "tensor"], default="auto",
+                    help="fused kernel LoG: tensor cores where exact and worthwhile (auto), forced CUDA cores, "
+                         "or tensor cores wherever exact (A/B)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="do not report the oracle timing")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check of the last step")
@@ -160,16 +161,23 @@ def _backend_name():
     return "NCCL" if b == "nccl" else f"{b} (host-staged; ranks sharing a GPU: test hook, not a measurement)"
 
 
-def log_unit_of(ctx, p, forced_cuda: bool) -> str:
+def log_unit_of(ctx, p, unit: str, units: int) -> str:
     """Which unit the fused kernel computes the two LoG responses on (the library's
     rule, kernel_fused.cu tc_exact): the tensor cores when exact there -- u16 input with
     b <= 12 and every mask coefficient an fp16 value -- else the CUDA cores."""
     import numpy as np
-    qs = [ctx.mask(j)[0] for j in (0, 1)]
-    exact = all(np.all(np.float16(q).astype(np.float64) == q) for q in qs)
-    if not forced_cuda and 8 < p.bit_depth <= 12 and exact and p.std_source == 0:
-        return ("tensor cores (tcgen05.mma kind::f16 into TMEM; exact: u16 bits = fp16 v*2^-24, fp16-exact integer masks"
-                + ("; b = 12: v & 0x7FF and bit 11 as two K halves)" if p.bit_depth == 12 else ")"))
+    qs = [ctx.mask(j)[0].astype(np.float64) for j in (0, 1)]
+    hi = [np.float16(q).astype(np.float64) for q in qs]
+    exact = all(np.all(h == q) for h, q in zip(hi, qs))
+    split = all(np.all(np.float16(q - h).astype(np.float64) == q - h) for h, q in zip(hi, qs)) and \
+        max(float(np.abs(h).sum() + np.abs(q - h).sum()) for h, q in zip(hi, qs)) * ((1 << p.bit_depth) - 1) < 2 ** 24
+    tc = (8 < p.bit_depth <= 12 and exact) or (p.bit_depth <= 8 and split)
+    tc = tc and (units >= 32 * 148 or unit == "tensor")  # the library's small-launch rule (kernel_fused.cu)
+    if unit != "cuda" and tc and p.std_source == 0:
+        return ("tensor cores (tcgen05.mma kind::f16 into TMEM; exact: the input bits as fp16 = v*2^-24"
+                + ("; b = 12: v & 0x7FF and bit 11 as two K halves)" if p.bit_depth == 12 else
+                   "; u8: weights as fp16(q) + remainder in two B matrices)" if p.bit_depth <= 8 else
+                   ", fp16-exact integer masks)"))
     return "CUDA cores (exact-integer fp32 FFMA)"
 
 
@@ -492,7 +500,8 @@ def main():
     esz = elem(cfg)
     ctx = lfe.Context(p)
     ctx.set_option(lfe.LFE_OPT_KERNEL, {"auto": 0, "staged": 1, "fused": 2}[args.kernel])
-    ctx.set_option(lfe.LFE_OPT_LOG_UNIT, {"auto": lfe.LFE_LOG_AUTO, "cuda": lfe.LFE_LOG_CUDA_CORES}[args.log_unit])
+    ctx.set_option(lfe.LFE_OPT_LOG_UNIT, {"auto": lfe.LFE_LOG_AUTO, "cuda": lfe.LFE_LOG_CUDA_CORES,
+                                          "tensor": lfe.LFE_LOG_TENSOR_CORES}[args.log_unit])
     if args.tile:
         tw, th = (int(v) for v in args.tile.split("x"))
         ctx.set_option(lfe.LFE_OPT_TILE_W, tw)
@@ -803,7 +812,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": config_dict(name, cfg, world, p, graph=graph is not None, halo_mode=halo_mode,
-                                  log_unit=log_unit_of(ctx, p, args.log_unit == "cuda")),
+                                  log_unit=log_unit_of(ctx, p, args.log_unit,
+                                                       NB * ((W + 1343) // 1344) * (H // world))),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel": "lfe fused stencil kernel (dominant launch: the interior band / all whole bands)"

@@ -66,10 +66,12 @@ enum { LFE_TOP_IS_EDGE = 1u, LFE_BOTTOM_IS_EDGE = 2u };
 enum { LFE_OPT_KERNEL = 1, LFE_OPT_TILE_W = 2, LFE_OPT_TILE_H = 3, LFE_OPT_HOST_STRIP_ROWS = 4, LFE_OPT_LOG_UNIT = 5 };
 /* LFE_OPT_LOG_UNIT values: where the fused kernel computes the two LoG responses.
  * AUTO: on the tensor cores (tcgen05) when exact there -- uint16 input with
- * b <= 11 and every mask coefficient an fp16 value -- else on the CUDA cores
- * (exact-integer fp32 FFMA); CUDA_CORES forces the latter (A/B and tests).
- * Results are identical either way. */
-enum { LFE_LOG_AUTO = 0, LFE_LOG_CUDA_CORES = 1 };
+ * b <= 12 and every mask coefficient an fp16 value, or uint8 input whose mask
+ * coefficients split into two fp16 values -- and the launch has at least 32 rows
+ * per SM; else on the CUDA cores (exact-integer fp32 FFMA).  CUDA_CORES forces the
+ * latter, TENSOR_CORES the former wherever exact (any size; tests, A/B).  Results
+ * are identical either way. */
+enum { LFE_LOG_AUTO = 0, LFE_LOG_CUDA_CORES = 1, LFE_LOG_TENSOR_CORES = 2 };
 /* LFE_OPT_KERNEL values. */
 enum { LFE_KERNEL_AUTO = 0, LFE_KERNEL_STAGED = 1, LFE_KERNEL_FUSED = 2 };
 /* lfe_params.adaptive flags (NEXT-2, readings R21/R22). */

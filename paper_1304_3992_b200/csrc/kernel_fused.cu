@@ -324,15 +324,27 @@ cudaError_t launch_signal(unsigned long long *flag, unsigned long long value, cu
 // The LoG on the tensor cores is exact when the u16 input bits read as fp16 are the
 // values themselves times 2^-24 (v < 2048: subnormals and the first binade) and every
 // mask coefficient is an fp16 value (scripts/tc_probe.cu).  b = 12
-// splits v into v & 0x7FF and bit 11 (TC12).  0: not exact, 1: TC, 2: TC12.
+// splits v into v & 0x7FF and bit 11 (TC12).  u8 input (TC8) takes every weight as
+// fp16(c) plus the remainder c - fp16(c), both exact fp16 values, in two matrices whose
+// partial sums together stay below 2^24 units.  0: not exact, 1: TC (TC8 for u8),
+// 2: TC12.
 static int tc_exact(const KParams &kp, bool in16)
 {
-    if (!in16 || kp.maxv > 4095) return 0;
-    for (int j = 0; j < 2; ++j)
+    if (kp.maxv > 4095) return 0;
+    double sum_abs = 0.0;  // sum |fp16(q)| + |q - fp16(q)| over the 25 taps, both branches' max
+    for (int j = 0; j < 2; ++j) {
+        double sj = 0.0;
         for (int k = 0; k < 6; ++k) {
             const float c = (float)kp.orb[j][k];
-            if (std::fabs(c) > 65504.0f || __half2float(__float2half_rn(c)) != c) return 0;
+            if (std::fabs(c) > 65504.0f) return 0;
+            const float hi = __half2float(__float2half_rn(c)), lo = c - hi;
+            if (in16 ? hi != c : __half2float(__float2half_rn(lo)) != lo) return 0;
+            static const int orbit[6] = {1, 4, 4, 4, 8, 4};
+            sj += orbit[k] * ((double)std::fabs(hi) + std::fabs(lo));
         }
+        sum_abs = std::max(sum_abs, sj);
+    }
+    if (!in16) return kp.maxv * sum_abs < 16777216.0 ? 1 : 0;
     return kp.maxv > 2047 ? 2 : 1;
 }
 
@@ -356,14 +368,25 @@ cudaError_t launch_fused(const KParams &kp, const Geometry &g, bool in16, int lo
     if (v.stdi && (v.peer || v.devt)) return cudaErrorNotSupported;
     v.gap = kp.zc_t[0] > 0 || kp.zc_t[1] > 0 || v.hml == 2 || v.rc || v.peer || v.devt || v.stdi;
     // the tensor-core LoG where it is exact and compiled (else the CUDA-core one)
-    const int tcx = log_unit != LFE_LOG_CUDA_CORES && !v.stdi ? tc_exact(kp, in16) : 0;
+    // ... and where it pays: a launch with under ~32 rows per SM (c1's 512^2) is bound by
+    // the per-CTA warm-up, which the TMEM allocation, the MMA prologue and the zeroed
+    // ring lengthen (c1: 0.0447 ms on the CUDA cores, 0.047 ms on the tensor cores)
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long units = (long long)fa.nbands * fa.col_groups * (fa.o1 - fa.o0);
+    const bool tc_pays = units >= 32LL * (sms > 0 ? sms : 148);
+    const int tcx = log_unit != LFE_LOG_CUDA_CORES && !v.stdi && (tc_pays || log_unit == LFE_LOG_TENSOR_CORES)
+                        ? tc_exact(kp, in16)
+                        : 0;
     for (int pass = tcx ? 0 : 1; pass < 2; ++pass) {
         v.tc = pass == 0;
         v.tc12 = pass == 0 && tcx == 2;
         for (auto group : {fz::launch_group0, fz::launch_group1, fz::launch_group2, fz::launch_group3,
                            fz::launch_group4, fz::launch_group5, fz::launch_group6, fz::launch_group7,
                            fz::launch_group8, fz::launch_group9, fz::launch_group10, fz::launch_group11,
-                           fz::launch_group12, fz::launch_group13, fz::launch_group14}) {
+                           fz::launch_group12, fz::launch_group13, fz::launch_group14,
+                           fz::launch_group15}) {
             e = group(v, fa, maps, err_flag, s);
             if (e != cudaErrorNotSupported) return e;
         }

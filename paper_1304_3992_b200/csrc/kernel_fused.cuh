@@ -179,6 +179,7 @@ cudaError_t launch_group11(const Variant &, const FusedArgs &, const Maps &, int
 cudaError_t launch_group12(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group13(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 cudaError_t launch_group14(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
+cudaError_t launch_group15(const Variant &, const FusedArgs &, const Maps &, int *, cudaStream_t);
 
 // Test-only kernel variants (TV): the stage before the one under test is replaced
 // by values injected through the input image (test/kernel_fused_test.cu).
@@ -260,8 +261,10 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 // B: K = 64 (8 patch rows x 8 columns) x N = 32 (4 r rows x 2 branches x 4 pixels), fp16
 // (TC12: K = 128, every patch row twice: its low 11 bits, then its bit 11), then the
 // 6 issue counters and the TMEM base address
-template <bool TC12> __host__ __device__ constexpr int tc_b_bytes() { return (TC12 ? 128 : 64) * 32 * 2; }
-template <bool TC12> __host__ __device__ constexpr int tc_smem() { return tc_b_bytes<TC12>() + 64; }
+// (TC8, u8 input: two K = 64 matrices, the weights rounded to fp16 and the remainders,
+// both exact fp16 values -- a b = 8 mask has a 12-bit coefficient)
+template <bool TC12, bool TC8> __host__ __device__ constexpr int tc_b_bytes() { return (TC12 || TC8 ? 128 : 64) * 32 * 2; }
+template <bool TC12, bool TC8> __host__ __device__ constexpr int tc_smem() { return tc_b_bytes<TC12, TC8>() + 64; }
 constexpr int kTcCols = 160;       // TMEM columns per group of 4 warps: A x2 (48 each) + D (2 halves x 32)
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -300,24 +303,25 @@ __device__ __forceinline__ void tc_wait_ld(uint32_t (&v)[8])
 // D[dcol .. +32) (= 4 r rows) from A columns [acol, acol + 32) (= 8 patch rows) and B:
 // four K = 16 steps (TC12: eight, one patch row each, over A columns [acol, acol + 64)),
 // then a commit to `bar` (one elected thread)
-template <bool TC12>
+template <bool TC12, bool TC8>
 __device__ __forceinline__ void tc_mma_half(uint32_t dcol, uint32_t acol, uint32_t b_saddr, uint64_t *bar)
 {
     // kind::f16: A = B = F16, D = F32, both K-major, N = 32 (>> 3), M = 128 (>> 4)
     constexpr uint32_t idesc = (1u << 4) | (4u << 17) | (8u << 24);
-    constexpr int kSteps = TC12 ? 8 : 4;
-    constexpr uint32_t kSbo = 128 * 2 * kSteps;  // one 8-row group of B along N: every K core matrix
+    constexpr int kSteps = TC12 || TC8 ? 8 : 4;
+    constexpr uint32_t kSbo = 128 * 2 * (TC12 ? 8 : 4);  // one 8-row group of a B matrix along N: every K core matrix
 #pragma unroll
     for (int kk = 0; kk < kSteps; ++kk) {
         // canonical K-major layout without swizzle: core matrices of 8 rows x 16 B,
-        // 128 B apart along K (LBO), kSbo apart along N (SBO); version 1
-        const uint32_t sa = b_saddr + kk * 256;
+        // 128 B apart along K (LBO), kSbo apart along N (SBO); version 1.  TC8: steps
+        // 4..7 repeat A's columns against the second matrix (the remainders)
+        const uint32_t sa = TC8 && kk >= 4 ? b_saddr + 4096 + (kk - 4) * 256 : b_saddr + kk * 256;
         const uint64_t desc = (uint64_t)((sa >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(kSbo >> 4) << 32) |
                               (1ull << 46);
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
-            "r"(acol + kk * 8), "l"(desc), "r"(idesc), "r"((uint32_t)kk)
+            "r"(acol + (TC8 ? (kk & 3) : kk) * 8), "l"(desc), "r"(idesc), "r"((uint32_t)kk)
             : "memory");
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -431,6 +435,10 @@ __device__ __forceinline__ float byte_f(uint32_t w, uint32_t sel) { return __uin
     if (v.in16 && v.hml == B && v.mask == C && v.gap && !v.rc && !v.peer && v.devt && !v.stdi && v.tc && !v.tc12) \
         return launch_t<true, B, C, true, false, false, kTvNone, true, false, true>(fa, maps, err_flag, s);
 // b = 12 (u16): the patch split into its low 11 bits and bit 11 (TC12)
+// u8 input (TC8): the patch's bytes as u16 pairs, the weights split into two fp16 matrices
+#define LFE_FUSED_TC8_VARIANT(B, C, D, E)                                                      \
+    if (!v.in16 && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && v.tc) \
+        return launch_t<false, B, C, D, E, false, kTvNone, false, false, true>(fa, maps, err_flag, s);
 #define LFE_FUSED_TC12_VARIANT(B, C, D, E)                                                     \
     if (v.in16 && v.hml == B && v.mask == C && v.gap == D && v.rc == E && !v.peer && !v.devt && !v.stdi && v.tc && v.tc12) \
         return launch_t<true, B, C, D, E, false, kTvNone, false, false, true, true>(fa, maps, err_flag, s);
@@ -784,7 +792,8 @@ __global__ void __launch_bounds__(LFE_LB, 1)
     uint64_t *tcbar = full + 2 * kS;
     static_assert(kHdr >= 8 * (2 * kS + 2 * (kWarps / 4)), "mbarrier header");
     unsigned char *tcB = ring + kS * kStageBytes + kWarps * warp_bytes(HML);
-    constexpr int kBB = tc_b_bytes<TC12>();  // B bytes; the counters and the TMEM base follow
+    constexpr bool TC8 = TC && !IN16;  // u8 input: B split into rounded weights + remainders
+    constexpr int kBB = tc_b_bytes<TC12, TC8>();  // B bytes; the counters and the TMEM base follow
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tcB + kBB + 32);
     const unsigned long long t_start = gtime();
     if (threadIdx.x == 0) {
@@ -806,16 +815,17 @@ __global__ void __launch_bounds__(LFE_LB, 1)
         // (TC12: k = (patch row, part, patch column), both parts the same weights):
         // q_branch(dy, dx) with dy = patch row - r row - 2, dx = patch column - pixel - 2
         constexpr int kK = TC12 ? 128 : 64;
-        for (int e = threadIdx.x; e < kK * 32; e += kThreads) {
-            const int n = e / kK, k = e % kK;
+        for (int e = threadIdx.x; e < (TC8 ? 2 : 1) * kK * 32; e += kThreads) {
+            const int part = e / (kK * 32), n = (e % (kK * 32)) / kK, k = e % kK;
             const int prow_k = TC12 ? k >> 4 : k >> 3;
             const int dy = prow_k - (n >> 3) - 2, dx = (k & 7) - (n & 3) - 2, br = (n >> 2) & 1;
             const int ay = dy < 0 ? -dy : dy, ax = dx < 0 ? -dx : dx;
             const int hi = ay > ax ? ay : ax, lo = ay > ax ? ax : ay;
             float c = 0.0f;
             if (hi <= 2) c = a.c[br][hi == 0 ? 0 : hi == 1 ? (lo == 0 ? 1 : 3) : (lo == 0 ? 2 : lo == 1 ? 4 : 5)];
-            *reinterpret_cast<__half *>(tcB + (n >> 3) * (kK / 8) * 128 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) =
-                __float2half_rn(c);
+            const __half ch = __float2half_rn(c);  // (TC8 part 1: the remainder c - fp16(c), exact)
+            *reinterpret_cast<__half *>(tcB + part * 4096 + (n >> 3) * (kK / 8) * 128 + (k >> 3) * 128 + (n & 7) * 16 +
+                                        (k & 7) * 2) = part ? __float2half_rn(c - __half2float(ch)) : ch;
         }
         if (threadIdx.x < 6) reinterpret_cast<uint32_t *>(tcB + kBB)[threadIdx.x] = 0;  // group x half counters
         // the ring starts zeroed: a slot no TMA has filled yet never holds fp16 NaN patterns
@@ -1511,11 +1521,24 @@ __global__ void __launch_bounds__(LFE_LB, 1)
             for (int j = 0; j < kRowsPerSt; ++j) {
                 const int ky = kRowsPerSt * q + j;
                 const unsigned char *p = ky < 4 ? prev + (4 + ky) * kRowBytes : cur + (ky - 4) * kRowBytes;
-                const uint2 own = *reinterpret_cast<const uint2 *>(p);
-                if (ky >= 4) range_acc |= (own.x & clo) | (own.y & chi);
-                uint32_t L = __shfl_up_sync(0xffffffffu, own.y, 1), R = __shfl_down_sync(0xffffffffu, own.x, 1);
-                if constexpr (XQ) L = isL ? prmt(own.x, 0, 0x1010) : L;  // columns -2, -1 := column 0 (R5)
-                if constexpr (XQ) R = isR ? prmt(own.y, 0, 0x3232) : R;  // columns W, W+1 := column W-1
+                uint2 own;
+                uint32_t L, R;
+                if constexpr (IN16) {
+                    own = *reinterpret_cast<const uint2 *>(p);
+                    if (ky >= 4) range_acc |= (own.x & clo) | (own.y & chi);
+                    L = __shfl_up_sync(0xffffffffu, own.y, 1);
+                    R = __shfl_down_sync(0xffffffffu, own.x, 1);
+                    if constexpr (XQ) L = isL ? prmt(own.x, 0, 0x1010) : L;  // columns -2, -1 := column 0 (R5)
+                    if constexpr (XQ) R = isR ? prmt(own.y, 0, 0x3232) : R;  // columns W, W+1 := column W-1
+                } else {  // TC8: 4 bytes -> two u16 pairs (the raw bits ARE the fp16 operand)
+                    const uint32_t w = *reinterpret_cast<const uint32_t *>(p);
+                    if (ky >= 4) range_acc |= w & clo;
+                    own = make_uint2(prmt(w, 0, 0x4140), prmt(w, 0, 0x4342));
+                    L = prmt(__shfl_up_sync(0xffffffffu, w, 1), 0, 0x4342);
+                    R = prmt(__shfl_down_sync(0xffffffffu, w, 1), 0, 0x4140);
+                    if constexpr (XQ) L = isL ? prmt(w, 0, 0x4040) : L;
+                    if constexpr (XQ) R = isR ? prmt(w, 0, 0x4343) : R;
+                }
                 if constexpr (TC12) {
                     r[8 * j] = L & 0x07FF07FFu;
                     r[8 * j + 1] = own.x & 0x07FF07FFu;
@@ -1554,7 +1577,7 @@ __global__ void __launch_bounds__(LFE_LB, 1)
                          : "memory");
             if ((old & 3) == 3) {
                 tc_fence_after();
-                tc_mma_half<TC12>((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + (TC12 ? 32 : 16) * h, smem_u32(tcB),
+                tc_mma_half<TC12, TC8>((tl & 0xFFFFu) + td0 + 32 * h, (tl & 0xFFFFu) + acol + (TC12 ? 32 : 16) * h, smem_u32(tcB),
                             &tcbar[2 * (warp >> 2) + h]);
             }
         }
@@ -1764,10 +1787,10 @@ __global__ void __launch_bounds__(LFE_LB, 1)
         const bool xedge_cta = (it.xo - kHaloX < 0 || it.xo - kHaloX + (kWarps - 1) * kWarpOut + 128 > W) && !a.dbg_nofix;
         const bool yf_item = it.ys - kHalo < 0 || it.ye + kHalo > H || (xedge_cta && (W & 3));
         bool shadow = false;
-        if constexpr (TC12) shadow = xw + kHaloX >= W && !yf_item;
+        if constexpr (TC12 || TC8) shadow = xw + kHaloX >= W && !yf_item;
         if (shadow) {
             tc_shadow();
-        } else if (!(TC && !TC12) && xw + kHaloX >= W) {
+        } else if (!(TC && !TC12 && !TC8) && xw + kHaloX >= W) {
             // no output column of this warp is in the image (the last column group of a
             // width that is not a multiple of 1344): follow the ring without computing --
             // wait for each stage, then release it, in order (an early release would count
@@ -1825,10 +1848,11 @@ template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false
           bool STDI = false, bool TC = false, bool TC12 = false>
 cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaStream_t s)
 {
-    static_assert(!TC || (IN16 && !STDI && TV == kTvNone), "TC: u16 plain / DEVT / PEER variants only");
-    static_assert(!TC12 || TC, "TC12 is a TC variant");
+    static_assert(!TC || (!STDI && TV == kTvNone), "TC: plain / DEVT / PEER variants only");
+    static_assert(!TC12 || (TC && IN16), "TC12 is a u16 TC variant");
     auto kfn = fused_kernel<IN16, HML, MASKOUT, GAP, RC, PEER, TV, DEVT, STDI, TC, TC12>;
-    constexpr size_t smem = fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0) + (TC ? (size_t)tc_smem<TC12>() : 0);
+    constexpr size_t smem =
+        fused_smem<IN16, HML>() + (STDI ? (size_t)kWarps * kPBytes : 0) + (TC ? (size_t)tc_smem<TC12, TC && !IN16>() : 0);
     // the shared-memory attribute is per device: one-time setup for each device this
     // process launches on (a ctx binds one device; several ctxs may span devices)
     // (std::call_once: distinct ctxs on distinct host threads may launch concurrently)
@@ -1853,7 +1877,7 @@ cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaS
     // The 11-bit TC kernels walk warps with no output column like the others (their MMA
     // protocol needs the group's 4 warps; a shadow walk would add ~1.4 k instructions to
     // the c3 kernel, measured 2.6% slower); TC12 and the CUDA-core kernels shadow / skip them
-    fw.idle_walk = TC && !TC12;
+    fw.idle_walk = TC && !TC12 && IN16;
     cached_partition(fw, grid, halo_of(HML));
     static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
     FusedArgs fb = fw;

@@ -449,7 +449,7 @@ lfe_status lfe_set_option(lfe_ctx *c, int32_t key, int64_t value)
         c->host_strip_rows = (int)value;
         return LFE_OK;
     case LFE_OPT_LOG_UNIT:
-        if (value < LFE_LOG_AUTO || value > LFE_LOG_CUDA_CORES) return fail(LFE_EINVAL, "bad LoG unit");
+        if (value < LFE_LOG_AUTO || value > LFE_LOG_TENSOR_CORES) return fail(LFE_EINVAL, "bad LoG unit");
         c->cfg.log_unit = (int)value;
         return LFE_OK;
     }

@@ -30,7 +30,7 @@ LFE_PEER_ROWS = 8  # rows lfe_extract_rows_peer reads from each neighbour
 LFE_OPT_KERNEL, LFE_OPT_TILE_W, LFE_OPT_TILE_H, LFE_OPT_HOST_STRIP_ROWS = 1, 2, 3, 4
 LFE_KERNEL_AUTO, LFE_KERNEL_STAGED, LFE_KERNEL_FUSED = 0, 1, 2
 LFE_OPT_LOG_UNIT = 5
-LFE_LOG_AUTO, LFE_LOG_CUDA_CORES = 0, 1  # fused kernel: LoG on the tensor cores where exact / forced CUDA cores
+LFE_LOG_AUTO, LFE_LOG_CUDA_CORES, LFE_LOG_TENSOR_CORES = 0, 1, 2  # fused kernel LoG unit (lfe.h)
 LFE_ADAPT_ZC, LFE_ADAPT_STD = 1, 2
 
 _STATUS = {0: "LFE_OK", 1: "LFE_EINVAL", 2: "LFE_EUNSUPPORTED", 3: "LFE_ENOMEM",

@@ -89,3 +89,17 @@ for bd, shape in [(8, (70, 300)), (16, (133, 1030))]:
         ctx.stats_rows(torch.from_numpy(x).cuda(), 0, shape[0], 0, 0, 3, st)
         ctx.check()
     print('ok stats5', bd, shape)
+
+# tensor-core LoG (kernel_fused TC / TC12): interior, cheap column edges with warps
+# that have no output column (11-bit: they walk; 12-bit: shadow walk), short pieces
+rng = np.random.default_rng(5)
+for bd, W in ((10, 1444), (11, 2696), (12, 1444), (12, 8192)):
+    img = scenes.random_image(rng, 120, W, bd, "mixed")
+    for seg in (0, 5):
+        with lfe.Context(lfe.Params(bit_depth=bd, zc_threshold=(0.02, 0.02))) as ctx:
+            if seg:
+                ctx.set_option(lfe.LFE_OPT_TILE_H, seg)
+            d = torch.from_numpy(img).cuda()
+            out = ctx.extract(d)
+            ctx.check()
+            print('ok tc', bd, W, seg)

@@ -33,14 +33,15 @@ def _gpu():
     lfe.load()
 
 
-def run(img, p, log_unit=lfe.LFE_LOG_AUTO, seg=0):
+def run(img, p, log_unit=lfe.LFE_LOG_TENSOR_CORES, seg=0):
     with lfe.Context(p) as ctx:
         ctx.set_option(lfe.LFE_OPT_KERNEL, lfe.LFE_KERNEL_FUSED)
         ctx.set_option(lfe.LFE_OPT_LOG_UNIT, log_unit)
         if seg:
             ctx.set_option(lfe.LFE_OPT_TILE_H, seg)
-        tout = torch.uint8 if p.out_mode == lfe.LFE_OUT_MASK else torch.uint16
-        d = _pitched(img.shape, torch.uint16)
+        tin = torch.uint8 if p.bit_depth <= 8 else torch.uint16
+        tout = torch.uint8 if p.out_mode == lfe.LFE_OUT_MASK else tin
+        d = _pitched(img.shape, tin)
         d.copy_(torch.from_numpy(np.ascontiguousarray(img)))
         out = _pitched(img.shape, tout)
         ctx.extract(d, out)
@@ -65,6 +66,13 @@ def _variants():
     yield lfe.Params(bit_depth=12, median_window2=3, zc_threshold=(0.01, 0.01))
     yield lfe.Params(bit_depth=12, std3_threshold=(0.4, 0.2), zc_threshold=(0.01, 0.0))
     yield lfe.Params(bit_depth=12, hybrid_median=False, zc_threshold=(0.02, 0.0))
+    # u8 (c1, c2): bytes as u16 pairs, weights as fp16(q) + remainder (TC8)
+    yield lfe.Params(bit_depth=8, zc_threshold=(0.02, 0.02))
+    yield lfe.Params(bit_depth=8, zc_threshold=(0.0, 0.0), out_mode=lfe.LFE_OUT_MASK)
+    yield lfe.Params(bit_depth=8, median_window2=3, zc_threshold=(0.01, 0.01))
+    yield lfe.Params(bit_depth=8, std3_threshold=(0.4, 0.2), zc_threshold=(0.01, 0.0))
+    yield lfe.Params(bit_depth=8, hybrid_median=False, zc_threshold=(0.02, 0.0))
+    yield lfe.Params(bit_depth=6, sigma=(1.0, 2.0), zc_threshold=(0.01, 0.02))
 
 
 VARIANTS = list(_variants())
@@ -85,7 +93,7 @@ def test_tc_equals_cuda_cores_and_oracle(vi):
         assert_same(run(img, p, lfe.LFE_LOG_CUDA_CORES), got, f"CUDA cores vs TC {H}x{W} {kind}")
 
 
-@pytest.mark.parametrize("bd", [11, 12])
+@pytest.mark.parametrize("bd", [8, 11, 12])
 @pytest.mark.parametrize("kind", ["max", "binade", "checker", "ramp"])
 def test_tc_bit_depth_extremes(kind, bd):
     """b = 11: the u16 bits 1024..2047 are fp16 normals of the first binade (still
@@ -104,7 +112,7 @@ def test_tc_bit_depth_extremes(kind, bd):
         img = np.where(((y // 2) + (x // 2)) % 2 == 0, M, 0)
     else:
         img = (x * 7 + y * 13) % (M + 1)
-    img = img.astype(np.uint16)
+    img = img.astype(np.uint8 if bd <= 8 else np.uint16)
     for p in (lfe.Params(bit_depth=bd, zc_threshold=(0.0, 0.0)),
               lfe.Params(bit_depth=bd, zc_threshold=(0.02, 0.02), median_window2=3)):
         want = O.run(img, _oparams(p))
@@ -139,6 +147,15 @@ def test_tc12_wide_strip_equals_oracle():
     assert_same(got, O.run(img, _oparams(p)), "b12 strip vs oracle")
 
 
+def test_tc8_c2_tile_equals_cuda_cores():
+    """c2's recipe (u8 urban tile) at 1500^2 (two column groups, one mostly idle), both LoG units."""
+    img = scenes.scene_c2(size=1500)
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.02, 0.02))
+    got = run(img, p)
+    assert_same(got, run(img, p, lfe.LFE_LOG_CUDA_CORES), "c2 tile")
+    assert_same(got, O.run(img, _oparams(p)), "c2 tile vs oracle")
+
+
 def test_tc_c3_strip_equals_cuda_cores():
     """The bench scene's recipe: 600 rows of c3 at full width, both LoG units."""
     img = scenes.scene_c3(height=600)
@@ -151,6 +168,17 @@ def test_tc_c3_strip_equals_cuda_cores():
 def test_log_unit_option_validation():
     with lfe.Context(lfe.Params(bit_depth=10)) as ctx:
         ctx.set_option(lfe.LFE_OPT_LOG_UNIT, lfe.LFE_LOG_CUDA_CORES)
+        ctx.set_option(lfe.LFE_OPT_LOG_UNIT, lfe.LFE_LOG_TENSOR_CORES)
         ctx.set_option(lfe.LFE_OPT_LOG_UNIT, lfe.LFE_LOG_AUTO)
         with pytest.raises(lfe.LfeError):
-            ctx.set_option(lfe.LFE_OPT_LOG_UNIT, 2)
+            ctx.set_option(lfe.LFE_OPT_LOG_UNIT, 3)
+
+
+def test_auto_log_unit_equals_forced_units_on_c1():
+    """c1 (below the 32-rows-per-SM rule: CUDA cores under AUTO) gives the same
+    result on either unit."""
+    img = scenes.scene_c1()
+    p = lfe.Params(bit_depth=8, zc_threshold=(0.02, 0.02))
+    got = run(img, p, lfe.LFE_LOG_AUTO)
+    assert_same(got, run(img, p, lfe.LFE_LOG_TENSOR_CORES), "c1 auto vs tensor cores")
+    assert_same(got, O.run(img, _oparams(p)), "c1 vs oracle")

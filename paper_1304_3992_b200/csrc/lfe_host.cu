@@ -17,8 +17,21 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "lfe.h"
 #include "lfe_internal.h"
+
+namespace {
+// NVTX ranges on the host entry points and the streamed strips, for nsys / ncu --nvtx
+// (a no-op unless a tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace
 
 using namespace lfe;
 
@@ -530,6 +543,7 @@ lfe_status lfe_stats_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch, i
                           int32_t halo_above, int32_t halo_below, uint32_t edge_flags, lfe_stats *d_stats,
                           void *stream)
 {
+    NvtxRange nvtx_range("lfe_stats_rows");
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
     lfe_status st = check_bound_device(c);
     if (st != LFE_OK) return st;
@@ -594,6 +608,7 @@ static bool device_resolvable(const lfe_ctx *c, const Geometry &g)
 lfe_status lfe_extract(lfe_ctx *c, const void *d_in, int64_t in_pitch, int32_t W, int32_t H, void *d_out,
                        int64_t out_pitch, void *stream)
 {
+    NvtxRange nvtx_range("lfe_extract");
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
     lfe_status st = check_bound_device(c);
     if (st != LFE_OK) return st;
@@ -639,6 +654,7 @@ lfe_status lfe_extract_bands(lfe_ctx *c, const void *d_in, int64_t in_pitch, int
                              int32_t H, int32_t bands, void *d_out, int64_t out_pitch, int64_t out_band_stride,
                              void *stream)
 {
+    NvtxRange nvtx_range("lfe_extract_bands");
     lfe_status st = check_image_args(c, d_in, in_pitch, W, H, d_out, out_pitch, H);
     if (st != LFE_OK) return st;
     if (bands < 1 || bands > 65535) return fail(LFE_EINVAL, "bands %d not in 1..65535", bands);
@@ -680,6 +696,7 @@ lfe_status lfe_extract_rows(lfe_ctx *c, const void *d_in_row0, int64_t in_pitch,
                             int32_t halo_above, int32_t halo_below, uint32_t edge_flags, void *d_out_row0,
                             int64_t out_pitch, void *stream)
 {
+    NvtxRange nvtx_range("lfe_extract_rows");
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
     if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
     return extract_rows(c, c->kp, d_in_row0, in_pitch, W, rows, halo_above, halo_below, edge_flags, d_out_row0,
@@ -691,6 +708,7 @@ lfe_status lfe_extract_rows_peer(lfe_ctx *c, const void *d_in_row0, int64_t in_p
                                  uint32_t edge_flags, const uint64_t *wait_above, const uint64_t *wait_below,
                                  uint64_t wait_value, void *d_out_row0, int64_t out_pitch, void *stream)
 {
+    NvtxRange nvtx_range("lfe_extract_rows_peer");
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
     if (!c->have_thresholds) return fail(LFE_EINVAL, "adaptive ctx needs whole-image statistics (lfe_set_stats)");
     lfe_status st = check_image_args(c, d_in_row0, in_pitch, W, rows, d_out_row0, out_pitch, rows);
@@ -867,6 +885,7 @@ static std::vector<int> host_strip_cuts(int H, int S)
 lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int32_t W, int32_t H, void *h_out,
                             int64_t out_pitch)
 {
+    NvtxRange nvtx_range("lfe_extract_host");
     if (!c) return fail(LFE_EINVAL, "ctx is NULL");
     lfe_status st = check_bound_device(c);
     if (st != LFE_OK) return st;
@@ -928,6 +947,7 @@ lfe_status lfe_extract_host(lfe_ctx *c, const void *h_in, int64_t in_pitch, int3
     }
     if (ndbg) cudaEventRecord(dev[6 * ndbg], sh);
     for (int i = 0; i < nstrips; ++i) {
+        NvtxRange nvtx_strip("strip: H2D -> extract -> D2H");
         const int b = i % kHostBuffers;
         const int a0 = cut[i], a1 = cut[i + 1];
         const int lo = a0 - h > 0 ? a0 - h : 0, hi = a1 + h < H ? a1 + h : H;

@@ -382,10 +382,15 @@ cudaError_t launch_stats(const KParams &kp, const Geometry &g, bool in16, lfe_st
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
-        if (in16)
+        // (the instantiation that runs: without the intensity sums it fits 5 CTAs per SM, not 4)
+        if (in16 && need_i)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint16_t, true>, kThreads, 0);
-        else
+        else if (in16)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint16_t, false>, kThreads, 0);
+        else if (need_i)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint8_t, true>, kThreads, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats5_kernel<uint8_t, false>, kThreads, 0);
         const long long cap = (long long)sms * (per_sm > 0 ? per_sm : 4);
         const int grid = (int)(nt < cap ? nt : cap);
         if (in16 && need_i)

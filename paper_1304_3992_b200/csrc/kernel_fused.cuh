@@ -736,7 +736,10 @@ struct Producer {
 //     E = I, so the hybrid-median stages (one or two levels) can be checked on any E.
 template <bool IN16, int HML, bool MASKOUT, bool GAP, bool RC, bool PEER = false, int TV = kTvNone, bool DEVT = false,
           bool STDI = false, bool TC = false, bool TC12 = false>
-__global__ void __launch_bounds__(kThreads, 1)
+#ifndef LFE_LB
+#define LFE_LB kThreads
+#endif
+__global__ void __launch_bounds__(LFE_LB, 1)
     fused_kernel(const __grid_constant__ Maps maps, const __grid_constant__ FusedArgs a, int *err_flag)
 {
     constexpr bool HM = HML >= 1, HM2 = HML == 2;

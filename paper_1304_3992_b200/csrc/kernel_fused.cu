@@ -57,6 +57,12 @@ namespace part {
 constexpr double kPiece = 19.5;      // row-equivalents per piece (pipeline warm-up)
 constexpr double kEdgePiece = 2.7;    // extra for an edge-row piece (general path)
 constexpr double kEdgeCol = 1.048;   // column-edge group, cheap path (W % 4 == 0)
+// the tensor-core kernels (refit to their own trace: a piece also pays the A build and
+// MMA round trip before its first row; the edge-row pieces run the CUDA-core LoG, about
+// as fast as the now shorter interior rows)
+constexpr double kPieceTC = 27.3;
+constexpr double kEdgePieceTC = 0.0;
+constexpr double kEdgeColTC = 1.066;
 constexpr double kEdgeColGen = 1.40; // column-edge group, general path
 constexpr double kPartialFloor = 0.55; // a column group with 1-2 working warps (see partial_floor; 0.45 / 0.6 / 1.0 measured)
 
@@ -81,7 +87,8 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool pair
     while (u < u1) {
         const int bg = (int)(u / R), r0 = (int)(u - (long long)bg * R), g = bg % G;
         const int n = (int)std::min<long long>(R - r0, u1 - u);
-        double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kEdgeCol) : 1.0;
+        const double kCol = fa.tc_model ? kEdgeColTC : kEdgeCol;
+        double f = (g == 0 || g == G - 1) ? ((fa.W & 3) ? kEdgeColGen : kCol) : 1.0;
         // a last column group where only one or two warps hold output columns (the
         // others only follow the ring) costs about a single warp's latency per row; with
         // more working warps the per-row time stays near a full group's (10 warps: 0.97,
@@ -96,7 +103,7 @@ double cost(const FusedArgs &fa, long long u0, long long u1, int halo, bool pair
             if (fa.o1 + halo > fa.H && ys < fa.H - kEdge && ye > fa.H - kEdge) ye = fa.H - kEdge;
             const bool edge = ys - halo < 0 || ye + halo > fa.H;
             const int rows = paired ? (ye - ys + 1) / 2 : ye - ys;
-            c += f * (rows + kPiece + (edge ? kEdgePiece : 0.0));
+            c += f * (rows + (fa.tc_model ? kPieceTC : kPiece) + (edge ? (fa.tc_model ? kEdgePieceTC : kEdgePiece) : 0.0));
             ys = ye;
         }
         u += n;
@@ -152,11 +159,11 @@ void weighted_partition(FusedArgs &fa, int grid, int halo)
 // strips of a host stream) reuse it.  A small per-thread table keyed by
 // everything the partition depends on.
 struct PartKey {
-    int W, H, o0, o1, nbands, cap, grid, halo, idle_walk;
+    int W, H, o0, o1, nbands, cap, grid, halo, idle_walk, tc_model;
     bool operator==(const PartKey &k) const
     {
         return W == k.W && H == k.H && o0 == k.o0 && o1 == k.o1 && nbands == k.nbands && cap == k.cap &&
-               grid == k.grid && halo == k.halo && idle_walk == k.idle_walk;
+               grid == k.grid && halo == k.halo && idle_walk == k.idle_walk && tc_model == k.tc_model;
     }
 };
 
@@ -170,7 +177,7 @@ void cached_partition(FusedArgs &fa, int grid, int halo)
     constexpr int kEntries = 8;
     static thread_local Entry table[kEntries];
     static thread_local int used = 0, next = 0;
-    const PartKey key{fa.W, fa.H, fa.o0, fa.o1, fa.nbands, fa.cap, grid, halo, fa.idle_walk};
+    const PartKey key{fa.W, fa.H, fa.o0, fa.o1, fa.nbands, fa.cap, grid, halo, fa.idle_walk, fa.tc_model};
     for (int i = 0; i < used; ++i)
         if (table[i].key == key) {
             fa.nb = table[i].nb;

@@ -104,6 +104,7 @@ struct FusedArgs {
     unsigned long long *dbg;  // optional per-CTA [start, end, items] globaltimer record (LFE_DEBUG_TIMING)
     int dbg_nofix;            // timing experiments only: never take the column-fix path (wrong borders)
     int idle_walk;            // partition: warps with no output column still walk the rows (TC, not TC12)
+    int tc_model;             // partition: the tensor-core kernels' cost constants
     // Peer-halo strips (lfe_extract_rows_peer): virtual rows [0, seg_a) are the rows
     // above (seg_base[0], pitch seg_pitch[0]), [seg_a, seg_b) the own rows (the tensor
     // map; own row = virtual row - seg_a; also seg_base[1]), [seg_b, H) the rows below
@@ -1878,6 +1879,7 @@ cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaS
     // protocol needs the group's 4 warps; a shadow walk would add ~1.4 k instructions to
     // the c3 kernel, measured 2.6% slower); TC12 and the CUDA-core kernels shadow / skip them
     fw.idle_walk = TC && !TC12 && IN16;
+    fw.tc_model = TC;
     cached_partition(fw, grid, halo_of(HML));
     static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
     FusedArgs fb = fw;

@@ -1879,7 +1879,7 @@ cudaError_t launch_t(const FusedArgs &fa, const Maps &maps, int *err_flag, cudaS
     // protocol needs the group's 4 warps; a shadow walk would add ~1.4 k instructions to
     // the c3 kernel, measured 2.6% slower); TC12 and the CUDA-core kernels shadow / skip them
     fw.idle_walk = TC && !TC12 && IN16;
-    fw.tc_model = TC;
+    fw.tc_model = TC && IN16;  // (fitted on the u16 kernels; c2's u8 TC kernel balances better with the old ones)
     cached_partition(fw, grid, halo_of(HML));
     static const char *dbg_path = getenv("LFE_DEBUG_TIMING");
     FusedArgs fb = fw;

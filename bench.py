@@ -236,8 +236,55 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+class NvmlSampler:
+    """SM clocks and clock-event (throttle) reasons polled through NVML every ~1 ms
+    by a background thread DURING the timed region (an in-process query: no
+    nvidia-smi start-up latency, so even a 16 ms region gets several samples)."""
+
+    def __init__(self, gpu_index: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.rows = []
+        self._run = False
+
+    def _poll(self):
+        nv = self.nv
+        while self._run:
+            self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                              nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            time.sleep(0.001)
+
+    def start(self):
+        self._run = True
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+        while not self.rows:  # the first sample is in before the timed region starts
+            time.sleep(0.0005)
+        self.rows.clear()
+
+    def stop(self):
+        self._run = False
+        self._t.join(1)
+        nv = self.nv
+        if not self.rows:  # a region shorter than the poll period (c1: ~1 ms): one sample at its end
+            self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                              nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({n for _, r in self.rows for n, b in bits.items() if r & b})
+        sm = [float(c) for c, _ in self.rows]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(sm), "source": "NVML, polled every 1 ms in the timed region"}
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (the
+    fallback when NVML is not importable)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -658,7 +705,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    clocks = ClockSampler(local)
+    try:
+        clocks = NvmlSampler(local)
+    except Exception:
+        clocks = ClockSampler(local)
     clocks.start()
     launches0 = ctx.launches
     stream = cur_stream()
